@@ -1,0 +1,149 @@
+/* dlvm.h -- C ABI of the B200-native DLVM hot path.
+ *
+ * What it computes: a straight-line DLVM IR function (§3.1.1
+ * L200-218, instruction set Table 1) and the gradient function the
+ * paper's AD pass generates from a gradient declaration (§3.1.3,
+ * Fig. 3): "The canonicalization process first copies basic blocks
+ * and instructions from the original function to the new function body, and
+ * then applies adjoint code generation" (L296).  A handle is the
+ * shape-specialised, "reified" callable of NNKit's JIT (§3.4):
+ * parse -> verify -> differentiate -> dead-code-eliminate -> plan fused
+ * sm_100a launches, once, at create time.
+ *
+ * Conventions (all entry points):
+ *  - No C++ exception crosses this boundary.  Every call returns a
+ *    dlvm_status; on failure dlvm_last_error() holds a thread-local message
+ *    "line:col: error: ..." (line/col 0 when not tied to the text).
+ *  - Tensors are dense, row-major, with `data` 16-byte aligned.  All device
+ *    memory (inputs, outputs, seed, workspace) is CALLER-OWNED (e.g. torch)
+ *    and must stay alive until the work queued on `cuda_stream` completes.
+ *    The library allocates no device memory and never synchronises the host
+ *    in dlvm_fn_run / dlvm_grad_run, so both are CUDA-graph capturable.
+ *  - A handle is not re-entrant (the workspace is shared): one handle per
+ *    stream.  Handles are immutable after create and may be destroyed from
+ *    any thread once their work has completed.
+ *  - Shapes are static (NNKit "shape-specialized DLVM IR"): tensors
+ *    passed to run must match the signature exactly (DLVM_ERR_USAGE).
+ */
+#ifndef DLVM_H_
+#define DLVM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; 0-4 mirror the exit codes of SPEC.md L557-559. */
+typedef enum {
+  DLVM_OK = 0,
+  DLVM_ERR_VERIFY = 1,      /* type/shape/gradient-declaration error (create) */
+  DLVM_ERR_PARSE = 2,       /* malformed IR text (create) */
+  DLVM_ERR_USAGE = 3,       /* bad arguments: arity, shape, dtype, NULL handle */
+  DLVM_ERR_RUNTIME = 4,     /* internal planner/executor failure */
+  DLVM_ERR_CUDA = 5,        /* a CUDA launch or driver call failed */
+  DLVM_ERR_UNSUPPORTED = 6  /* valid IR outside what the GPU path executes */
+} dlvm_status;
+
+/* Element types of caller tensors.  IR `bool` is stored one byte per element
+ * (0/1).  DLVM_BF16 is an execution-precision policy, not an IR type (reading
+ * A15 of SURVEY.md §8(c)): an f32 argument that feeds only `dot` may be
+ * passed as bf16 under DLVM_DOT_BF16, and an f32 output may be requested as
+ * bf16 (stored with round-to-nearest-even). */
+typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3 } dlvm_dtype;
+
+#define DLVM_MAX_RANK 8
+typedef struct {
+  void* data;                    /* device pointer (host pointer for dlvm_*_host) */
+  int32_t dtype;                 /* dlvm_dtype */
+  int32_t rank;                  /* 0..DLVM_MAX_RANK; 0 = scalar */
+  int64_t shape[DLVM_MAX_RANK];
+} dlvm_tensor;
+
+/* dot precision policy (reading A15) */
+#define DLVM_DOT_F32 0   /* exact fp32 operands, FFMA accumulation */
+#define DLVM_DOT_BF16 1  /* bf16 operands (RNE), fp32 accumulation in TMEM (tcgen05) */
+
+/* option flags */
+#define DLVM_PLAN_ONLY 0x1u      /* parse/verify/differentiate/plan only; no device calls */
+#define DLVM_NO_FUSION 0x2u      /* one launch group per instruction (testing) */
+#define DLVM_NO_SPECIALIZE 0x4u  /* always use the generic element-wise program interpreter */
+
+typedef struct {
+  int32_t dot_precision; /* DLVM_DOT_F32 | DLVM_DOT_BF16 */
+  int32_t device;        /* CUDA device ordinal the handle launches on */
+  uint32_t flags;        /* DLVM_PLAN_ONLY | DLVM_NO_FUSION | DLVM_NO_SPECIALIZE */
+} dlvm_options;
+
+typedef struct dlvm_fn_s* dlvm_fn;
+
+/* Which function of a handle. */
+#define DLVM_PRIMAL 0
+#define DLVM_GRADIENT 1
+
+/* Parse `module_text` (len bytes, need not be NUL-terminated), verify the
+ * whole module, and build a handle for function `fn_name` and, if
+ * `grad_name` is non-NULL, the gradient declaration of that name (which must
+ * be a `[gradient @fn_name ...]` declaration); with grad_name NULL the unique
+ * gradient declaration of fn_name is used if there is exactly one.
+ * Errors: DLVM_ERR_PARSE, DLVM_ERR_VERIFY (incl. non-differentiable),
+ * DLVM_ERR_UNSUPPORTED (e.g. f64/integer tensors on the GPU path),
+ * DLVM_ERR_USAGE (NULL pointers, unknown function names). `opts` may be NULL
+ * (defaults: DLVM_DOT_F32, device 0, no flags). */
+dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_name,
+                           const char* grad_name, const dlvm_options* opts, dlvm_fn* out);
+
+/* Inferred signature of the primal (which=0) or gradient (which=1) function.
+ * On entry *n_in / *n_out hold the capacity of in_types / out_types (either
+ * array may be NULL with capacity 0 to query counts); on exit they hold the
+ * counts.  Returned tensors have data=NULL and dtype DLVM_F32/DLVM_F64/
+ * DLVM_BOOL as typed in the IR.  Gradient outputs are ordered: gradients in
+ * `wrt` order, then `keeping` outputs (Fig. 3, Fig. 4). */
+dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_types, int* n_out,
+                              dlvm_tensor* out_types);
+
+/* Text of the typed primal (which=0), the generated gradient function after
+ * dead-code elimination (which=1) in the .dl syntax of Fig. 3, or the launch
+ * plan of the primal (2) / gradient (3).  Writes at most `cap` bytes
+ * including the NUL; *needed receives the full size including the NUL. */
+dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);
+
+/* Device workspace bytes dlvm_fn_run (which=0) / dlvm_grad_run (which=1)
+ * need; the caller passes a buffer at least this large (256-byte aligned). */
+dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes);
+
+/* Number of kernel launches one run (which=0) / grad run (which=1) issues. */
+dlvm_status dlvm_fn_num_launches(dlvm_fn fn, int which, int* launches);
+
+/* Execute the primal function on `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  in[n_in] / out[n_out] follow the signature. */
+dlvm_status dlvm_fn_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, dlvm_tensor* out, int n_out,
+                        void* workspace, void* cuda_stream);
+
+/* Execute the gradient function.  `in` holds the primal arguments; `seed`
+ * is non-NULL iff the declaration is `seedable` (it is the last parameter of
+ * the gradient function).  out[n_out]: gradients in `wrt` order, then kept
+ * outputs.  If `grad_ready_events` is non-NULL it points to n_grads
+ * cudaEvent_t (n_grads = number of `wrt` gradients), each recorded on
+ * `cuda_stream` as soon as that gradient is final -- a communication stream
+ * can wait on them to overlap a gradient all-reduce with the rest of the
+ * adjoint (data-parallel path). */
+dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlvm_tensor* seed,
+                          dlvm_tensor* out, int n_out, void* workspace, void* cuda_stream,
+                          void* const* grad_ready_events);
+
+/* Thread-local text of the last error on this thread ("" if none). */
+const char* dlvm_last_error(void);
+
+/* Release the host-side plan.  NULL is ignored. */
+void dlvm_fn_destroy(dlvm_fn fn);
+
+/* Library version string, e.g. "dlvm-b200 0.1 sm_100a". */
+const char* dlvm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DLVM_H_ */

@@ -1,0 +1,391 @@
+// C ABI (include/dlvm.h) and the run-time executor.
+//
+// dlvm_fn_create = the NNKit JIT phases of PAPER.md §3.4 L386-390 for one
+// shape-specialised function: parse (.dl text, Fig. 3 syntax) -> verify
+// (Fig. 2 "Analyses & Verification") -> differentiate the gradient
+// declaration by adjoint code generation (§3.1.3) -> dead-code
+// elimination (L304-305) -> plan fused sm_100a launches.  dlvm_fn_run /
+// dlvm_grad_run bind caller pointers and enqueue the planned launches on the
+// caller's stream: no allocation, no host synchronisation (graph-capturable).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <optional>
+#include <string>
+
+#include "../../include/dlvm.h"
+#include "ir.h"
+#include "kernels/kernels.h"
+#include "plan.h"
+
+using namespace dlvm;
+
+struct dlvm_fn_s {
+  Function primal;
+  std::optional<Function> grad;
+  Plan plan[2];
+  bool planned[2] = {false, false};
+  std::string plan_error[2];
+  dlvm_options opts{};
+  int n_grads = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+dlvm_status fail(dlvm_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+dlvm_status from_error(const Error& e) {
+  g_last_error = e.what();
+  return (dlvm_status)e.status;
+}
+
+void fill_sig(const Type& t, dlvm_tensor* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->data = nullptr;
+  out->dtype = t.dtype == DType::Bool ? DLVM_BOOL : t.dtype == DType::F64 ? DLVM_F64 : DLVM_F32;
+  out->rank = t.rank();
+  for (int i = 0; i < t.rank() && i < DLVM_MAX_RANK; ++i) out->shape[i] = t.shape[i];
+}
+
+bool shape_matches(const dlvm_tensor& t, const Type& ty) {
+  if (t.rank != ty.rank()) return false;
+  for (int i = 0; i < t.rank; ++i)
+    if (t.shape[i] != ty.shape[i]) return false;
+  return true;
+}
+
+SType stype_of(int32_t dt) { return dt == DLVM_BF16 ? SType::BF16 : dt == DLVM_BOOL ? SType::U8 : SType::F32; }
+
+struct Bound {
+  std::vector<void*> ptr;     // per BufferSlot
+  std::vector<uint8_t> st;    // runtime storage type per BufferSlot
+};
+
+void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->ndims = g.ndims;
+  p->vec = g.vec;
+  p->rpt = g.rpt;
+  for (int d = 0; d < kMaxIterDims; ++d) p->dims[d] = g.dims[d];
+  p->gx = g.gx;
+  p->gy = g.gy;
+  p->prog = g.prog;
+  for (size_t i = 0; i < g.inputs.size(); ++i) {
+    const IterRef& r = g.inputs[i];
+    EwDevIn& d = p->in[i];
+    if (r.buf < 0) continue;  // accumulator
+    const uint8_t st = b.st[r.buf];
+    size_t esz = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+    d.ptr = static_cast<const char*>(b.ptr[r.buf]) + r.offset * esz;
+    for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
+    d.nchunks = r.nchunks;
+    d.chunk_stride = r.chunk_stride;
+    d.st = st;
+  }
+  for (size_t i = 0; i < g.stores.size(); ++i) {
+    const IterRef& r = g.stores[i];
+    EwDevOut& d = p->out[i];
+    const uint8_t st = b.st[r.buf];
+    size_t esz = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+    d.ptr = static_cast<char*>(b.ptr[r.buf]) + r.offset * esz;
+    for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
+    d.st = st;
+  }
+  for (size_t i = 0; i < g.reduces.size(); ++i) p->red[i] = static_cast<float*>(b.ptr[g.reduces[i].buf]);
+}
+
+// epilogue vectorisation along n: every ref must allow 4-wide access
+int epi_vec(const EwParams& e) {
+  for (int i = 1; i < e.prog.n_in; ++i) {
+    const EwDevIn& r = e.in[i];
+    if (r.nchunks != 1) return 1;
+    if (r.s[1] != 0 && r.s[1] != 1) return 1;
+    if (r.s[1] == 1 && (r.s[0] % 4 || (reinterpret_cast<uintptr_t>(r.ptr) % 16))) return 1;
+  }
+  for (int i = 0; i < e.prog.n_stores; ++i) {
+    const EwDevOut& r = e.out[i];
+    if (r.s[1] != 1 || r.s[0] % 4 || (reinterpret_cast<uintptr_t>(r.ptr) % 16)) return 1;
+  }
+  return 4;
+}
+
+dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, const dlvm_tensor* seed,
+                    dlvm_tensor* out, int n_out, void* workspace, void* stream_v, void* const* events) {
+  if (!fn) return fail(DLVM_ERR_USAGE, "NULL handle");
+  if (fn->opts.flags & DLVM_PLAN_ONLY) return fail(DLVM_ERR_USAGE, "handle was created with DLVM_PLAN_ONLY");
+  if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
+  const Function& f = which ? *fn->grad : fn->primal;
+  const Plan& P = fn->plan[which];
+  if (n_in != P.n_inputs) return fail(DLVM_ERR_USAGE, "expected " + std::to_string(P.n_inputs) + " inputs");
+  if (n_out != P.n_outputs) return fail(DLVM_ERR_USAGE, "expected " + std::to_string(P.n_outputs) + " outputs");
+  if (n_in && !in) return fail(DLVM_ERR_USAGE, "NULL inputs");
+  if (n_out && !out) return fail(DLVM_ERR_USAGE, "NULL outputs");
+  if (P.seed_is_input && !seed) return fail(DLVM_ERR_USAGE, "seedable gradient needs a seed");
+  if (!P.seed_is_input && seed) return fail(DLVM_ERR_USAGE, "seed given for a non-seedable gradient");
+  if (P.workspace_bytes && !workspace) return fail(DLVM_ERR_USAGE, "NULL workspace");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(DLVM_ERR_USAGE, "workspace must be 256-byte aligned");
+  for (int i = 0; i < n_in; ++i) {
+    const Type& t = f.params[i];
+    if (!shape_matches(in[i], t)) return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " shape mismatch");
+    bool ok = t.dtype == DType::Bool ? in[i].dtype == DLVM_BOOL
+                                     : (in[i].dtype == DLVM_F32 || (in[i].dtype == DLVM_BF16 && P.input_feeds_only_dot[i]));
+    if (!ok) return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " dtype mismatch");
+    if (!in[i].data || reinterpret_cast<uintptr_t>(in[i].data) % 16)
+      return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " NULL or not 16-byte aligned");
+  }
+  if (seed) {
+    const Type& t = f.params.back();
+    if (!shape_matches(*seed, t) || seed->dtype != DLVM_F32 || !seed->data ||
+        reinterpret_cast<uintptr_t>(seed->data) % 16)
+      return fail(DLVM_ERR_USAGE, "seed must be f32, 16-byte aligned, of type " + t.str());
+  }
+  for (int i = 0; i < n_out; ++i) {
+    const Type& t = f.results[i];
+    if (!shape_matches(out[i], t)) return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " shape mismatch");
+    bool ok = t.dtype == DType::Bool ? out[i].dtype == DLVM_BOOL : (out[i].dtype == DLVM_F32 || out[i].dtype == DLVM_BF16);
+    if (!ok) return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " dtype mismatch");
+    if (!out[i].data || reinterpret_cast<uintptr_t>(out[i].data) % 16)
+      return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " NULL or not 16-byte aligned");
+  }
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  Bound b;
+  b.ptr.resize(P.bufs.size());
+  b.st.resize(P.bufs.size());
+  for (size_t k = 0; k < P.bufs.size(); ++k) {
+    const BufferSlot& s = P.bufs[k];
+    b.st[k] = (uint8_t)s.st;
+    switch (s.kind) {
+      case BufferSlot::Input:
+        b.ptr[k] = in[s.index].data;
+        b.st[k] = (uint8_t)stype_of(in[s.index].dtype);
+        break;
+      case BufferSlot::Output:
+        b.ptr[k] = out[s.index].data;
+        b.st[k] = (uint8_t)stype_of(out[s.index].dtype);
+        break;
+      case BufferSlot::Seed:
+        b.ptr[k] = seed->data;
+        break;
+      case BufferSlot::Work:
+        if (s.cast_of >= 0 && in[s.cast_of].dtype == DLVM_BF16)
+          b.ptr[k] = in[s.cast_of].data;
+        else
+          b.ptr[k] = static_cast<char*>(workspace) + s.offset;
+        break;
+    }
+  }
+  for (const Step& st : P.steps) {
+    cudaError_t e = cudaSuccess;
+    if (st.kind == Step::EW) {
+      EwParams p;
+      to_dev(st.ew, b, &p);
+      e = launch_ew(p, st.ew.bx, st.ew.by, stream);
+    } else if (st.kind == Step::GEMM) {
+      const GemmStep& g = st.gemm;
+      GemmParams gp;
+      std::memset(&gp, 0, sizeof(gp));
+      gp.M = g.M;
+      gp.N = g.N;
+      gp.K = g.K;
+      const uint8_t sta = b.st[g.a.buf], stb = b.st[g.b.buf];
+      size_t ea = sta == (uint8_t)SType::BF16 ? 2 : 4, eb = stb == (uint8_t)SType::BF16 ? 2 : 4;
+      gp.a = static_cast<const char*>(b.ptr[g.a.buf]) + g.a.offset * ea;
+      gp.b = static_cast<const char*>(b.ptr[g.b.buf]) + g.b.offset * eb;
+      gp.a_s0 = g.a.strides[0];
+      gp.a_s1 = g.a.strides[1];
+      gp.b_s0 = g.b.strides[0];
+      gp.b_s1 = g.b.strides[1];
+      gp.a_kmajor = g.a_kmajor;
+      gp.b_kmajor = g.b_kmajor;
+      gp.bf16 = sta == (uint8_t)SType::BF16;
+      if ((sta == (uint8_t)SType::BF16) != (stb == (uint8_t)SType::BF16))
+        return fail(DLVM_ERR_RUNTIME, "dot operands with different storage types");
+      gp.bm = g.bm;
+      gp.bn = g.bn;
+      to_dev(g.epi, b, &gp.epi);
+      gp.epi.vec = epi_vec(gp.epi);
+      bool aligned = (reinterpret_cast<uintptr_t>(gp.a) % 16 == 0) && (reinterpret_cast<uintptr_t>(gp.b) % 16 == 0);
+      if (g.tensor_core && aligned && gp.bf16)
+        e = launch_gemm_tc(gp, stream);
+      else {
+        if (g.tensor_core) return fail(DLVM_ERR_RUNTIME, "tensor-core dot operand misaligned");
+        e = launch_gemm_simt(gp, stream);
+      }
+    } else if (st.kind == Step::CAST) {
+      if (in[st.cast.input].dtype == DLVM_F32)
+        e = launch_cast_bf16(static_cast<const float*>(in[st.cast.input].data), b.ptr[st.cast.dst_buf],
+                             st.cast.numel, stream);
+    } else if (st.kind == Step::EVENT) {
+      if (events && events[st.event_index]) e = cudaEventRecord(static_cast<cudaEvent_t>(events[st.event_index]), stream);
+    }
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("CUDA error in '") + st.desc + "': " + cudaGetErrorString(e));
+  }
+  return DLVM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_name, const char* grad_name,
+                           const dlvm_options* opts, dlvm_fn* out) {
+  if (!module_text || !fn_name || !out) return fail(DLVM_ERR_USAGE, "NULL argument");
+  *out = nullptr;
+  dlvm_options o{};
+  o.dot_precision = DLVM_DOT_F32;
+  if (opts) o = *opts;
+  if (o.dot_precision != DLVM_DOT_F32 && o.dot_precision != DLVM_DOT_BF16)
+    return fail(DLVM_ERR_USAGE, "unknown dot precision");
+  try {
+    Module m = parse_module(std::string(module_text, len));
+    verify_module(m);
+    Function* src = m.find(fn_name);
+    if (!src) return fail(DLVM_ERR_USAGE, std::string("no function @") + fn_name);
+    if (!src->has_body) return fail(DLVM_ERR_USAGE, std::string("@") + fn_name + " has no body");
+    Function* decl = nullptr;
+    if (grad_name) {
+      decl = m.find(grad_name);
+      if (!decl || !decl->grad || decl->grad->source != fn_name)
+        return fail(DLVM_ERR_USAGE, std::string("@") + grad_name + " is not a gradient declaration of @" + fn_name);
+    } else {
+      int n = 0;
+      for (auto& g : m.fns)
+        if (g.grad && g.grad->source == fn_name) {
+          decl = &g;
+          ++n;
+        }
+      if (n > 1) decl = nullptr;
+    }
+    auto* h = new (std::nothrow) dlvm_fn_s;
+    if (!h) return fail(DLVM_ERR_RUNTIME, "out of host memory");
+    h->opts = o;
+    h->primal = *src;
+    if (decl) {
+      h->grad = differentiate(*src, *decl->grad, decl->name);
+      int nw = decl->grad->has_wrt ? (int)decl->grad->wrt.size() : src->num_args();
+      h->n_grads = nw;
+    }
+    for (int which = 0; which < 2; ++which) {
+      if (which == 1 && !h->grad) continue;
+      PlanOptions po;
+      po.policy = o.dot_precision == DLVM_DOT_BF16 ? Policy::BF16 : Policy::F32;
+      po.no_fusion = (o.flags & DLVM_NO_FUSION) != 0;
+      po.specialize = (o.flags & DLVM_NO_SPECIALIZE) == 0;
+      po.n_grads = which ? h->n_grads : 0;
+      try {
+        h->plan[which] = make_plan(which ? *h->grad : h->primal, po);
+        h->planned[which] = true;
+      } catch (const Error& e) {
+        h->plan_error[which] = e.what();
+        if (!(o.flags & DLVM_PLAN_ONLY)) {
+          dlvm_status st = from_error(e);
+          delete h;
+          return st;
+        }
+      }
+    }
+    *out = h;
+    return DLVM_OK;
+  } catch (const Error& e) {
+    return from_error(e);
+  } catch (const std::exception& e) {
+    return fail(DLVM_ERR_RUNTIME, std::string("internal error: ") + e.what());
+  } catch (...) {
+    return fail(DLVM_ERR_RUNTIME, "internal error");
+  }
+}
+
+dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_types, int* n_out,
+                              dlvm_tensor* out_types) {
+  if (!fn || !n_in || !n_out) return fail(DLVM_ERR_USAGE, "NULL argument");
+  if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+  if (which != 0 && which != 1) return fail(DLVM_ERR_USAGE, "which must be 0 or 1");
+  const Function& f = which ? *fn->grad : fn->primal;
+  int ci = *n_in, co = *n_out;
+  *n_in = (int)f.params.size();
+  *n_out = (int)f.results.size();
+  for (int i = 0; i < *n_in && i < ci && in_types; ++i) fill_sig(f.params[i], &in_types[i]);
+  for (int i = 0; i < *n_out && i < co && out_types; ++i) fill_sig(f.results[i], &out_types[i]);
+  return DLVM_OK;
+}
+
+dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed) {
+  if (!fn) return fail(DLVM_ERR_USAGE, "NULL handle");
+  std::string s;
+  try {
+    switch (which) {
+      case 0: s = print_function(fn->primal); break;
+      case 1:
+        if (!fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        s = print_function(*fn->grad);
+        break;
+      case 2:
+      case 3: {
+        int w = which - 2;
+        if (w == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        s = fn->planned[w] ? fn->plan[w].str() : "unsupported: " + fn->plan_error[w] + "\n";
+        break;
+      }
+      default:
+        return fail(DLVM_ERR_USAGE, "which must be 0..3");
+    }
+  } catch (const std::exception& e) {
+    return fail(DLVM_ERR_RUNTIME, e.what());
+  }
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return DLVM_OK;
+}
+
+dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes) {
+  if (!fn || !bytes) return fail(DLVM_ERR_USAGE, "NULL argument");
+  if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+  if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
+  *bytes = fn->plan[which].workspace_bytes;
+  return DLVM_OK;
+}
+
+dlvm_status dlvm_fn_num_launches(dlvm_fn fn, int which, int* launches) {
+  if (!fn || !launches) return fail(DLVM_ERR_USAGE, "NULL argument");
+  if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+  if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
+  *launches = fn->plan[which].launches();
+  return DLVM_OK;
+}
+
+dlvm_status dlvm_fn_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, dlvm_tensor* out, int n_out, void* workspace,
+                        void* cuda_stream) {
+  try {
+    return execute(fn, 0, in, n_in, nullptr, out, n_out, workspace, cuda_stream, nullptr);
+  } catch (const std::exception& e) {
+    return fail(DLVM_ERR_RUNTIME, e.what());
+  }
+}
+
+dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlvm_tensor* seed, dlvm_tensor* out,
+                          int n_out, void* workspace, void* cuda_stream, void* const* grad_ready_events) {
+  if (fn && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+  try {
+    return execute(fn, 1, in, n_in, seed, out, n_out, workspace, cuda_stream, grad_ready_events);
+  } catch (const std::exception& e) {
+    return fail(DLVM_ERR_RUNTIME, e.what());
+  }
+}
+
+const char* dlvm_last_error(void) { return g_last_error.c_str(); }
+
+void dlvm_fn_destroy(dlvm_fn fn) { delete fn; }
+
+const char* dlvm_version(void) { return "dlvm-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// Element-wise program kernel (K1/K2/K3/K7/K8 of SURVEY.md §2.5): one pass
+// over an [R, C] iteration space (R = product of up to three row dims)
+// evaluating a fused chain of the IR's element-wise ops with broadcasting
+// ("fuse compatible element-wise operators to a single
+// kernel"; P:L213 broadcasting), storing results and producing
+// deterministic per-CTA partial sums for `reduce` (Table 1):
+//   RED_COL  partial[blockIdx.y][c]          (sum over this CTA's rows)
+//   RED_ROW  partial[r][blockIdx.x]          (sum over this CTA's columns)
+//   RED_ALL  partial[blockIdx.y*gx + blockIdx.x]
+// A finalize launch (the same kernel over the partials, nchunks > 1) sums
+// partials in a fixed order.
+//
+// Thread layout: blockDim = (bx, by), bx*by = 256, bx a multiple of 32;
+// thread (tx, ty) owns VEC consecutive columns c = (blockIdx.x*bx + tx)*VEC
+// and rows r = (blockIdx.y*rpt + k)*by + ty, k < rpt.  With VEC = 4 every
+// full-stride operand moves as one 16-byte (f32) / 8-byte (bf16) / 4-byte
+// (bool) access per thread, coalesced across the warp.
+#include "ew_device.cuh"
+
+namespace dlvm {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParams p) {
+  const EwProgram& P = p.prog;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int bx = blockDim.x, by = blockDim.y;
+  const int nd = p.ndims;
+  const int64_t C = p.dims[nd - 1];
+  int64_t R = 1;
+  for (int d = 0; d < nd - 1; ++d) R *= p.dims[d];
+  const int64_t c = ((int64_t)blockIdx.x * bx + tx) * VEC;
+  const bool cval = c < C;
+  const int n_in = P.n_in;
+  float v[kMaxSlots][VEC];
+  for (int i = 0; i < P.n_lits; ++i)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) v[n_in + i][j] = P.lits[i];
+
+  bool has_row = false, has_colall = false;
+  for (int q = 0; q < P.n_reduces; ++q) {
+    has_row |= P.reduce_kind[q] == RED_ROW;
+    has_colall |= P.reduce_kind[q] != RED_ROW;
+  }
+  float acc[kMaxReduces][VEC];
+#pragma unroll
+  for (int q = 0; q < kMaxReduces; ++q)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[q][j] = 0.f;
+  __shared__ float red_s[256 * 4];
+  __shared__ float row_s[8][8];
+
+  for (int k = 0; k < p.rpt; ++k) {
+    const int64_t r = ((int64_t)blockIdx.y * p.rpt + k) * by + ty;
+    const bool valid = cval && r < R;
+    float rowv[kMaxReduces];
+#pragma unroll
+    for (int q = 0; q < kMaxReduces; ++q) rowv[q] = 0.f;
+    if (valid) {
+      int64_t idx[3] = {0, 0, 0};
+      int64_t rr = r;
+      for (int d = nd - 2; d >= 0; --d) {
+        idx[d] = rr % p.dims[d];
+        rr /= p.dims[d];
+      }
+      for (int i = 0; i < n_in; ++i) {
+        const EwDevIn& in = p.in[i];
+        int64_t off = c * in.s[nd - 1];
+        for (int d = 0; d < nd - 1; ++d) off += idx[d] * in.s[d];
+        vm_load<VEC>(in, off, in.s[nd - 1], v[i]);
+      }
+      vm_exec<VEC>(P, v);
+      for (int s = 0; s < P.n_stores; ++s) {
+        const EwDevOut& o = p.out[s];
+        int64_t off = c * o.s[nd - 1];
+        for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
+        vm_store<VEC>(o, off, o.s[nd - 1], v[P.store_slot[s]]);
+      }
+      for (int q = 0; q < P.n_reduces; ++q) {
+        const float* x = v[P.reduce_slot[q]];
+        if (P.reduce_kind[q] == RED_ROW) {
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) s = __fadd_rn(s, x[j]);
+          rowv[q] = s;
+        } else {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) acc[q][j] = __fadd_rn(acc[q][j], x[j]);
+        }
+      }
+    }
+    if (has_row) {  // block-uniform: every thread takes part
+      for (int q = 0; q < P.n_reduces; ++q) {
+        if (P.reduce_kind[q] != RED_ROW) continue;
+        float s = warp_sum(rowv[q]);
+        if ((tx & 31) == 0) row_s[ty][tx >> 5] = s;
+        __syncthreads();
+        if (tx == 0 && r < R) {
+          float t = 0.f;
+          for (int w = 0; w < (bx >> 5); ++w) t = __fadd_rn(t, row_s[ty][w]);
+          p.red[q][r * p.gx + blockIdx.x] = t;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (!has_colall) return;
+  for (int q = 0; q < P.n_reduces; ++q) {
+    const uint8_t kind = P.reduce_kind[q];
+    if (kind == RED_ROW) continue;
+    if (kind == RED_COL) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) red_s[(ty * bx + tx) * VEC + j] = acc[q][j];
+      __syncthreads();
+      if (ty == 0 && cval) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          float t = 0.f;
+          for (int y = 0; y < by; ++y) t = __fadd_rn(t, red_s[(y * bx + tx) * VEC + j]);
+          if (VEC == 1 || c + j < C) p.red[q][blockIdx.y * C + c + j] = t;
+        }
+      }
+      __syncthreads();
+    } else {  // RED_ALL
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) t = __fadd_rn(t, acc[q][j]);
+      t = warp_sum(t);
+      const int lin = ty * bx + tx;
+      if ((lin & 31) == 0) red_s[lin >> 5] = t;
+      __syncthreads();
+      if (lin == 0) {
+        float u = 0.f;
+        for (int w = 0; w < (bx * by) >> 5; ++w) u = __fadd_rn(u, red_s[w]);
+        p.red[q][blockIdx.y * p.gx + blockIdx.x] = u;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* __restrict__ dst, int64_t n) {
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (; i + 3 < n; i += stride) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(src + i));
+    uint2 o;
+    o.x = (unsigned)f2bf(x.x) | ((unsigned)f2bf(x.y) << 16);
+    o.y = (unsigned)f2bf(x.z) | ((unsigned)f2bf(x.w) << 16);
+    *reinterpret_cast<uint2*>(dst + i) = o;
+  }
+  for (; i < n; ++i) dst[i] = f2bf(src[i]);
+}
+
+}  // namespace
+
+cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
+  dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
+  if (p.vec == 4)
+    ew_kernel<4><<<grid, block, 0, stream>>>(p);
+  else
+    ew_kernel<1><<<grid, block, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream) {
+  int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
+  cast_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(src, reinterpret_cast<unsigned short*>(dst), n);
+  return cudaGetLastError();
+}
+
+}  // namespace dlvm

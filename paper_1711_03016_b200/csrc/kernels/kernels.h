@@ -1,0 +1,61 @@
+// Host-visible kernel parameter blocks and launchers (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ew_program.h"
+
+namespace dlvm {
+
+// one program input: element (i_0..i_{n-1}) at ptr + sum_d i_d * s[d]
+// (+ k * chunk_stride summed over k < nchunks for reduction partials)
+struct EwDevIn {
+  const void* ptr;
+  int64_t s[kMaxIterDims];
+  int64_t chunk_stride;
+  int32_t nchunks;
+  uint8_t st;  // SType
+};
+
+struct EwDevOut {
+  void* ptr;
+  int64_t s[kMaxIterDims];
+  uint8_t st;
+};
+
+struct EwParams {
+  int32_t ndims;
+  int32_t vec;     // 1 or 4 elements per thread along the column dim
+  int32_t rpt;     // rows per thread (EW kernel)
+  int64_t dims[kMaxIterDims];
+  int64_t gx, gy;  // grid (column tiles, row tiles)
+  EwProgram prog;
+  EwDevIn in[kMaxIn];
+  EwDevOut out[kMaxStores];
+  float* red[kMaxReduces];  // partial buffers
+};
+
+// element-wise program kernel over an [R, C] iteration space
+cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream);
+
+struct GemmParams {
+  int64_t M, N, K;
+  const void* a;  // bf16 or f32
+  const void* b;
+  int64_t a_s0, a_s1;  // A[m,k] at a + m*a_s0 + k*a_s1 (elements)
+  int64_t b_s0, b_s1;  // B[k,n] at b + k*b_s0 + n*b_s1
+  int32_t a_kmajor, b_kmajor;
+  int32_t bf16;        // operand element type: 1 bf16, 0 f32
+  int32_t bm, bn;      // tile; defines the epilogue partial layout
+  EwParams epi;        // ndims 2, dims {M, N}; slot 0 = accumulator
+};
+
+cudaError_t launch_gemm_simt(const GemmParams& p, cudaStream_t stream);
+cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream);
+bool gemm_tc_available();
+
+cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
+
+}  // namespace dlvm

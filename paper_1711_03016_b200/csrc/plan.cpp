@@ -1,0 +1,1363 @@
+// Launch planner (see plan.h).  Create-time only; host C++.
+//
+// Steps:
+//  1. peepholes: `subtract(1, multiply(tanh z, tanh z))` -> sech2(z)
+//     (reading A12: derivative closed forms evaluated from the
+//     pre-activation, cancellation-free in fp32); reduce(reduce(x, a), b)
+//     with a single-use inner reduce -> one multi-axis reduction.
+//  2. availability: every SSA value is an argument, a literal, inlined
+//     (recomputed in registers inside each kernel that needs it) or
+//     materialised (stored by the kernel that produces it).  `dot` and
+//     `reduce` results are always materialised; element-wise values are
+//     materialised when returned, used by a `dot`, or needed by two
+//     kernels; transpose / shapeCast / slice are views (strided refs, or
+//     index maps when inlined).
+//  3. regions: every materialised element-wise value and every reduction is
+//     a root; its region is the DAG of inlined values it needs.  Independent
+//     roots over the same iteration space merge into one kernel (P:L19,
+//     "fuse compatible element-wise operators to a single kernel").
+//  4. a kernel reading a `dot` result at the dot's own index space becomes
+//     that dot's GEMM epilogue ("Wx + b" fusion, B200 form: the
+//     bias/activation run on the accumulator tile instead of padding).
+//  5. schedule (program order, topological), lay out the workspace, emit
+//     reduction finalizes and gradient-ready events.
+#include "plan.h"
+
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
+namespace dlvm {
+
+bool TensorRef::contiguous() const {
+  int64_t s = 1;
+  for (int i = (int)shape.size() - 1; i >= 0; --i) {
+    if (shape[i] != 1 && strides[i] != s) return false;
+    s *= shape[i];
+  }
+  return nchunks == 1;
+}
+
+int Plan::launches() const {
+  int n = 0;
+  for (auto& s : steps) n += (s.kind == Step::EW || s.kind == Step::GEMM) ? 1 : 0;
+  return n;
+}
+
+std::string Plan::str() const {
+  std::ostringstream o;
+  o << "plan: " << steps.size() << " steps, " << launches() << " launches, workspace " << workspace_bytes
+    << " bytes\n";
+  for (size_t i = 0; i < steps.size(); ++i) o << "  [" << i << "] " << steps[i].desc << "\n";
+  return o.str();
+}
+
+namespace {
+
+std::vector<int64_t> contig_strides(const std::vector<int64_t>& shape) {
+  std::vector<int64_t> st(shape.size());
+  int64_t s = 1;
+  for (int i = (int)shape.size() - 1; i >= 0; --i) {
+    st[i] = s;
+    s *= shape[i];
+  }
+  return st;
+}
+size_t stype_size(SType t) { return t == SType::F32 ? 4 : t == SType::BF16 ? 2 : 1; }
+
+[[noreturn]] void unsupported(const std::string& m) { throw Error(kStatusUnsupported, 0, 0, m); }
+
+using Map = std::vector<int>;  // value dim -> iteration dim, or -1 (index 0)
+
+Map identity(int r) {
+  Map m(r);
+  for (int i = 0; i < r; ++i) m[i] = i;
+  return m;
+}
+bool is_identity(const std::vector<int>& p) {
+  for (size_t i = 0; i < p.size(); ++i)
+    if (p[i] != (int)i) return false;
+  return true;
+}
+
+struct Home {
+  int buf = -1;
+  SType st = SType::F32;
+  TensorRef ref;
+};
+
+struct VInfo {
+  int def = -1;            // defining instruction index, -1 for arguments
+  int arg = -1;            // argument index
+  std::vector<int> users;  // instruction indices
+  std::vector<int> outs;   // output indices returning this value
+  bool mat = false;        // element-wise/view value stored by its own root
+  bool inl = false;        // element-wise/view value recomputed in registers
+  bool dead = false;       // fused away (inner reduce of a chain)
+  bool dot_use = false;    // operand of a dot (through views)
+  bool group_use = false;  // read by an element-wise kernel
+  std::vector<Home> homes; // materialised copies
+  int out_home = -1;       // output index this value is produced into directly
+};
+
+struct Root {
+  enum Kind { Store, Reduce, Copy, Fill } kind = Store;
+  int v = -1;              // Store: value; Reduce: reduced operand x; Copy: source value
+  int red = -1;            // Reduce: the (outermost) reduce result value
+  uint8_t rkind = RED_ALL; // Reduce: kind in the node's iteration space
+  int out = -1;            // Copy / Fill: output index
+  double lit = 0;          // Fill
+  std::vector<int64_t> fill_shape;
+};
+
+struct Node {
+  bool is_dot = false;
+  int dot_inst = -1;
+  std::vector<int64_t> shape;  // iteration shape
+  std::vector<int> perm;       // iteration dim i <- reduced-operand dim perm[i] (reduce nodes)
+  int split = -1;              // number of row dims, -1 if free
+  std::vector<Root> roots;
+  std::set<int> reads, writes, inl;
+  std::set<int> nonident;      // values read at a non-identity index map
+  std::set<int> stored;        // element-wise values stored by this group's Store roots
+  int pos = 0;
+  int merged_into = -1;
+  int fused_epilogue = -1;     // dot: group fused as its epilogue
+  bool fused = false;          // group fused into a dot
+};
+
+struct RedInfo {
+  int value;
+  int slot_index;
+  uint8_t kind;
+};
+
+struct Planner {
+  Function f;
+  PlanOptions opt;
+  Plan plan;
+  std::vector<VInfo> vi;
+  std::vector<Node> nodes;
+  std::set<int> force_mat;
+  std::map<int, std::pair<int, std::vector<int>>> red_root;  // outer reduce -> (x, summed axes of x)
+  std::vector<int> node_of_value;
+  std::vector<std::set<int>> succ;
+  std::vector<int> cast_buf;
+
+  Planner(const Function& fn, const PlanOptions& o) : f(fn), opt(o) {}
+
+  const Type& ty(int v) const { return f.types[v]; }
+  const Inst* def(int v) const { return vi[v].def >= 0 ? &f.insts[vi[v].def] : nullptr; }
+  static bool is_view(const Inst* in) {
+    return in && (in->op == Op::Transpose || in->op == Op::ShapeCast || in->op == Op::Slice);
+  }
+  static bool is_ew(const Inst* in) {
+    return in && (is_elementwise(in->op) || in->op == Op::Sech2 || in->op == Op::DataTypeCast);
+  }
+  bool produced(int v) const {
+    const Inst* in = def(v);
+    if (!in || vi[v].dead) return false;
+    return in->op == Op::Dot || (in->op == Op::Reduce && red_root.count(v)) || vi[v].mat;
+  }
+  SType natural(int v) const { return ty(v).dtype == DType::Bool ? SType::U8 : SType::F32; }
+
+  // ---------------------------------------------------------------- checks
+  void check_supported() {
+    for (size_t i = 0; i < f.types.size(); ++i) {
+      DType d = f.types[i].dtype;
+      if (d != DType::F32 && d != DType::Bool)
+        unsupported("value %" + f.names[i] + " has type " + f.types[i].str() +
+                    "; the GPU path executes f32 and bool tensors");
+      if (f.types[i].rank() > kPlanDims) unsupported("rank > 8 tensors are not supported");
+    }
+    for (auto& in : f.insts) {
+      if (in.op == Op::Reduce && in.reduce_mul) unsupported("'reduce by multiply' is not supported on the GPU path");
+      if (in.op == Op::DataTypeCast && !((in.cast_to == DType::F32 || in.cast_to == DType::Bool)))
+        unsupported("dataTypeCast target");
+      for (auto& o : in.ops)
+        if (o.is_lit() && o.type.dtype != DType::F32 && o.type.dtype != DType::Bool)
+          unsupported("literal of type " + o.type.str());
+    }
+  }
+
+  // ------------------------------------------------------------- peepholes
+  void peepholes() {
+    std::vector<int> defidx(f.types.size(), -1);
+    for (size_t k = 0; k < f.insts.size(); ++k) defidx[f.insts[k].result] = (int)k;
+    for (auto& in : f.insts) {  // subtract(1, multiply(t, t)), t = tanh(z) -> sech2(z)
+      if (in.op != Op::Subtract || !in.ops[0].is_lit() || in.ops[0].lit != 1.0 || in.ops[1].is_lit()) continue;
+      int m = defidx[in.ops[1].value];
+      if (m < 0) continue;
+      const Inst& mi = f.insts[m];
+      if (mi.op != Op::Multiply || mi.ops[0].is_lit() || mi.ops[1].is_lit() || mi.ops[0].value != mi.ops[1].value)
+        continue;
+      int t = defidx[mi.ops[0].value];
+      if (t < 0 || f.insts[t].op != Op::Tanh) continue;
+      const Operand z = f.insts[t].ops[0];
+      if (z.is_lit() || f.types[z.value].shape != f.types[in.result].shape) continue;
+      in.op = Op::Sech2;
+      in.ops = {z};
+    }
+    dead_code_elim(f);
+  }
+
+  // ------------------------------------------------------------- analysis
+  void analyse() {
+    vi.assign(f.types.size(), VInfo{});
+    for (int i = 0; i < f.num_args(); ++i) vi[i].arg = i;
+    for (size_t k = 0; k < f.insts.size(); ++k) {
+      const Inst& in = f.insts[k];
+      vi[in.result].def = (int)k;
+      for (auto& o : in.ops)
+        if (!o.is_lit()) vi[o.value].users.push_back((int)k);
+    }
+    for (size_t k = 0; k < f.ret.size(); ++k)
+      if (!f.ret[k].is_lit()) vi[f.ret[k].value].outs.push_back((int)k);
+    for (auto& in : f.insts) {
+      if (in.op != Op::Dot) continue;
+      for (auto& o : in.ops) {
+        if (o.is_lit()) continue;
+        int v = o.value;
+        vi[v].dot_use = true;
+        while (is_view(def(v))) {
+          v = def(v)->ops[0].value;
+          vi[v].dot_use = true;
+        }
+      }
+    }
+  }
+
+  void reduce_chains() {
+    for (auto& in : f.insts) {
+      if (in.op != Op::Reduce) continue;
+      if (in.ops[0].is_lit()) unsupported("reduce of a literal");
+      int x = in.ops[0].value;
+      auto it = red_root.find(x);
+      if (it != red_root.end() && vi[x].users.size() == 1 && vi[x].outs.empty()) {
+        auto [x0, ax0] = it->second;
+        std::vector<int> keep;
+        for (int d = 0; d < ty(x0).rank(); ++d)
+          if (std::find(ax0.begin(), ax0.end(), d) == ax0.end()) keep.push_back(d);
+        std::vector<int> ax = ax0;
+        ax.push_back(keep[in.axis]);
+        std::sort(ax.begin(), ax.end());
+        red_root.erase(it);
+        vi[x].dead = true;
+        red_root[in.result] = {x0, ax};
+      } else {
+        red_root[in.result] = {x, {in.axis}};
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ index maps
+  Map bcast_map(const std::vector<int64_t>& sa, const std::vector<int64_t>& su, const Map& mu) const {
+    Map ma(sa.size(), -1);
+    size_t off = su.size() - sa.size();
+    for (size_t j = 0; j < sa.size(); ++j) ma[j] = (sa[j] == 1) ? -1 : mu[j + off];
+    return ma;
+  }
+  // index map through a view (result map mu -> source map)
+  bool view_map(const Inst& in, const Map& mu, Map* ma) const {
+    const auto& sa = ty(in.ops[0].value).shape;
+    const auto& su = ty(in.result).shape;
+    if (in.op == Op::Transpose) {
+      ma->assign(sa.size(), -1);
+      for (size_t j = 0; j < sa.size(); ++j) (*ma)[j] = mu[sa.size() - 1 - j];
+      return true;
+    }
+    if (in.op == Op::ShapeCast) {
+      std::vector<int> nu, na;
+      for (size_t j = 0; j < su.size(); ++j)
+        if (su[j] != 1) nu.push_back((int)j);
+      for (size_t j = 0; j < sa.size(); ++j)
+        if (sa[j] != 1) na.push_back((int)j);
+      if (nu.size() != na.size()) return false;
+      for (size_t k = 0; k < nu.size(); ++k)
+        if (su[nu[k]] != sa[na[k]]) return false;
+      ma->assign(sa.size(), -1);
+      for (size_t k = 0; k < na.size(); ++k) (*ma)[na[k]] = mu[nu[k]];
+      return true;
+    }
+    return false;
+  }
+  bool composable(const Inst& in) const {
+    Map m;
+    return in.op != Op::Slice && view_map(in, identity(ty(in.result).rank()), &m);
+  }
+  // strided view of a materialised source
+  bool view_ref(const Inst& in, const TensorRef& src, TensorRef* out) const {
+    *out = src;
+    const auto& su = ty(in.result).shape;
+    if (in.op == Op::Transpose) {
+      std::reverse(out->shape.begin(), out->shape.end());
+      std::reverse(out->strides.begin(), out->strides.end());
+      return true;
+    }
+    if (in.op == Op::Slice) {
+      out->offset += in.from * src.strides[0];
+      out->shape[0] = in.upto - in.from;
+      return true;
+    }
+    if (src.contiguous()) {
+      out->shape = su;
+      out->strides = contig_strides(su);
+      return true;
+    }
+    Map m;
+    if (!view_map(in, identity((int)su.size()), &m)) return false;
+    out->shape = su;
+    out->strides.assign(su.size(), 0);
+    for (size_t j = 0; j < m.size(); ++j)
+      if (m[j] >= 0) out->strides[m[j]] = src.strides[j];
+    return true;
+  }
+  // would the materialised ref of view value v be expressible?
+  bool structurally_contiguous(int v) const {
+    const Inst* in = def(v);
+    if (!in || !is_view(in) || !vi[v].inl) return true;
+    int src = in->ops[0].value;
+    if (in->op == Op::Transpose) {
+      int nonunit = 0;
+      for (auto d : ty(v).shape) nonunit += d != 1;
+      return nonunit <= 1 && structurally_contiguous(src);
+    }
+    if (in->op == Op::Slice) return structurally_contiguous(src);
+    return structurally_contiguous(src);
+  }
+
+  // -------------------------------------------------------- availability
+  void decide() {
+    for (size_t v = 0; v < f.types.size(); ++v) {
+      VInfo& x = vi[v];
+      x.mat = x.inl = false;
+      const Inst* in = def((int)v);
+      if (!in || x.dead) continue;
+      if (is_ew(in)) {
+        x.mat = !x.outs.empty() || x.dot_use || force_mat.count((int)v) || opt.no_fusion;
+        x.inl = !x.mat;
+      } else if (is_view(in)) {
+        x.mat = force_mat.count((int)v) > 0;
+        x.inl = !x.mat;
+      }
+    }
+  }
+
+  // outputs produced in place by their producer (no copy kernel)
+  void alias_outputs() {
+    for (auto& x : vi) x.out_home = -1;
+    std::set<int> used;
+    for (size_t k = 0; k < f.ret.size(); ++k) {
+      const Operand& o = f.ret[k];
+      if (o.is_lit()) continue;
+      int v = o.value;
+      if (used.count(v) || vi[v].arg >= 0) continue;
+      // follow single-use contiguous shapeCast views back to their producer
+      std::vector<int> chain{v};
+      int u = v;
+      while (vi[u].inl && def(u) && def(u)->op == Op::ShapeCast) {
+        int s = def(u)->ops[0].value;
+        if (vi[s].users.size() != 1 || !vi[s].outs.empty() || vi[s].arg >= 0) break;
+        chain.push_back(s);
+        u = s;
+      }
+      if (!produced(u) || used.count(u)) continue;
+      if (ty(u).dtype != ty(v).dtype) continue;
+      for (int c : chain) {
+        vi[c].out_home = (int)k;
+        used.insert(c);
+      }
+    }
+  }
+
+  // ----------------------------------------------------------- the nodes
+  bool need_iterate = false;
+  void build_nodes() {
+    nodes.clear();
+    node_of_value.assign(f.types.size(), -1);
+    for (size_t k = 0; k < f.insts.size(); ++k) {
+      const Inst& in = f.insts[k];
+      int v = in.result;
+      if (vi[v].dead) continue;
+      Node n;
+      n.pos = (int)k;
+      n.writes.insert(v);
+      if (in.op == Op::Dot) {
+        n.is_dot = true;
+        n.dot_inst = (int)k;
+      } else if (in.op == Op::Reduce && red_root.count(v)) {
+        auto [x, axes] = red_root[v];
+        const auto& sx = ty(x).shape;
+        int rk = (int)sx.size();
+        Root r;
+        r.kind = Root::Reduce;
+        r.v = x;
+        r.red = v;
+        bool leading = true;
+        for (size_t i = 0; i < axes.size(); ++i) leading &= axes[i] == (int)i;
+        if ((int)axes.size() == rk) {
+          n.perm = identity(rk);
+          r.rkind = RED_ALL;
+        } else if (leading) {
+          n.perm = identity(rk);
+          n.split = (int)axes.size();
+          r.rkind = RED_COL;
+        } else {
+          for (int d = 0; d < rk; ++d)
+            if (std::find(axes.begin(), axes.end(), d) == axes.end()) n.perm.push_back(d);
+          n.split = (int)n.perm.size();
+          for (int d : axes) n.perm.push_back(d);
+          r.rkind = RED_ROW;
+        }
+        for (int d : n.perm) n.shape.push_back(sx[d]);
+        n.roots.push_back(r);
+      } else if (vi[v].mat) {
+        Root r;
+        r.kind = Root::Store;
+        r.v = v;
+        n.roots.push_back(r);
+        n.shape = ty(v).shape;
+        n.perm = identity(ty(v).rank());
+      } else {
+        continue;
+      }
+      nodes.push_back(n);
+      node_of_value[v] = (int)nodes.size() - 1;
+    }
+    for (size_t k = 0; k < f.ret.size(); ++k) {
+      const Operand& o = f.ret[k];
+      Node n;
+      Root r;
+      n.pos = (int)f.insts.size() + (int)k;
+      if (o.is_lit()) {
+        r.kind = Root::Fill;
+        r.out = (int)k;
+        r.lit = o.lit;
+        r.fill_shape = o.type.shape;
+        n.shape = o.type.shape;
+      } else {
+        if (vi[o.value].out_home == (int)k) continue;  // produced in place
+        r.kind = Root::Copy;
+        r.v = o.value;
+        r.out = (int)k;
+        n.shape = ty(o.value).shape;
+      }
+      n.perm = identity((int)n.shape.size());
+      n.roots.push_back(r);
+      nodes.push_back(n);
+    }
+  }
+
+  int base_of(int v) const {  // materialised value behind a chain of inlined views
+    while (vi[v].inl && is_view(def(v))) v = def(v)->ops[0].value;
+    return v;
+  }
+
+  void region_of(Node& n) {
+    n.reads.clear();
+    n.inl.clear();
+    n.nonident.clear();
+    n.stored.clear();
+    if (n.is_dot) {
+      for (auto& o : f.insts[n.dot_inst].ops)
+        if (!o.is_lit()) {
+          n.reads.insert(base_of(o.value));
+          n.nonident.insert(base_of(o.value));
+        }
+      return;
+    }
+    const int rk = (int)n.shape.size();
+    std::function<void(int, const Map&)> walk = [&](int v, const Map& m) {
+      if (vi[v].arg >= 0 || !vi[v].inl) {
+        n.reads.insert(v);
+        if (!((int)m.size() == rk && is_identity(m) && ty(v).shape == n.shape)) n.nonident.insert(v);
+        return;
+      }
+      const Inst* in = def(v);
+      n.inl.insert(v);
+      if (is_view(in)) {
+        int src = in->ops[0].value;
+        Map ma;
+        if (in->op != Op::Slice && view_map(*in, m, &ma)) {
+          walk(src, ma);
+        } else {
+          if (vi[src].inl) {
+            force_mat.insert(src);
+            need_iterate = true;
+          }
+          n.reads.insert(base_of(src));
+          n.nonident.insert(base_of(src));
+        }
+        return;
+      }
+      const auto& su = ty(v).shape;
+      for (auto& o : in->ops)
+        if (!o.is_lit()) walk(o.value, bcast_map(ty(o.value).shape, su, m));
+    };
+    for (auto& r : n.roots) {
+      if (r.kind == Root::Fill) continue;
+      if (r.kind == Root::Store) {
+        n.stored.insert(r.v);
+        const Inst* in = def(r.v);
+        const auto& su = ty(r.v).shape;
+        Map id = identity(ty(r.v).rank());
+        if (is_view(in)) {  // forced view copy: reads its source through the view
+          int src = in->ops[0].value;
+          Map ma;
+          if (in->op != Op::Slice && view_map(*in, id, &ma)) {
+            walk(src, ma);
+          } else {
+            n.reads.insert(base_of(src));
+            n.nonident.insert(base_of(src));
+          }
+          continue;
+        }
+        for (auto& o : in->ops)
+          if (!o.is_lit()) walk(o.value, bcast_map(ty(o.value).shape, su, id));
+      } else if (r.kind == Root::Reduce) {
+        Map mx(ty(r.v).rank(), -1);
+        for (size_t i = 0; i < n.perm.size(); ++i) mx[n.perm[i]] = (int)i;
+        walk(r.v, mx);
+      } else {
+        walk(r.v, identity(ty(r.v).rank()));
+      }
+    }
+  }
+
+  int find(int a) const {
+    while (nodes[a].merged_into >= 0) a = nodes[a].merged_into;
+    return a;
+  }
+  void build_edges() {
+    std::map<int, int> writer;
+    for (size_t i = 0; i < nodes.size(); ++i)
+      for (int v : nodes[i].writes) writer[v] = (int)i;
+    succ.assign(nodes.size(), {});
+    for (size_t i = 0; i < nodes.size(); ++i)
+      for (int v : nodes[i].reads) {
+        auto it = writer.find(v);
+        if (it != writer.end() && it->second != (int)i) succ[it->second].insert((int)i);
+      }
+  }
+  // is there a dependency path from group `from` to group `to` (merged view)?
+  // With skip_direct, the direct edges from -> to are ignored (they are
+  // satisfied in registers when the two merge).
+  bool reaches(int from, int to, bool skip_direct = false) const {
+    from = find(from);
+    to = find(to);
+    std::vector<char> seen(nodes.size(), 0);
+    std::vector<int> st{from};
+    seen[from] = 1;
+    while (!st.empty()) {
+      int a = st.back();
+      st.pop_back();
+      for (size_t i = 0; i < nodes.size(); ++i) {
+        if (find((int)i) != a) continue;
+        for (int b : succ[i]) {
+          int g = find(b);
+          if (g == a) continue;
+          if (g == to) {
+            if (skip_direct && a == from) continue;
+            return true;
+          }
+          if (!seen[g]) {
+            seen[g] = 1;
+            st.push_back(g);
+          }
+        }
+      }
+    }
+    return false;
+  }
+
+  void merge_groups() {
+    if (opt.no_fusion) return;
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      Node& a = nodes[i];
+      if (a.is_dot) continue;
+      for (size_t j = 0; j < i; ++j) {
+        Node& g = nodes[j];
+        if (g.is_dot || g.merged_into >= 0) continue;
+        if (g.shape != a.shape || g.perm != a.perm) continue;
+        if (a.split >= 0 && g.split >= 0 && a.split != g.split) continue;
+        if (g.roots.size() + a.roots.size() > (size_t)kMaxStores) continue;
+        if (reaches((int)i, (int)j)) continue;
+        // direct dependencies are allowed when `a` only reads values that `g`
+        // stores, element for element (identity map): they stay in registers
+        bool direct_ok = true, direct = false;
+        for (int v : a.reads) {
+          bool written_by_g = false;
+          for (size_t k = 0; k < nodes.size(); ++k)
+            if (find((int)k) == (int)j && nodes[k].writes.count(v)) written_by_g = true;
+          if (!written_by_g) continue;
+          direct = true;
+          if (!g.stored.count(v) || a.nonident.count(v) || !is_ew(def(v))) direct_ok = false;
+        }
+        if (direct && !direct_ok) continue;
+        if (reaches((int)j, (int)i, direct)) continue;
+        a.merged_into = (int)j;
+        for (auto& r : a.roots) g.roots.push_back(r);
+        g.reads.insert(a.reads.begin(), a.reads.end());
+        g.writes.insert(a.writes.begin(), a.writes.end());
+        g.inl.insert(a.inl.begin(), a.inl.end());
+        g.nonident.insert(a.nonident.begin(), a.nonident.end());
+        g.stored.insert(a.stored.begin(), a.stored.end());
+        g.pos = std::max(g.pos, a.pos);
+        g.split = std::max(g.split, a.split);
+        break;
+      }
+    }
+  }
+
+  // an inlined element-wise value computed by two kernels is materialised,
+  // unless it is a small broadcast value (cheaper to recompute)
+  bool duplicates() {
+    std::map<int, std::set<int>> where;
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      if (nodes[i].merged_into >= 0 || nodes[i].is_dot) continue;
+      for (int v : nodes[i].inl) where[v].insert((int)i);
+    }
+    // materialise one value per round, the latest in program order (closest
+    // to its consumers), so that its producers can stay inlined
+    int pick = -1;
+    for (auto& [v, gs] : where) {
+      if (gs.size() < 2 || !is_ew(def(v)) || force_mat.count(v)) continue;
+      int64_t big = 0;
+      for (int g : gs) {
+        int64_t n = 1;
+        for (auto d : nodes[g].shape) n *= d;
+        big = std::max(big, n);
+      }
+      if (ty(v).numel() * 16 <= big) continue;
+      if (pick < 0 || vi[v].def > vi[pick].def) pick = v;
+    }
+    if (pick < 0) return false;
+    force_mat.insert(pick);
+    return true;
+  }
+
+  void fuse_epilogues() {
+    if (opt.no_fusion) return;
+    for (size_t d = 0; d < nodes.size(); ++d) {
+      if (!nodes[d].is_dot) continue;
+      int dv = f.insts[nodes[d].dot_inst].result;
+      for (size_t g = 0; g < nodes.size(); ++g) {
+        Node& G = nodes[g];
+        if (G.is_dot || G.merged_into >= 0 || G.fused || !G.reads.count(dv)) continue;
+        if (G.shape != ty(dv).shape || !is_identity(G.perm) || !(G.split < 0 || G.split == 1)) break;
+        bool via_view = false;
+        for (int v : G.inl)
+          if (is_view(def(v)) && def(v)->ops[0].value == dv) via_view = true;
+        if (via_view) break;
+        bool ok = true;
+        for (int v : G.reads) {
+          if (v == dv) continue;
+          int p = node_of_value[v];
+          if (p < 0 || find(p) == (int)g) continue;  // argument, or stored by G itself
+          if (find(p) == (int)d || reaches((int)d, p)) ok = false;
+        }
+        if (ok) {
+          nodes[d].fused_epilogue = (int)g;
+          G.fused = true;
+        }
+        break;
+      }
+    }
+  }
+
+  // ----------------------------------------------------------- buffers
+  int add_buf(BufferSlot::Kind k, int index, size_t bytes, SType st) {
+    BufferSlot b;
+    b.kind = k;
+    b.index = index;
+    b.bytes = bytes;
+    b.st = st;
+    if (k == BufferSlot::Work) {
+      plan.workspace_bytes = (plan.workspace_bytes + 255) / 256 * 256;
+      b.offset = plan.workspace_bytes;
+      plan.workspace_bytes += bytes;
+    }
+    plan.bufs.push_back(b);
+    return (int)plan.bufs.size() - 1;
+  }
+  Home make_home(int buf, int v, SType st) {
+    Home h;
+    h.buf = buf;
+    h.st = st;
+    h.ref.buf = buf;
+    h.ref.shape = ty(v).shape;
+    h.ref.strides = contig_strides(ty(v).shape);
+    h.ref.st = st;
+    return h;
+  }
+  int output_buf(int k) const {
+    for (size_t b = 0; b < plan.bufs.size(); ++b)
+      if (plan.bufs[b].kind == BufferSlot::Output && plan.bufs[b].index == k) return (int)b;
+    return -1;
+  }
+
+  void assign_homes() {
+    plan.bufs.clear();
+    plan.workspace_bytes = 0;
+    // group_use: read by a (non-dot) kernel, through views
+    for (auto& n : nodes) {
+      if (n.is_dot || n.merged_into >= 0) continue;
+      for (int v : n.reads) vi[v].group_use = true;
+    }
+    for (int i = 0; i < f.num_args(); ++i) {
+      bool seed = plan.seed_is_input && i == f.num_args() - 1;
+      int b = add_buf(seed ? BufferSlot::Seed : BufferSlot::Input, seed ? 0 : i,
+                      ty(i).numel() * stype_size(natural(i)), natural(i));
+      vi[i].homes.push_back(make_home(b, i, natural(i)));
+    }
+    for (size_t k = 0; k < f.ret.size(); ++k) {
+      SType st = f.results[k].dtype == DType::Bool ? SType::U8 : SType::F32;
+      add_buf(BufferSlot::Output, (int)k, f.results[k].numel() * stype_size(st), st);
+    }
+    std::map<int, int> fused_dot_group;  // dot value -> fused group node
+    for (auto& n : nodes)
+      if (n.is_dot && n.fused_epilogue >= 0) fused_dot_group[f.insts[n.dot_inst].result] = n.fused_epilogue;
+    for (size_t v = 0; v < f.types.size(); ++v) {
+      VInfo& x = vi[v];
+      if (!produced((int)v)) continue;
+      bool is_dot = def((int)v)->op == Op::Dot;
+      bool others_read = false;
+      if (is_dot && fused_dot_group.count((int)v)) {
+        int g = fused_dot_group[(int)v];
+        for (size_t i = 0; i < nodes.size(); ++i)
+          if (!nodes[i].is_dot && nodes[i].merged_into < 0 && (int)i != g && nodes[i].reads.count((int)v))
+            others_read = true;
+      } else {
+        others_read = x.group_use;
+      }
+      bool need32 = others_read || !x.outs.empty() || x.out_home >= 0 ||
+                    (x.dot_use && opt.policy == Policy::F32);
+      if (x.out_home >= 0) {
+        x.homes.push_back(make_home(output_buf(x.out_home), (int)v,
+                                    ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
+      } else if (need32) {
+        int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * stype_size(natural((int)v)), natural((int)v));
+        x.homes.push_back(make_home(b, (int)v, natural((int)v)));
+      }
+      if (x.dot_use && opt.policy == Policy::BF16) {
+        int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * 2, SType::BF16);
+        x.homes.push_back(make_home(b, (int)v, SType::BF16));
+      }
+      if (x.homes.empty() && !(is_dot && fused_dot_group.count((int)v))) {
+        int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * stype_size(natural((int)v)), natural((int)v));
+        x.homes.push_back(make_home(b, (int)v, natural((int)v)));
+      }
+    }
+    cast_buf.assign(f.num_args(), -1);
+    plan.input_feeds_only_dot.assign(f.num_args(), 0);
+    if (opt.policy == Policy::BF16) {
+      for (int i = 0; i < f.num_args(); ++i) {
+        if (!vi[i].dot_use || ty(i).dtype != DType::F32) continue;
+        int b = add_buf(BufferSlot::Work, -1, ty(i).numel() * 2, SType::BF16);
+        plan.bufs[b].cast_of = i;
+        cast_buf[i] = b;
+        vi[i].homes.push_back(make_home(b, i, SType::BF16));
+        plan.input_feeds_only_dot[i] = (vi[i].group_use || !vi[i].outs.empty()) ? 0 : 1;
+      }
+    }
+  }
+
+  // materialised ref of value v (through views), preferring bf16 or not
+  bool ref_of(int v, bool want_bf16, TensorRef* out) {
+    const Inst* in = def(v);
+    if (vi[v].inl && is_view(in)) {
+      TensorRef src;
+      if (!ref_of(in->ops[0].value, want_bf16, &src)) return false;
+      return view_ref(*in, src, out);
+    }
+    const auto& hs = vi[v].homes;
+    if (hs.empty()) return false;
+    const Home* pick = &hs[0];
+    for (auto& h : hs)
+      if ((h.st == SType::BF16) == want_bf16) {
+        pick = &h;
+        break;
+      }
+    *out = pick->ref;
+    return true;
+  }
+
+  // ----------------------------------------------------- program building
+  struct ProgBuilder {
+    Planner& P;
+    int acc_value = -1;
+    std::set<int> stored;            // element-wise values this group stores (computed in registers)
+    std::vector<int64_t> shape;      // iteration shape
+    std::map<std::pair<int, Map>, int> memo;
+    std::vector<float> lits;
+    std::vector<EwIns> ins;
+    std::vector<std::array<int, 3>> raw;
+    std::vector<IterRef> inputs;
+    explicit ProgBuilder(Planner& p) : P(p) {}
+
+    int lit(float v) {
+      for (size_t i = 0; i < lits.size(); ++i)
+        if (lits[i] == v) return 100 + (int)i;
+      if ((int)lits.size() >= kMaxLits) unsupported("too many literals in one fused kernel");
+      lits.push_back(v);
+      return 100 + (int)lits.size() - 1;
+    }
+    int input(const TensorRef& r, const Map& m) {
+      IterRef it;
+      it.buf = r.buf;
+      it.offset = r.offset;
+      it.nchunks = r.nchunks;
+      it.chunk_stride = r.chunk_stride;
+      it.st = r.st;
+      for (size_t j = 0; j < m.size(); ++j)
+        if (m[j] >= 0) it.strides[m[j]] += r.strides[j];
+      for (size_t i = 0; i < inputs.size(); ++i) {
+        const IterRef& o = inputs[i];
+        bool same = o.buf == it.buf && o.offset == it.offset && o.st == it.st && o.nchunks == it.nchunks;
+        for (int d = 0; d < kPlanDims && same; ++d) same = o.strides[d] == it.strides[d];
+        if (same) return (int)i;
+      }
+      if ((int)inputs.size() >= kMaxIn) unsupported("too many inputs in one fused kernel");
+      inputs.push_back(it);
+      return (int)inputs.size() - 1;
+    }
+    int emit(uint8_t op, int a, int b, int c) {
+      if ((int)ins.size() >= kMaxIns) unsupported("fused kernel program too long");
+      ins.push_back(EwIns{op, 0, 0, 0});
+      raw.push_back({a, b, c});
+      return 200 + (int)ins.size() - 1;
+    }
+    int operand(const Operand& o, const std::vector<int64_t>& su, const Map& mu) {
+      if (o.is_lit()) return lit((float)o.lit);
+      return node(o.value, P.bcast_map(P.ty(o.value).shape, su, mu));
+    }
+    int node(int v, const Map& m) {
+      auto key = std::make_pair(v, m);
+      auto it = memo.find(key);
+      if (it != memo.end()) return it->second;
+      int s = compute(v, m, false);
+      memo[key] = s;
+      return s;
+    }
+    // force: compute a root's own value even though it is materialised
+    int compute(int v, const Map& m, bool force) {
+      const Inst* in = P.def(v);
+      const VInfo& x = P.vi[v];
+      if (!force && stored.count(v) && is_identity(m) && P.ty(v).shape == shape && is_ew(in)) force = true;
+      bool inline_it = in && x.arg < 0 && (x.inl || force);
+      if (inline_it && is_view(in)) {
+        int src = in->ops[0].value;
+        Map ma;
+        if (P.vi[src].inl && P.view_map(*in, m, &ma)) return node(src, ma);
+        TensorRef sr, r;
+        if (!P.ref_of(src, false, &sr) || !P.view_ref(*in, sr, &r))
+          unsupported("cannot address view %" + P.f.names[v]);
+        return input(r, m);
+      }
+      if (inline_it && is_ew(in)) {
+        const auto& su = P.ty(v).shape;
+        uint8_t op;
+        switch (in->op) {
+          case Op::Negate: op = VM_NEG; break;
+          case Op::Tanh: op = VM_TANH; break;
+          case Op::Exp: op = VM_EXP; break;
+          case Op::Log: op = VM_LOG; break;
+          case Op::Sqrt: op = VM_SQRT; break;
+          case Op::Abs: op = VM_ABS; break;
+          case Op::Sign: op = VM_SIGN; break;
+          case Op::Add: op = VM_ADD; break;
+          case Op::Subtract: op = VM_SUB; break;
+          case Op::Multiply: op = VM_MUL; break;
+          case Op::Divide: op = VM_DIV; break;
+          case Op::Power: op = VM_POW; break;
+          case Op::Lt: op = VM_LT; break;
+          case Op::Le: op = VM_LE; break;
+          case Op::Gt: op = VM_GT; break;
+          case Op::Ge: op = VM_GE; break;
+          case Op::Eq: op = VM_EQ; break;
+          case Op::Ne: op = VM_NE; break;
+          case Op::Select: op = VM_SELECT; break;
+          case Op::Sech2: op = VM_SECH2; break;
+          case Op::DataTypeCast:
+            op = (P.ty(v).dtype == DType::Bool && in->ops[0].type.dtype != DType::Bool) ? VM_TOBOOL : VM_COPY;
+            break;
+          default:
+            unsupported(std::string("op ") + op_name(in->op) + " in a fused kernel");
+        }
+        int a = operand(in->ops[0], su, m);
+        int b = in->ops.size() > 1 ? operand(in->ops[1], su, m) : 0;
+        int c = in->ops.size() > 2 ? operand(in->ops[2], su, m) : 0;
+        return emit(op, a, b, c);
+      }
+      TensorRef r;
+      if (!P.ref_of(v, false, &r)) unsupported("value %" + P.f.names[v] + " is not addressable");
+      return input(r, m);
+    }
+    uint8_t fix(int s) const {
+      if (s >= 200) return (uint8_t)(inputs.size() + lits.size() + (s - 200));
+      if (s >= 100) return (uint8_t)(inputs.size() + (s - 100));
+      return (uint8_t)s;
+    }
+  };
+
+  IterRef store_ref(const TensorRef& r, const Map& m) const {
+    IterRef it;
+    it.buf = r.buf;
+    it.offset = r.offset;
+    it.st = r.st;
+    for (size_t j = 0; j < m.size(); ++j)
+      if (m[j] >= 0) it.strides[m[j]] += r.strides[j];
+    return it;
+  }
+
+  // program + refs of a group; acc_value >= 0 binds that dot value to slot 0
+  void build_group(const Node& n, EwGroup& g, int acc_value, std::vector<RedInfo>* reds) {
+    ProgBuilder pb(*this);
+    int rk = (int)n.shape.size();
+    pb.stored = n.stored;
+    pb.shape = n.shape;
+    if (acc_value >= 0) {
+      IterRef acc;
+      acc.buf = -2;
+      pb.inputs.push_back(acc);
+      pb.memo[{acc_value, identity(2)}] = 0;
+    }
+    std::vector<int> store_slots, red_slots;
+    std::vector<uint8_t> red_kinds;
+    std::vector<IterRef> stores;
+    for (auto& r : n.roots) {
+      if (r.kind == Root::Fill) {
+        TensorRef out;
+        out.buf = output_buf(r.out);
+        out.shape = r.fill_shape;
+        out.strides = contig_strides(r.fill_shape);
+        out.st = plan.bufs[out.buf].st;
+        store_slots.push_back(pb.lit((float)r.lit));
+        stores.push_back(store_ref(out, identity(rk)));
+        continue;
+      }
+      if (r.kind == Root::Reduce) {
+        Map mx(ty(r.v).rank(), -1);
+        for (size_t i = 0; i < n.perm.size(); ++i) mx[n.perm[i]] = (int)i;
+        red_slots.push_back(pb.node(r.v, mx));
+        red_kinds.push_back(r.rkind);
+        reds->push_back(RedInfo{r.red, (int)red_slots.size() - 1, r.rkind});
+        continue;
+      }
+      int v = r.v;
+      if (r.kind == Root::Copy) {
+        int s = pb.node(v, identity(ty(v).rank()));
+        TensorRef out;
+        out.buf = output_buf(r.out);
+        out.shape = ty(v).shape;
+        out.strides = contig_strides(out.shape);
+        out.st = plan.bufs[out.buf].st;
+        store_slots.push_back(s);
+        stores.push_back(store_ref(out, identity(rk)));
+        continue;
+      }
+      int s;
+      auto key = std::make_pair(v, identity(ty(v).rank()));
+      if (pb.memo.count(key))
+        s = pb.memo[key];
+      else {
+        s = pb.compute(v, identity(ty(v).rank()), true);
+        pb.memo[key] = s;
+      }
+      for (auto& h : vi[v].homes) {
+        store_slots.push_back(s);
+        IterRef st = store_ref(h.ref, identity(rk));
+        st.st = h.st;
+        stores.push_back(st);
+      }
+    }
+    EwProgram& p = g.prog;
+    p.n_in = (uint8_t)pb.inputs.size();
+    p.n_lits = (uint8_t)pb.lits.size();
+    p.n_ins = (uint8_t)pb.ins.size();
+    for (size_t k = 0; k < pb.ins.size(); ++k) {
+      p.ins[k] = pb.ins[k];
+      p.ins[k].a = pb.fix(pb.raw[k][0]);
+      p.ins[k].b = pb.fix(pb.raw[k][1]);
+      p.ins[k].c = pb.fix(pb.raw[k][2]);
+    }
+    for (size_t k = 0; k < pb.lits.size(); ++k) p.lits[k] = pb.lits[k];
+    if (store_slots.size() > (size_t)kMaxStores) unsupported("too many stores in one fused kernel");
+    if (red_slots.size() > (size_t)kMaxReduces) unsupported("too many reductions in one fused kernel");
+    p.n_stores = (uint8_t)store_slots.size();
+    p.n_reduces = (uint8_t)red_slots.size();
+    for (size_t k = 0; k < store_slots.size(); ++k) p.store_slot[k] = pb.fix(store_slots[k]);
+    for (size_t k = 0; k < red_slots.size(); ++k) {
+      p.reduce_slot[k] = pb.fix(red_slots[k]);
+      p.reduce_kind[k] = red_kinds[k];
+    }
+    g.inputs = pb.inputs;
+    g.stores = stores;
+    g.reduces.assign(red_slots.size(), IterRef{});
+  }
+
+  // collapse the iteration space to <= 4 dims: row dims + one column dim
+  void collapse(EwGroup& g, std::vector<int64_t> dims, int split) {
+    int r = (int)dims.size();
+    std::vector<std::vector<int64_t>> in_s(g.inputs.size()), st_s(g.stores.size());
+    for (size_t i = 0; i < g.inputs.size(); ++i) in_s[i].assign(g.inputs[i].strides, g.inputs[i].strides + r);
+    for (size_t i = 0; i < g.stores.size(); ++i) st_s[i].assign(g.stores[i].strides, g.stores[i].strides + r);
+    std::vector<std::vector<int64_t>*> refs;
+    for (auto& v : in_s) refs.push_back(&v);
+    for (auto& v : st_s) refs.push_back(&v);
+    std::vector<int> part(r);  // 0 = row, 1 = column
+    for (int i = 0; i < r; ++i) part[i] = split < 0 ? 0 : (i < split ? 0 : 1);
+    auto erase = [&](int i) {
+      dims.erase(dims.begin() + i);
+      part.erase(part.begin() + i);
+      for (auto* s : refs) s->erase(s->begin() + i);
+    };
+    for (int i = r - 1; i >= 0; --i)  // unit dims carry no data
+      if (dims[i] == 1 && dims.size() > 1) erase(i);
+    for (int i = (int)dims.size() - 2; i >= 0; --i) {
+      if (part[i] != part[i + 1]) continue;
+      bool ok = true;
+      for (auto* s : refs) ok &= (*s)[i] == (*s)[i + 1] * dims[i + 1];
+      if (!ok) continue;
+      dims[i] *= dims[i + 1];
+      for (auto* s : refs) (*s)[i] = (*s)[i + 1];
+      erase(i + 1);
+    }
+    if (dims.empty() || (dims.size() == 1 && dims[0] == 1)) {
+      dims = {1};
+      part = {1};
+      for (auto* s : refs) s->assign(1, 0);
+    }
+    int n_col = 0;
+    for (int p : part) n_col += p;
+    if (split < 0) {  // free split: the last dim is the column dim
+      n_col = 1;
+    } else if (n_col == 0) {  // every dim is a row dim: append a unit column
+      dims.push_back(1);
+      for (auto* s : refs) s->push_back(0);
+      n_col = 1;
+    }
+    if (n_col != 1) unsupported("reduction over a strided column space that does not collapse");
+    if ((int)dims.size() > kMaxIterDims) unsupported("iteration space does not collapse to 4 dims");
+    g.ndims = (int)dims.size();
+    for (int d = 0; d < kMaxIterDims; ++d) g.dims[d] = d < g.ndims ? dims[d] : 1;
+    for (size_t i = 0; i < g.inputs.size(); ++i)
+      for (int d = 0; d < kPlanDims; ++d) g.inputs[i].strides[d] = d < g.ndims ? in_s[i][d] : 0;
+    for (size_t i = 0; i < g.stores.size(); ++i)
+      for (int d = 0; d < kPlanDims; ++d) g.stores[i].strides[d] = d < g.ndims ? st_s[i][d] : 0;
+  }
+
+  static void ew_launch(EwGroup& g) {
+    int64_t C = g.dims[g.ndims - 1], R = 1;
+    for (int d = 0; d < g.ndims - 1; ++d) R *= g.dims[d];
+    bool v4 = C % 4 == 0;
+    auto ok4 = [&](const IterRef& r) {
+      if (r.buf == -2) return true;
+      int64_t cs = r.strides[g.ndims - 1];
+      if (r.nchunks != 1) return false;
+      if (cs == 0) return true;
+      if (cs != 1 || r.offset % 4) return false;
+      for (int d = 0; d < g.ndims - 1; ++d)
+        if (r.strides[d] % 4) return false;
+      return true;
+    };
+    for (auto& r : g.inputs) v4 &= ok4(r);
+    for (auto& r : g.stores) v4 &= ok4(r);
+    g.vec = v4 ? 4 : 1;
+    int64_t cols = (C + g.vec - 1) / g.vec;
+    int bx = 32;
+    while (bx < 256 && bx < cols) bx *= 2;
+    g.bx = bx;
+    g.by = 256 / bx;
+    g.gx = (cols + bx - 1) / bx;
+    int64_t want_gy = std::max<int64_t>(1, (148 * 8) / g.gx);
+    int64_t rpt = (R + (int64_t)g.by * want_gy - 1) / ((int64_t)g.by * want_gy);
+    g.rpt = (int)std::min<int64_t>(64, std::max<int64_t>(1, rpt));
+    g.gy = (R + (int64_t)g.by * g.rpt - 1) / ((int64_t)g.by * g.rpt);
+  }
+
+  // ------------------------------------------------------------ schedule
+  int rep_of(int i) const {
+    i = find(i);
+    if (nodes[i].fused)
+      for (size_t d = 0; d < nodes.size(); ++d)
+        if (nodes[d].is_dot && nodes[d].fused_epilogue == i) return (int)d;
+    return i;
+  }
+  std::vector<int> schedule() {
+    std::vector<int> reps;
+    for (size_t i = 0; i < nodes.size(); ++i)
+      if (nodes[i].merged_into < 0 && !nodes[i].fused) reps.push_back((int)i);
+    std::map<int, std::set<int>> preds;
+    for (int a : reps) preds[a];
+    for (size_t i = 0; i < nodes.size(); ++i)
+      for (int b : succ[i]) {
+        int ga = rep_of((int)i), gb = rep_of(b);
+        if (ga != gb) preds[gb].insert(ga);
+      }
+    auto pos = [&](int a) {
+      int p = nodes[a].pos;
+      if (nodes[a].is_dot && nodes[a].fused_epilogue >= 0) p = std::max(p, nodes[nodes[a].fused_epilogue].pos);
+      return p;
+    };
+    std::vector<int> order;
+    std::set<int> done;
+    while (order.size() < reps.size()) {
+      int best = -1;
+      for (int a : reps) {
+        if (done.count(a)) continue;
+        bool ready = true;
+        for (int p : preds[a]) ready &= done.count(p) > 0;
+        if (ready && (best < 0 || pos(a) < pos(best))) best = a;
+      }
+      if (best < 0) throw Error(kStatusRuntime, 0, 0, "planner: dependency cycle");
+      order.push_back(best);
+      done.insert(best);
+    }
+    return order;
+  }
+
+  // --------------------------------------------------------------- emit
+  void finalize_reds(const std::vector<RedInfo>& reds, int step_index, int64_t gx, int64_t gy, int64_t R,
+                     int64_t C, const std::string& who) {
+    for (auto& ri : reds) {
+      int64_t n_out = ri.kind == RED_COL ? C : ri.kind == RED_ROW ? R : 1;
+      int64_t nch = ri.kind == RED_COL ? gy : ri.kind == RED_ROW ? gx : gx * gy;
+      int pbuf = add_buf(BufferSlot::Work, -1, (size_t)(n_out * nch) * 4, SType::F32);
+      Step& prod = plan.steps[step_index];
+      EwGroup& pg = prod.kind == Step::GEMM ? prod.gemm.epi : prod.ew;
+      pg.reduces[ri.slot_index].buf = pbuf;
+      EwGroup fg;
+      fg.ndims = 1;
+      fg.dims[0] = n_out;
+      IterRef in;
+      in.buf = pbuf;
+      in.nchunks = (int)nch;
+      if (ri.kind == RED_COL) {
+        in.strides[0] = 1;
+        in.chunk_stride = C;
+      } else if (ri.kind == RED_ROW) {
+        in.strides[0] = gx;
+        in.chunk_stride = 1;
+      } else {
+        in.chunk_stride = 1;
+      }
+      fg.inputs.push_back(in);
+      fg.prog.n_in = 1;
+      for (auto& h : vi[ri.value].homes) {
+        IterRef o;
+        o.buf = h.buf;
+        o.st = h.st;
+        o.strides[0] = 1;
+        fg.prog.store_slot[fg.stores.size()] = 0;
+        fg.stores.push_back(o);
+      }
+      fg.prog.n_stores = (uint8_t)fg.stores.size();
+      ew_launch(fg);
+      Step s;
+      s.kind = Step::EW;
+      s.ew = fg;
+      s.desc = "finalize %" + f.names[ri.value] + " (" + std::to_string(nch) + " partials x " +
+               std::to_string(n_out) + ") of " + who;
+      s.ew.desc = s.desc;
+      plan.steps.push_back(s);
+    }
+  }
+
+  void emit_steps(const std::vector<int>& order) {
+    plan.steps.clear();
+    for (int i = 0; i < f.num_args(); ++i) {
+      if (cast_buf[i] < 0) continue;
+      Step s;
+      s.kind = Step::CAST;
+      s.cast.input = i;
+      s.cast.dst_buf = cast_buf[i];
+      s.cast.numel = ty(i).numel();
+      s.desc = "cast %" + f.names[i] + " f32->bf16 (skipped when passed as bf16)";
+      plan.steps.push_back(s);
+    }
+    for (int ni : order) {
+      Node& n = nodes[ni];
+      if (n.is_dot) {
+        emit_gemm(n);
+        continue;
+      }
+      Step s;
+      s.kind = Step::EW;
+      std::vector<RedInfo> reds;
+      build_group(n, s.ew, -1, &reds);
+      std::vector<int64_t> shape = n.shape;
+      int split = n.split;
+      bool only_all = true;
+      for (auto& ri : reds) only_all &= ri.kind == RED_ALL;
+      if (reds.empty() || only_all) split = -1;
+      if (shape.empty()) shape = {1};
+      collapse(s.ew, shape, split);
+      for (auto& ri : reds) {  // kinds in the collapsed space
+        if (s.ew.ndims == 1 && ri.kind == RED_COL) ri.kind = RED_ALL;
+        s.ew.prog.reduce_kind[ri.slot_index] = ri.kind;
+      }
+      ew_launch(s.ew);
+      int64_t C = s.ew.dims[s.ew.ndims - 1], R = 1;
+      for (int d = 0; d < s.ew.ndims - 1; ++d) R *= s.ew.dims[d];
+      std::ostringstream d;
+      d << "ew [";
+      for (int k = 0; k < s.ew.ndims; ++k) d << (k ? "," : "") << s.ew.dims[k];
+      d << "] vec" << s.ew.vec << " in=" << (int)s.ew.prog.n_in << " ops=" << (int)s.ew.prog.n_ins
+        << " stores=" << (int)s.ew.prog.n_stores << " reductions=" << (int)s.ew.prog.n_reduces << " roots:";
+      for (auto& r : n.roots) {
+        if (r.kind == Root::Fill) d << " fill(out" << r.out << ")";
+        else if (r.kind == Root::Copy) d << " copy(%" << f.names[r.v] << "->out" << r.out << ")";
+        else if (r.kind == Root::Reduce) d << " reduce(%" << f.names[r.red] << ")";
+        else d << " %" << f.names[r.v];
+      }
+      s.desc = d.str();
+      s.ew.desc = s.desc;
+      plan.steps.push_back(s);
+      finalize_reds(reds, (int)plan.steps.size() - 1, s.ew.gx, s.ew.gy, R, C, "ew");
+    }
+    add_events();
+    plan.workspace_bytes = (plan.workspace_bytes + 255) / 256 * 256;
+    plan.n_inputs = plan.seed_is_input ? f.num_args() - 1 : f.num_args();
+    plan.n_outputs = (int)f.ret.size();
+  }
+
+  void emit_gemm(Node& n) {
+    const Inst& in = f.insts[n.dot_inst];
+    int dv = in.result;
+    Step s;
+    s.kind = Step::GEMM;
+    GemmStep& gm = s.gemm;
+    gm.M = ty(dv).shape[0];
+    gm.N = ty(dv).shape[1];
+    gm.K = in.ops[0].type.shape[1];
+    bool bf = opt.policy == Policy::BF16;
+    for (int k = 0; k < 2; ++k) {
+      const Operand& o = in.ops[k];
+      if (o.is_lit()) unsupported("dot of a literal operand");
+      TensorRef r;
+      if (!ref_of(o.value, bf, &r)) unsupported("dot operand not addressable");
+      if (bf && r.st != SType::BF16) unsupported("missing bf16 copy of a dot operand");
+      if (r.strides.size() != 2 || !(r.strides[1] == 1 || r.strides[0] == 1 || r.shape[0] == 1 || r.shape[1] == 1))
+        unsupported("dot operand needs a unit stride");
+      (k == 0 ? gm.a : gm.b) = r;
+    }
+    // A [M,K]: K-major if K is the contiguous dim; B [K,N]: K-major if K is contiguous
+    gm.a_kmajor = gm.a.strides[1] == 1 && (gm.a.shape[0] == 1 || gm.a.strides[0] != 1 || gm.a.shape[1] == 1);
+    if (gm.a.strides[1] == 1 && gm.a.shape[1] != 1) gm.a_kmajor = true;
+    if (gm.a.strides[0] == 1 && gm.a.shape[0] != 1 && gm.a.strides[1] != 1) gm.a_kmajor = false;
+    gm.b_kmajor = gm.b.strides[0] == 1 && gm.b.shape[0] != 1 && gm.b.strides[1] != 1;
+    int64_t lda = gm.a_kmajor ? gm.a.strides[0] : gm.a.strides[1];
+    int64_t ldb = gm.b_kmajor ? gm.b.strides[1] : gm.b.strides[0];
+    gm.tensor_core = bf && lda % 8 == 0 && ldb % 8 == 0 && gm.a.offset % 8 == 0 && gm.b.offset % 8 == 0 &&
+                     gm.M >= 128 && gm.N >= 64 && gm.K >= 64;
+    gm.bm = gm.tensor_core ? 128 : 64;
+    gm.bn = gm.tensor_core ? (gm.N >= 256 ? 256 : 128) : 64;
+    Node epi;
+    if (n.fused_epilogue >= 0) epi = nodes[n.fused_epilogue];
+    epi.shape = ty(dv).shape;
+    epi.perm = identity(2);
+    std::vector<Root> roots;
+    if (!vi[dv].homes.empty()) {
+      Root self;
+      self.kind = Root::Store;
+      self.v = dv;
+      roots.push_back(self);
+    }
+    for (auto& r : epi.roots) roots.push_back(r);
+    epi.roots = roots;
+    std::vector<RedInfo> reds;
+    build_group(epi, gm.epi, dv, &reds);
+    gm.epi.ndims = 2;
+    gm.epi.dims[0] = gm.M;
+    gm.epi.dims[1] = gm.N;
+    for (auto& ri : reds) gm.epi.prog.reduce_kind[ri.slot_index] = ri.kind;
+    int64_t gx = (gm.N + gm.bn - 1) / gm.bn, gy = (gm.M + gm.bm - 1) / gm.bm;
+    gm.epi.gx = gx;
+    gm.epi.gy = gy;
+    std::ostringstream d;
+    d << (gm.tensor_core ? "gemm tcgen05 bf16" : (bf ? "gemm simt bf16" : "gemm simt f32")) << " %"
+      << f.names[dv] << " M=" << gm.M << " N=" << gm.N << " K=" << gm.K << " A:" << (gm.a_kmajor ? "K" : "M")
+      << "-major B:" << (gm.b_kmajor ? "K" : "N") << "-major; epilogue ops=" << (int)gm.epi.prog.n_ins
+      << " in=" << (int)gm.epi.prog.n_in << " stores=" << (int)gm.epi.prog.n_stores
+      << " reductions=" << (int)gm.epi.prog.n_reduces;
+    if (n.fused_epilogue >= 0) {
+      d << " roots:";
+      for (auto& r : nodes[n.fused_epilogue].roots) {
+        if (r.kind == Root::Reduce) d << " reduce(%" << f.names[r.red] << ")";
+        else if (r.kind == Root::Store) d << " %" << f.names[r.v];
+        else if (r.kind == Root::Copy) d << " copy(%" << f.names[r.v] << ")";
+      }
+    }
+    s.desc = d.str();
+    gm.epi.desc = s.desc;
+    plan.steps.push_back(s);
+    finalize_reds(reds, (int)plan.steps.size() - 1, gx, gy, gm.M, gm.N, "%" + f.names[dv]);
+  }
+
+  void add_events() {
+    if (opt.n_grads <= 0) return;
+    std::vector<int> last(opt.n_grads, -1);
+    for (size_t si = 0; si < plan.steps.size(); ++si) {
+      const Step& s = plan.steps[si];
+      const std::vector<IterRef>* st =
+          s.kind == Step::EW ? &s.ew.stores : s.kind == Step::GEMM ? &s.gemm.epi.stores : nullptr;
+      if (!st) continue;
+      for (auto& r : *st) {
+        const BufferSlot& b = plan.bufs[r.buf];
+        if (b.kind == BufferSlot::Output && b.index < opt.n_grads) last[b.index] = (int)si;
+      }
+    }
+    std::vector<Step> out;
+    auto ev = [&](int k) {
+      Step e;
+      e.kind = Step::EVENT;
+      e.event_index = k;
+      e.desc = "event: gradient " + std::to_string(k) + " ready";
+      out.push_back(e);
+    };
+    for (int k = 0; k < opt.n_grads; ++k)
+      if (last[k] < 0) ev(k);
+    for (size_t si = 0; si < plan.steps.size(); ++si) {
+      out.push_back(plan.steps[si]);
+      for (int k = 0; k < opt.n_grads; ++k)
+        if (last[k] == (int)si) ev(k);
+    }
+    plan.steps.swap(out);
+  }
+
+  void run() {
+    check_supported();
+    peepholes();
+    analyse();
+    reduce_chains();
+    for (int iter = 0;; ++iter) {
+      if (iter > 1000) throw Error(kStatusRuntime, 0, 0, "planner did not converge");
+      need_iterate = false;
+      decide();
+      alias_outputs();
+      build_nodes();
+      for (auto& n : nodes) region_of(n);
+      if (need_iterate) continue;
+      build_edges();
+      merge_groups();
+      if (!duplicates()) break;
+    }
+    fuse_epilogues();
+    assign_homes();
+    emit_steps(schedule());
+  }
+};
+
+}  // namespace
+
+Plan make_plan(const Function& f, const PlanOptions& opt) {
+  Planner p(f, opt);
+  p.plan.seed_is_input = f.grad.has_value() && f.grad->seedable;
+  p.run();
+  return p.plan;
+}
+
+}  // namespace dlvm

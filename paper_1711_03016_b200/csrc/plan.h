@@ -1,0 +1,123 @@
+// Launch planner: partitions a typed straight-line function into fused
+// sm_100a launch groups (the B200 replacement of the paper's "Compute
+// Generation" / "Compute Scheduling" stages, Fig. 2, and of
+// "fuse compatible element-wise operators to a single kernel to minimize
+// the latency between kernel launches"; "linear algebra fusion ...
+// Wx + b").
+//
+// Two kernel families execute every plan:
+//   * EW   -- an element-wise program over a strided iteration space with
+//             broadcasting loads, stores and row/column/full reductions
+//             (partials, finalised deterministically by their consumer);
+//   * GEMM -- `dot` (operand major-ness absorbs `transpose`) whose
+//             accumulator feeds the same element-wise program as epilogue
+//             (bias, activation, activation derivative, column sums).
+// The program format (EwProgram) is shared by both, and by the host.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ir.h"
+#include "kernels/ew_program.h"
+
+namespace dlvm {
+
+enum class Policy { F32 = 0, BF16 = 1 };
+
+// A device buffer the plan refers to.  Pointers are bound at run time.
+struct BufferSlot {
+  enum Kind { Input, Output, Seed, Work } kind = Work;
+  int index = -1;      // input / output index
+  size_t offset = 0;   // Work: byte offset into the workspace
+  size_t bytes = 0;
+  SType st = SType::F32;
+  int cast_of = -1;    // Work buffer holding a bf16 cast of Input `cast_of` (see CastStep)
+};
+
+// Strided view of a buffer: element (i_0..i_{r-1}) of the value lives at
+// offset + sum_j i_j * strides[j] (elements); if nchunks > 1 the value is
+// the sum over k < nchunks of the element at + k * chunk_stride (partials).
+struct TensorRef {
+  int buf = -1;
+  int64_t offset = 0;
+  std::vector<int64_t> shape, strides;
+  int nchunks = 1;
+  int64_t chunk_stride = 0;
+  SType st = SType::F32;
+  bool contiguous() const;
+};
+
+constexpr int kPlanDims = 8;  // iteration rank while planning (collapsed to kMaxIterDims)
+
+// An iteration-space operand of a kernel (input load or output store).
+struct IterRef {
+  int buf = -1;                  // -2: the GEMM accumulator (epilogue slot 0)
+  int64_t offset = 0;
+  int64_t strides[kPlanDims] = {0, 0, 0, 0, 0, 0, 0, 0};  // per iteration dim
+  int nchunks = 1;
+  int64_t chunk_stride = 0;
+  SType st = SType::F32;
+};
+
+struct EwGroup {
+  // iteration space, row-major: dims[0..ndims-2] are "row" dims, dims[ndims-1]
+  // is the column dim (ndims <= kMaxIterDims).
+  int ndims = 1;
+  int64_t dims[kMaxIterDims] = {1, 1, 1, 1};
+  // launch shape (fixed at plan time: it determines the partials layout)
+  int vec = 1, bx = 32, by = 8, rpt = 1;
+  int64_t gx = 1, gy = 1;
+  EwProgram prog;
+  std::vector<IterRef> inputs;   // prog input slots 0..n_in-1 (GEMM: slot 0 is the accumulator)
+  std::vector<IterRef> stores;   // prog.stores[k] -> stores[k]
+  std::vector<IterRef> reduces;  // prog.reduces[k] -> partial buffer (contiguous)
+  std::string desc;
+};
+
+struct GemmStep {
+  int64_t M = 0, N = 0, K = 0;
+  TensorRef a, b;                // a: [M,K], b: [K,N]; one unit stride each
+  bool a_kmajor = true, b_kmajor = false;
+  bool tensor_core = false;      // tcgen05 (bf16) vs SIMT (f32/bf16 operands)
+  int bm = 128, bn = 128;        // tile shape (partials layout of epilogue reductions)
+  EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator
+};
+
+struct CastStep {                // bf16 copy of an f32 input, skipped if the caller passed bf16
+  int input = -1;
+  int dst_buf = -1;
+  int64_t numel = 0;
+};
+
+struct Step {
+  enum Kind { EW, GEMM, CAST, EVENT } kind = EW;
+  EwGroup ew;
+  GemmStep gemm;
+  CastStep cast;
+  int event_index = -1;          // EVENT: gradient index whose value is final
+  std::string desc;
+};
+
+struct Plan {
+  std::vector<BufferSlot> bufs;
+  std::vector<Step> steps;
+  size_t workspace_bytes = 0;
+  int n_inputs = 0, n_outputs = 0;
+  bool seed_is_input = false;    // gradient plans: last parameter is the seed
+  std::vector<int> input_feeds_only_dot;  // per input: 1 if it may be passed as bf16
+  int launches() const;
+  std::string str() const;
+};
+
+struct PlanOptions {
+  Policy policy = Policy::F32;
+  bool no_fusion = false;
+  bool specialize = true;
+  int n_grads = 0;               // gradient plans: outputs [0, n_grads) get ready events
+};
+
+Plan make_plan(const Function& f, const PlanOptions& opt);
+
+}  // namespace dlvm
