@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the DLVM hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c3|c1|c2|c5]
+    python bench.py --impl reference ...   # the CPU float64 oracle as the reference arm
+
+Default workload (N GPUs, one process per GPU under torchrun): BASELINE.json
+config 4 -- the c3 MLP 4096->4096->4096->1000 (ReLU, MSE) at global batch
+65536, rows split over ranks, one fwd+adjoint step = dlvm_grad_run (forward
+recomputed inside the generated gradient function) + the bucketed NCCL
+gradient all-reduce.  Metric: global samples/s (strong scaling: fixed global
+batch).  Rank 0 also measures config 2 (the fused element-wise chain on 2^28
+fp32 elements) as `fused_elementwise` (HBM GB/s) when N == 1.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+synchronize, CUDA events on the launching stream, max over ranks.  Inputs
+are larger than L2 (x alone is 512 MiB per rank at N=1).  Per-kernel times
+come from CUDA events recorded between launches (dlvm_fn_launch_events) in
+the same timed steps; `roofline` reports the dominant kernel class (the
+tcgen05 GEMMs) against the measured sustained bf16 peak.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLP fwd+adjoint samples/s at 1/2/4/8 B200; fused-elementwise HBM GB/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower().startswith("active")})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------- workloads
+def to_dev(x, dev, bf16=False):
+    import torch
+    t = torch.from_numpy(x).to(dev, non_blocking=False)
+    return t.to(torch.bfloat16) if bf16 else t
+
+
+def mlp_setup(w, dev, rank):
+    """Inputs of the MLP gradient on this rank: x and W as bf16 (they feed
+    only dots, dlvm.h), b and t as f32.  Returns (handle, dev inputs, seed,
+    host inputs, n_grads)."""
+    import numpy as np
+    import torch
+    import paper_1711_03016_b200 as P
+    f = P.Function(w.text, w.fn, w.grad, dot_precision=w.dot_precision)
+    host = w.inputs(row_offset=rank * w.batch)
+    dev_in = []
+    for a, x in zip(w.args, host):
+        bf = w.dot_precision == "bf16" and (a.name == "x" or a.name.startswith("w"))
+        dev_in.append(to_dev(x, dev, bf))
+    seed = torch.tensor(np.float32(w.seed()), device=dev)
+    return f, dev_in, seed, host, 2 * len(w.layers)
+
+
+def time_steps(step, K, dev, world, group=None):
+    """K steps bracketed by barrier + synchronize; device time by CUDA events
+    on the current stream; max over ranks.  Returns ms per step."""
+    import torch
+    import torch.distributed as dist
+    st = torch.cuda.current_stream(dev)
+    if world > 1:
+        dist.barrier(group=group)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(K):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        dist.barrier(group=group)
+        ms = float(t.item())
+    return ms
+
+
+def kernel_breakdown(f, which, step, K, dev):
+    """Per-launch CUDA-event times over K steps (events recorded between the
+    launches on the launching stream).  Returns a list of dicts."""
+    import torch
+    n = f.num_launches(which)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(K)]
+    for row in evs:
+        for e in row:
+            e.record()  # create the events
+    torch.cuda.synchronize(dev)
+    for k in range(K):
+        f.set_launch_events(which, evs[k])
+        step()
+    f.set_launch_events(which, None)
+    torch.cuda.synchronize(dev)
+    out = []
+    for i in range(n):
+        desc, flops, nbytes = f.launch_info(which, i)
+        ms = [evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K)]
+        out.append({"desc": desc, "ms": statistics.mean(ms), "flops": flops, "bytes": nbytes})
+    return out
+
+
+# -------------------------------------------------------- cpu baseline
+def oracle_threads():
+    n = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(n)
+    except Exception:
+        pass
+    return n
+
+
+def cpu_baseline_mlp(w, rows: int):
+    """The oracle (plain float64 numpy interpreter + reverse sweep) timed on
+    `rows` rows of the same workload with full-size weights."""
+    import numpy as np
+    import oracle
+    import workloads as W
+    cores = oracle_threads()
+    ws = W.c3(rows, global_batch=w.global_batch, layers=w.layers)
+    ws.cfg = w.cfg
+    m = oracle.parse(ws.text)
+    ins = [x.astype(np.float64) for x in ws.inputs()] + [np.float64(w.seed())]
+    t0 = time.perf_counter()
+    oracle.run(m, ws.grad, ins)
+    dt = time.perf_counter() - t0
+    return {"value": rows / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows} rows of {w.name} (full {len(w.layers)}-layer weights), one fwd+adjoint, "
+                      f"float64 numpy ({dt:.2f} s)"}
+
+
+def cpu_baseline_chain(rows: int, C: int = 16384):
+    import numpy as np
+    import oracle
+    import workloads as W
+    cores = oracle_threads()
+    w = W.c2(rows, C)
+    m = oracle.parse(w.text)
+    ins = [x.astype(np.float64) for x in w.inputs()]
+    g = w.seed().astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.run(m, w.fn, ins)
+    oracle.run(m, w.grad, ins + [g])
+    dt = time.perf_counter() - t0
+    nbytes = rows * C * (12 + 16)
+    return {"value": nbytes / dt / 1e9, "unit": "GB/s (algorithmic)", "cores": cores, "kind": "oracle",
+            "sample": f"{rows}x{C} rows of c2, fwd + fwd-adjoint, float64 numpy ({dt:.2f} s)"}
+
+
+# ----------------------------------------------------------------- main
+def bench_chain(dev, K, W_):
+    """config 2: y = tanh(x*w + b)*m and its adjoint on [16384, 16384] f32."""
+    import torch
+    import numpy as np
+    import paper_1711_03016_b200 as P
+    import workloads as WL
+    w = WL.c2()
+    f = P.Function(w.text, w.fn, w.grad)
+    ins = [to_dev(x, dev) for x in w.inputs()]
+    seed = to_dev(w.seed(), dev)
+    (y,) = f._outputs(0, dev, None)
+    gouts = f._outputs(1, dev, None)
+    ws0, ws1 = f._workspace(0, dev), f._workspace(1, dev)
+    fwd = lambda: f.run(ins, outputs=[y], workspace=ws0)
+    adj = lambda: f.grad_run(ins, seed=seed, outputs=gouts, workspace=ws1)
+    for _ in range(W_):
+        fwd()
+        adj()
+    ms_f = time_steps(fwd, K, dev, 1)
+    ms_a = time_steps(adj, K, dev, 1)
+    n = 16384 * 16384
+    bf, ba = 12.0 * n, 16.0 * n
+    kb = kernel_breakdown(f, 1, adj, min(K, 5), dev)
+    main = max(kb, key=lambda r: r["ms"])
+    pk = peaks()
+    gbs_a = ba / (main["ms"] * 1e-3) / 1e9
+    return {"workload": "c2_chain [16384,16384] f32", "fwd_ms": ms_f, "fwd_gbs": bf / (ms_f * 1e-3) / 1e9,
+            "fwd_adj_ms": ms_a, "fwd_adj_gbs": ba / (ms_a * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": gbs_a, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs_a / pk["hbm_gbs"], "traffic": None,
+                         "kernel": main["desc"][:90], "algorithmic_bytes": ba},
+            "launches_fwd_adj": f.num_launches(1), "kernels": [{"desc": r["desc"][:80], "ms": r["ms"]} for r in kb]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c1", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-elementwise", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=128)
+    args = ap.parse_args()
+    W_ = max(3, args.warmup)
+    K = args.steps
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import workloads as WL
+
+    def make_workload():
+        if args.workload == "c4":
+            return WL.c4(world)
+        if args.workload == "c3":
+            return WL.c3()
+        if args.workload == "c1":
+            return WL.c1()
+        return WL.c5(131072 // max(world, 1) if world > 1 else 16384, 131072)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        w = make_workload()
+        rows = 64 if args.workload in ("c4", "c3") else (32 if args.workload == "c1" else 16)
+        import numpy as np
+        import oracle
+        cores = oracle_threads()
+        ws = WL.c3(rows, global_batch=w.global_batch, layers=w.layers) if args.workload != "c1" else WL.c1(rows)
+        m = oracle.parse(ws.text)
+        ins = [x.astype(np.float64) for x in ws.inputs()] + [np.float64(w.seed())]
+        for _ in range(W_):
+            oracle.run(m, ws.grad, ins)
+        t0 = time.perf_counter()
+        for _ in range(K):
+            oracle.run(m, ws.grad, ins)
+        dt = (time.perf_counter() - t0) / K
+        v = rows / dt
+        cb = {"value": v, "unit": "samples/s", "cores": cores, "kind": "oracle",
+              "sample": f"{rows} rows of {w.name} per step, float64 numpy"}
+        print(json.dumps({"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus, "steps": K,
+                          "warmup": W_, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                          "config": {"workload": w.name, "global_batch": w.global_batch, "sample_rows": rows,
+                                     "parallelism": f"dp{args.gpus}"},
+                          "cpu_baseline": cb,
+                          "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1711_03016_b200 as P
+    from paper_1711_03016_b200.dp import DataParallelStep
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pk = peaks()
+    w = make_workload()
+    f, dev_in, seed, host, n_grads = mlp_setup(w, dev, rank)
+    dps = DataParallelStep(f, n_grads, dev, world_size=world)
+    for e in dps.events:
+        e.record()
+    step = lambda: dps.step(dev_in, seed)
+    for _ in range(W_):
+        step()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        ms = time_steps(step, K, dev, world)
+    clocks = clk.summary()
+    value = w.global_batch / (ms * 1e-3)
+    # per-kernel breakdown (separate short pass with inter-launch events)
+    kb = kernel_breakdown(f, 1, step, min(K, 5), dev)
+    gemm = [r for r in kb if r["flops"] > 0]
+    gemm_ms = sum(r["ms"] for r in gemm)
+    gemm_flops = sum(r["flops"] for r in gemm)
+    step_flops = gemm_flops
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
+    tc = [r for r in gemm if "tcgen05" in r["desc"]]
+    roof = {"bound": "tensor", "achieved": achieved, "peak": pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+            "unit": "TFLOP/s", "frac": achieved / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+            "traffic": None, "kernel": "gemm_tcgen05 (all dots of the step)",
+            "peak_kind": "sustained bf16 " + pk["source"], "frac_of_burst": achieved / pk["bf16_tflops"],
+            "gemm_share_of_step": gemm_ms / sum(r["ms"] for r in kb) if kb else None,
+            "algorithmic_flops_per_step": step_flops, "tcgen05_launches": len(tc)}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get(w.name)
+        except Exception:
+            pass
+    launches = f.num_launches(1) * K
+    # end to end: H2D of this step's batch (pinned host) + step + D2H of the loss
+    e2e = None
+    if not args.no_e2e:
+        xi = [i for i, a in enumerate(w.args) if a.batched]
+        pinned = []
+        for i in xi:
+            t = torch.from_numpy(host[i])
+            if dev_in[i].dtype == torch.bfloat16:
+                t = t.to(torch.bfloat16)
+            pinned.append(t.pin_memory())
+        loss_h = torch.empty((), dtype=torch.float32).pin_memory()
+        h2d = sum(p.numel() * p.element_size() for p in pinned)
+
+        def e2e_step():
+            for i, p in zip(xi, pinned):
+                dev_in[i].copy_(p, non_blocking=True)
+            outs = dps.step(dev_in, seed)
+            loss_h.copy_(outs[-1], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        ms_e2e = time_steps(e2e_step, max(3, K // 2), dev, world)
+        e2e = {"value": w.global_batch / (ms_e2e * 1e-3), "unit": "samples/s", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * world,
+               "api": "paper_1711_03016_b200.Function.grad_run (dlvm_grad_run) + DataParallelStep"}
+    out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W_,
+           "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "bf16", "data": "synthetic (seeded PCG64 per workloads.py; Glorot weights)",
+           "config": {"workload": w.name, "global_batch": w.global_batch, "per_rank_batch": w.batch,
+                      "layers": [list(l) for l in w.layers], "parallelism": f"dp{world}",
+                      "dot_precision": "bf16 operands, fp32 accumulate (tcgen05)",
+                      "l2": "inputs larger than L2 (x is %d MiB per rank)" % (w.batch * w.layers[0][0] * 2 >> 20)},
+           "roofline": roof, "gpu_launches": launches, "clocks": clocks,
+           "kernels": [{"desc": r["desc"][:100], "ms": round(r["ms"], 4)} for r in kb]}
+    if e2e:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1:
+        try:
+            out["cpu_baseline"] = cpu_baseline_mlp(w, args.cpu_rows)
+        except Exception as ex:  # noqa: BLE001
+            out["cpu_baseline"] = {"error": repr(ex)}
+        if not args.no_elementwise:
+            ew = bench_chain(dev, K, W_)
+            out["fused_elementwise"] = ew
+            out["gpu_launches"] += (1 + ew["launches_fwd_adj"]) * K
+            try:
+                ew["cpu_baseline"] = cpu_baseline_chain(256)
+            except Exception as ex:  # noqa: BLE001
+                ew["cpu_baseline"] = {"error": repr(ex)}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

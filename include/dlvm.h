@@ -133,6 +133,21 @@ dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlv
                           dlvm_tensor* out, int n_out, void* workspace, void* cuda_stream,
                           void* const* grad_ready_events);
 
+/* Profiling hook.  With n_events == dlvm_fn_num_launches(fn, which) + 1,
+ * every later run of `which` records events[i] (cudaEvent_t) on its stream
+ * right before launch i and events[n_events-1] after the last launch, so a
+ * caller can time each kernel with cudaEventElapsedTime on the launching
+ * stream.  events == NULL (or n_events == 0) disables it.  The handle keeps
+ * the pointer array; the caller keeps it and the events alive while set. */
+dlvm_status dlvm_fn_launch_events(dlvm_fn fn, int which, void* const* events, int n_events);
+
+/* Short description ("gemm tcgen05 bf16 %z1 M=... N=... K=...", "ew [...]")
+ * of launch i of `which`, and its algorithmic work: flops (2*M*N*K for a
+ * GEMM, 0 otherwise) and the bytes it must move at minimum (every input
+ * element read once, every output element written once). */
+dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t cap, double* flops,
+                                double* bytes);
+
 /* Thread-local text of the last error on this thread ("" if none). */
 const char* dlvm_last_error(void);
 

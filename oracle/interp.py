@@ -14,6 +14,13 @@ Op definitions (Table 1):
   slice(a, f, u)                     a[f:u] on axis 0
 All floating-point values are float64 regardless of their IR dtype (the
 oracle is the exact-arithmetic stand-in; the paper fixes no precision).
+
+dot_policy="bf16" (reading A15 of SURVEY.md §8(c), not from the paper, which
+has no bf16): every `dot` operand is first rounded to the nearest bf16 value
+(round-to-nearest-even), then multiplied and summed in float64.  This is the
+definition of the GPU's bf16-dot execution policy written out; the parity
+tests use it for network-level checks where the unrounded comparison is
+ill-conditioned (ReLU's derivative jumps at 0).
 """
 
 from __future__ import annotations
@@ -44,7 +51,17 @@ def literal_value(o: Operand) -> np.ndarray:
     return np.full(o.type.shape, o.literal, dtype=np_dtype(o.type))
 
 
-def eval_inst(ins: Inst, args: List[np.ndarray], rt: TensorType) -> np.ndarray:
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """Nearest bf16 value of each float (RNE on the float32 bit pattern after
+    the float64 -> float32 rounding; NaN/inf pass through)."""
+    f = np.asarray(x, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    out = r.astype(np.uint32).view(np.float32).astype(np.float64)
+    return np.where(np.isfinite(f), out, f.astype(np.float64))
+
+
+def eval_inst(ins: Inst, args: List[np.ndarray], rt: TensorType, dot_policy=None) -> np.ndarray:
     op = ins.opcode
     if op == "negate":
         r = -args[0]
@@ -85,7 +102,10 @@ def eval_inst(ins: Inst, args: List[np.ndarray], rt: TensorType) -> np.ndarray:
     elif op == "select":
         r = np.where(args[0], args[1], args[2])
     elif op == "dot":
-        r = args[0] @ args[1]
+        if dot_policy == "bf16":
+            r = bf16_round(args[0]) @ bf16_round(args[1])
+        else:
+            r = args[0] @ args[1]
     elif op == "reduce":
         f = np.sum if ins.attrs["op"] == "add" else np.prod
         r = f(args[0], axis=ins.attrs["axis"])
@@ -105,7 +125,7 @@ def eval_inst(ins: Inst, args: List[np.ndarray], rt: TensorType) -> np.ndarray:
     return r
 
 
-def evaluate(fn: Function, inputs: Sequence) -> Dict[str, np.ndarray]:
+def evaluate(fn: Function, inputs: Sequence, dot_policy=None) -> Dict[str, np.ndarray]:
     """All SSA values of one execution of `fn`, keyed by name."""
     if len(inputs) != len(fn.param_types):
         raise ValueError(f"@{fn.name} takes {len(fn.param_types)} inputs, got {len(inputs)}")
@@ -117,19 +137,19 @@ def evaluate(fn: Function, inputs: Sequence) -> Dict[str, np.ndarray]:
         return literal_value(o) if o.kind == "literal" else env[o.name]
 
     for ins in fn.insts:
-        env[ins.result] = eval_inst(ins, [val(o) for o in ins.operands], fn.types[ins.result])
+        env[ins.result] = eval_inst(ins, [val(o) for o in ins.operands], fn.types[ins.result], dot_policy)
     return env
 
 
-def run_function(fn: Function, inputs: Sequence) -> List[np.ndarray]:
-    env = evaluate(fn, inputs)
+def run_function(fn: Function, inputs: Sequence, dot_policy=None) -> List[np.ndarray]:
+    env = evaluate(fn, inputs, dot_policy)
     return [literal_value(o) if o.kind == "literal" else env[o.name] for o in fn.ret]
 
 
-def run(mod: Module, name: str, inputs: Sequence) -> List[np.ndarray]:
+def run(mod: Module, name: str, inputs: Sequence, dot_policy=None) -> List[np.ndarray]:
     """Runs a defined function, or the result a gradient declaration denotes."""
     fn = mod.functions[name]
     if fn.gradient is not None:
         from .vjp import grad_function
-        return grad_function(mod, fn, inputs)
-    return run_function(fn, inputs)
+        return grad_function(mod, fn, inputs, dot_policy)
+    return run_function(fn, inputs, dot_policy)

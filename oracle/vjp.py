@@ -18,7 +18,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .interp import evaluate, literal_value
+from .interp import bf16_round, evaluate, literal_value
 from .ir import BINARY, COMPARE, FLOAT_DTYPES, Function, Inst, Module
 
 
@@ -36,7 +36,7 @@ def unbroadcast(c: np.ndarray, shape: Tuple[int, ...]) -> np.ndarray:
     return c
 
 
-def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray]
+def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray], dot_policy=None
              ) -> List[Tuple[int, Optional[np.ndarray]]]:
     """Contributions (operand index, adjoint before unbroadcast) of one
     instruction, given its incoming adjoint g, result y and operand values.
@@ -78,6 +78,8 @@ def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray]
         return []
     if op == "dot":
         a, b = args
+        if dot_policy == "bf16":  # the adjoint dots round their operands too (reading A15)
+            a, b, g = bf16_round(a), bf16_round(b), bf16_round(g)
         return [(0, g @ b.T), (1, a.T @ g)]
     if op == "transpose":
         return [(0, np.transpose(g, tuple(reversed(range(g.ndim)))))]
@@ -98,7 +100,7 @@ def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray]
 
 
 def reverse_sweep(src: Function, env: Dict[str, np.ndarray], out_index: int,
-                  seed: np.ndarray) -> Dict[str, np.ndarray]:
+                  seed: np.ndarray, dot_policy=None) -> Dict[str, np.ndarray]:
     """Adjoints of every value that the selected output depends on."""
     adj: Dict[str, np.ndarray] = {}
 
@@ -119,7 +121,7 @@ def reverse_sweep(src: Function, env: Dict[str, np.ndarray], out_index: int,
         g = adj[ins.result]
         args = [literal_value(o) if o.kind == "literal" else env[o.name] for o in ins.operands]
         args = [a.astype(np.float64) if a.dtype != np.bool_ else a for a in args]
-        for idx, c in vjp_rule(ins, g, env[ins.result], args):
+        for idx, c in vjp_rule(ins, g, env[ins.result], args, dot_policy):
             o = ins.operands[idx]
             if o.kind == "value" and is_float(o.name):
                 acc(o.name, c)
@@ -127,15 +129,15 @@ def reverse_sweep(src: Function, env: Dict[str, np.ndarray], out_index: int,
 
 
 def grad(src: Function, inputs: Sequence, wrt: Optional[Sequence[int]] = None,
-         keeping: Sequence[int] = (), from_: int = 0, seed=None) -> List[np.ndarray]:
+         keeping: Sequence[int] = (), from_: int = 0, seed=None, dot_policy=None) -> List[np.ndarray]:
     """Gradient result of `src` at `inputs` (reading A7 order: grads in `wrt`
     order, then kept outputs)."""
-    env = evaluate(src, inputs)
+    env = evaluate(src, inputs, dot_policy)
     outs = [literal_value(o) if o.kind == "literal" else env[o.name] for o in src.ret]
     if seed is None:
         seed = np.ones(src.result_types[from_].shape, dtype=np.float64)
     seed = np.asarray(seed, dtype=np.float64).reshape(src.result_types[from_].shape)
-    adj = reverse_sweep(src, env, from_, seed)
+    adj = reverse_sweep(src, env, from_, seed, dot_policy)
     wrt = list(range(len(src.param_types))) if wrt is None else list(wrt)
     res = []
     for i in wrt:
@@ -145,7 +147,7 @@ def grad(src: Function, inputs: Sequence, wrt: Optional[Sequence[int]] = None,
     return res
 
 
-def grad_function(mod: Module, gfn: Function, inputs: Sequence) -> List[np.ndarray]:
+def grad_function(mod: Module, gfn: Function, inputs: Sequence, dot_policy=None) -> List[np.ndarray]:
     """Runs a gradient declaration: inputs are the source's arguments, plus
     the seed last when `seedable` (Fig. 3 `@foo_grad_3`)."""
     cfg = gfn.gradient
@@ -153,4 +155,4 @@ def grad_function(mod: Module, gfn: Function, inputs: Sequence) -> List[np.ndarr
     n = len(src.param_types)
     seed = inputs[n] if cfg.seedable else None
     return grad(src, list(inputs[:n]), cfg.wrt, cfg.keeping,
-                0 if cfg.from_ is None else cfg.from_, seed)
+                0 if cfg.from_ is None else cfg.from_, seed, dot_policy)

@@ -29,6 +29,7 @@ struct dlvm_fn_s {
   std::string plan_error[2];
   dlvm_options opts{};
   int n_grads = 0;
+  std::vector<void*> launch_events[2];
 };
 
 namespace {
@@ -180,8 +181,17 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         break;
     }
   }
+  const std::vector<void*>& lev = fn->launch_events[which];
+  int li = 0;
+  auto mark = [&](int i) -> cudaError_t {
+    if (lev.empty() || !lev[i]) return cudaSuccess;
+    return cudaEventRecord(static_cast<cudaEvent_t>(lev[i]), stream);
+  };
   for (const Step& st : P.steps) {
     cudaError_t e = cudaSuccess;
+    const bool is_launch = st.kind == Step::EW || st.kind == Step::GEMM;
+    if (is_launch && (e = mark(li++)) != cudaSuccess)
+      return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
     if (st.kind == Step::EW) {
       EwParams p;
       to_dev(st.ew, b, &p);
@@ -226,7 +236,38 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     }
     if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("CUDA error in '") + st.desc + "': " + cudaGetErrorString(e));
   }
+  if (!lev.empty()) {
+    cudaError_t e = mark(li);
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+  }
   return DLVM_OK;
+}
+
+// minimum bytes a launch moves: each distinct input read once, each output written once
+double step_bytes(const Plan& P, const Step& st) {
+  const EwGroup& g = st.kind == Step::GEMM ? st.gemm.epi : st.ew;
+  auto esz = [&](int buf, SType fallback) {
+    SType t = buf >= 0 ? P.bufs[buf].st : fallback;
+    return t == SType::F32 ? 4.0 : t == SType::BF16 ? 2.0 : 1.0;
+  };
+  int64_t n = 1;
+  for (int d = 0; d < g.ndims; ++d) n *= g.dims[d];
+  double b = 0;
+  for (auto& r : g.inputs) {
+    if (r.buf < 0) continue;
+    int64_t cnt = r.nchunks;  // elements touched: product of dims with a nonzero stride
+    for (int d = 0; d < g.ndims; ++d)
+      if (r.strides[d] != 0) cnt *= g.dims[d];
+    b += cnt * esz(r.buf, r.st);
+  }
+  for (auto& r : g.stores) b += n * esz(r.buf, r.st);
+  for (auto& r : g.reduces) (void)r;
+  if (st.kind == Step::GEMM) {
+    const GemmStep& m = st.gemm;
+    double e = m.tensor_core || P.bufs[m.a.buf].st == SType::BF16 ? 2.0 : 4.0;
+    b += (double)(m.M * m.K + m.K * m.N) * e;
+  }
+  return b;
 }
 
 }  // namespace
@@ -380,6 +421,38 @@ dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlv
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());
   }
+}
+
+dlvm_status dlvm_fn_launch_events(dlvm_fn fn, int which, void* const* events, int n_events) {
+  if (!fn || (which != 0 && which != 1)) return fail(DLVM_ERR_USAGE, "bad handle or which");
+  if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
+  if (!events || n_events == 0) {
+    fn->launch_events[which].clear();
+    return DLVM_OK;
+  }
+  if (n_events != fn->plan[which].launches() + 1) return fail(DLVM_ERR_USAGE, "n_events must be launches + 1");
+  fn->launch_events[which].assign(events, events + n_events);
+  return DLVM_OK;
+}
+
+dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t cap, double* flops, double* bytes) {
+  if (!fn || (which != 0 && which != 1)) return fail(DLVM_ERR_USAGE, "bad handle or which");
+  if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
+  const Plan& P = fn->plan[which];
+  int li = 0;
+  for (const Step& st : P.steps) {
+    if (st.kind != Step::EW && st.kind != Step::GEMM) continue;
+    if (li++ != i) continue;
+    if (buf && cap) {
+      size_t n = std::min(cap - 1, st.desc.size());
+      std::memcpy(buf, st.desc.data(), n);
+      buf[n] = 0;
+    }
+    if (flops) flops[0] = st.kind == Step::GEMM ? 2.0 * st.gemm.M * st.gemm.N * st.gemm.K : 0.0;
+    if (bytes) bytes[0] = step_bytes(P, st);
+    return DLVM_OK;
+  }
+  return fail(DLVM_ERR_USAGE, "launch index out of range");
 }
 
 const char* dlvm_last_error(void) { return g_last_error.c_str(); }

@@ -3,8 +3,9 @@
 //
 // Arithmetic follows the IR's op definitions in fp32 (Table 1
 // L170-181) with IEEE round-to-nearest: explicit __f*_rn intrinsics
-// (no FMA contraction, so interpreted and specialised programs are
-// bit-identical), accurate expf/tanhf/logf/powf (no tanh.approx / ex2.approx:
+// (the compiler never contracts; the planner emits VM_FMA where it wants one
+// rounding for a*b + c, so every program evaluates identically wherever it
+// runs), accurate expf/tanhf/logf/powf (no tanh.approx / ex2.approx:
 // reading A13), no flush-to-zero.  sech2 is the cancellation-free tanh
 // derivative (reading A12).
 #pragma once
@@ -45,6 +46,7 @@ __device__ __forceinline__ float vm_apply(uint8_t op, float a, float b, float c)
     case VM_TOBOOL: return a != 0.f ? 1.f : 0.f;
     case VM_COPY: return a;
     case VM_SECH2: return vm_sech2(a);
+    case VM_FMA: return __fmaf_rn(a, b, c);
     default: return 0.f;
   }
 }

@@ -38,6 +38,7 @@ enum VmOp : uint8_t {
   // planner peepholes (reading A12: derivative closed forms evaluated from
   // the pre-activation, cancellation-free in fp32)
   VM_SECH2,    // subtract(1, multiply(tanh z, tanh z)) == sech^2(z), operand z
+  VM_FMA,      // add(multiply(a, b), c) with one rounding (FMA contraction, reading A13)
   VM_NUM_OPS
 };
 
@@ -62,7 +63,7 @@ struct EwProgram {
 
 inline int vm_arity(uint8_t op) {
   if (op <= VM_SIGN || op == VM_TOBOOL || op == VM_COPY || op == VM_SECH2) return 1;
-  if (op == VM_SELECT) return 3;
+  if (op == VM_SELECT || op == VM_FMA) return 3;
   return 2;
 }
 

@@ -82,6 +82,19 @@ bool is_identity(const std::vector<int>& p) {
   return true;
 }
 
+// size-1 dims carry no index: canonical maps send them to -1
+Map canon(Map m, const std::vector<int64_t>& shape) {
+  for (size_t j = 0; j < m.size(); ++j)
+    if (shape[j] == 1) m[j] = -1;
+  return m;
+}
+bool ident_map(const Map& m, const std::vector<int64_t>& shape, int rk) {
+  if ((int)m.size() != rk) return false;
+  for (size_t j = 0; j < m.size(); ++j)
+    if (shape[j] != 1 && m[j] != (int)j) return false;
+  return true;
+}
+
 struct Home {
   int buf = -1;
   SType st = SType::F32;
@@ -184,6 +197,30 @@ struct Planner {
 
   // ------------------------------------------------------------- peepholes
   void peepholes() {
+    // a splat literal feeding a dot is materialised by an element-wise
+    // `add(lit, 0)` (stored, since it is a dot operand)
+    for (size_t k = 0; k < f.insts.size(); ++k) {
+      if (f.insts[k].op != Op::Dot) continue;
+      for (int j = 0; j < 2; ++j) {
+        if (!f.insts[k].ops[j].is_lit()) continue;
+        Operand lit = f.insts[k].ops[j];
+        Inst splat;
+        splat.op = Op::Add;
+        Operand zero;
+        zero.lit = 0.0;
+        zero.type = Type{{}, lit.type.dtype};
+        splat.ops = {lit, zero};
+        splat.rname = "splat" + std::to_string(k) + "_" + std::to_string(j);
+        splat.result = f.add_value(splat.rname, lit.type);
+        Operand use;
+        use.value = splat.result;
+        use.vname = splat.rname;
+        use.type = lit.type;
+        f.insts[k].ops[j] = use;
+        f.insts.insert(f.insts.begin() + k, splat);
+        ++k;
+      }
+    }
     std::vector<int> defidx(f.types.size(), -1);
     for (size_t k = 0; k < f.insts.size(); ++k) defidx[f.insts[k].result] = (int)k;
     for (auto& in : f.insts) {  // subtract(1, multiply(t, t)), t = tanh(z) -> sech2(z)
@@ -472,7 +509,7 @@ struct Planner {
     std::function<void(int, const Map&)> walk = [&](int v, const Map& m) {
       if (vi[v].arg >= 0 || !vi[v].inl) {
         n.reads.insert(v);
-        if (!((int)m.size() == rk && is_identity(m) && ty(v).shape == n.shape)) n.nonident.insert(v);
+        if (!(ident_map(m, ty(v).shape, rk) && ty(v).shape == n.shape)) n.nonident.insert(v);
         return;
       }
       const Inst* in = def(v);
@@ -833,7 +870,8 @@ struct Planner {
       if (o.is_lit()) return lit((float)o.lit);
       return node(o.value, P.bcast_map(P.ty(o.value).shape, su, mu));
     }
-    int node(int v, const Map& m) {
+    int node(int v, const Map& m0) {
+      const Map m = canon(m0, P.ty(v).shape);
       auto key = std::make_pair(v, m);
       auto it = memo.find(key);
       if (it != memo.end()) return it->second;
@@ -845,7 +883,9 @@ struct Planner {
     int compute(int v, const Map& m, bool force) {
       const Inst* in = P.def(v);
       const VInfo& x = P.vi[v];
-      if (!force && stored.count(v) && is_identity(m) && P.ty(v).shape == shape && is_ew(in)) force = true;
+      if (!force && stored.count(v) && ident_map(m, P.ty(v).shape, (int)shape.size()) && P.ty(v).shape == shape &&
+          is_ew(in))
+        force = true;
       bool inline_it = in && x.arg < 0 && (x.inl || force);
       if (inline_it && is_view(in)) {
         int src = in->ops[0].value;
@@ -886,6 +926,23 @@ struct Planner {
           default:
             unsupported(std::string("op ") + op_name(in->op) + " in a fused kernel");
         }
+        // FMA contraction: add(multiply(a, b), c) / subtract(multiply(a, b), c)
+        // with a single-use inlined multiply (reading A13)
+        if (op == VM_ADD || op == VM_SUB) {
+          for (int side = 0; side < 2; ++side) {
+            const Operand& mo = in->ops[side];
+            if (op == VM_SUB && side == 1) break;
+            if (mo.is_lit() || !fusable_mul(mo.value)) continue;
+            const Inst* mi = P.def(mo.value);
+            Map mm = P.bcast_map(P.ty(mo.value).shape, su, m);
+            const auto& sm = P.ty(mo.value).shape;
+            int a = operand(mi->ops[0], sm, mm);
+            int b = operand(mi->ops[1], sm, mm);
+            int c = operand(in->ops[1 - side], su, m);
+            if (op == VM_SUB) c = emit(VM_NEG, c, 0, 0);
+            return emit(VM_FMA, a, b, c);
+          }
+        }
         int a = operand(in->ops[0], su, m);
         int b = in->ops.size() > 1 ? operand(in->ops[1], su, m) : 0;
         int c = in->ops.size() > 2 ? operand(in->ops[2], su, m) : 0;
@@ -894,6 +951,11 @@ struct Planner {
       TensorRef r;
       if (!P.ref_of(v, false, &r)) unsupported("value %" + P.f.names[v] + " is not addressable");
       return input(r, m);
+    }
+    bool fusable_mul(int v) const {
+      const Inst* mi = P.def(v);
+      const VInfo& x = P.vi[v];
+      return mi && mi->op == Op::Multiply && x.inl && x.users.size() == 1 && x.outs.empty() && !stored.count(v);
     }
     uint8_t fix(int s) const {
       if (s >= 200) return (uint8_t)(inputs.size() + lits.size() + (s - 200));
@@ -922,7 +984,7 @@ struct Planner {
       IterRef acc;
       acc.buf = -2;
       pb.inputs.push_back(acc);
-      pb.memo[{acc_value, identity(2)}] = 0;
+      pb.memo[{acc_value, canon(identity(2), ty(acc_value).shape)}] = 0;
     }
     std::vector<int> store_slots, red_slots;
     std::vector<uint8_t> red_kinds;
@@ -959,7 +1021,7 @@ struct Planner {
         continue;
       }
       int s;
-      auto key = std::make_pair(v, identity(ty(v).rank()));
+      auto key = std::make_pair(v, canon(identity(ty(v).rank()), ty(v).shape));
       if (pb.memo.count(key))
         s = pb.memo[key];
       else {

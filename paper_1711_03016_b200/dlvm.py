@@ -22,8 +22,8 @@ DLVM_PRIMAL, DLVM_GRADIENT = 0, 1
 MAX_RANK = 8
 
 EXPORTS = ["dlvm_fn_create", "dlvm_fn_signature", "dlvm_fn_print", "dlvm_fn_workspace_bytes",
-           "dlvm_fn_num_launches", "dlvm_fn_run", "dlvm_grad_run", "dlvm_last_error",
-           "dlvm_fn_destroy", "dlvm_version"]
+           "dlvm_fn_num_launches", "dlvm_fn_run", "dlvm_grad_run", "dlvm_fn_launch_events",
+           "dlvm_fn_launch_info", "dlvm_last_error", "dlvm_fn_destroy", "dlvm_version"]
 
 
 class dlvm_tensor(ctypes.Structure):
@@ -62,11 +62,15 @@ def lib() -> ctypes.CDLL:
         L.dlvm_fn_run.argtypes = [vp, ctypes.POINTER(dlvm_tensor), i32, ctypes.POINTER(dlvm_tensor), i32, vp, vp]
         L.dlvm_grad_run.argtypes = [vp, ctypes.POINTER(dlvm_tensor), i32, ctypes.POINTER(dlvm_tensor),
                                     ctypes.POINTER(dlvm_tensor), i32, vp, vp, ctypes.POINTER(vp)]
+        L.dlvm_fn_launch_events.argtypes = [vp, i32, ctypes.POINTER(vp), i32]
+        L.dlvm_fn_launch_info.argtypes = [vp, i32, i32, ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double)]
         L.dlvm_last_error.restype = ctypes.c_char_p
         L.dlvm_fn_destroy.argtypes = [vp]
         L.dlvm_version.restype = ctypes.c_char_p
         for name in ["dlvm_fn_create", "dlvm_fn_signature", "dlvm_fn_print", "dlvm_fn_workspace_bytes",
-                     "dlvm_fn_num_launches", "dlvm_fn_run", "dlvm_grad_run"]:
+                     "dlvm_fn_num_launches", "dlvm_fn_run", "dlvm_grad_run", "dlvm_fn_launch_events",
+                     "dlvm_fn_launch_info"]:
             getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -162,6 +166,23 @@ class Function:
         n = ctypes.c_int(0)
         _check(lib().dlvm_fn_num_launches(self._h, which, ctypes.byref(n)))
         return n.value
+
+    def launch_info(self, which: int, i: int):
+        """(description, algorithmic flops, minimum bytes) of launch i."""
+        buf = ctypes.create_string_buffer(512)
+        fl, by = ctypes.c_double(0), ctypes.c_double(0)
+        _check(lib().dlvm_fn_launch_info(self._h, which, i, buf, 512, ctypes.byref(fl), ctypes.byref(by)))
+        return buf.value.decode(), fl.value, by.value
+
+    def set_launch_events(self, which: int, events):
+        """Record events[i] before launch i (+ one after the last); None clears."""
+        if events is None:
+            self._lev = None
+            _check(lib().dlvm_fn_launch_events(self._h, which, None, 0))
+            return
+        arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+        self._lev = (arr, events)
+        _check(lib().dlvm_fn_launch_events(self._h, which, arr, len(events)))
 
     # ----------------------------------------------------------- execution
     def _workspace(self, which: int, device):

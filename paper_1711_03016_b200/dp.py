@@ -1,0 +1,124 @@
+"""Batch-sharded data parallelism (BASELINE.json north_star:
+"forward plus adjoint is sharded along the batch dimension, with one NCCL
+allreduce over NVLink of the parameter gradients").
+
+Rank r owns rows [r*B/N, (r+1)*B/N) of the batch arguments; weights are
+replicated.  Every forward op and every activation adjoint is row-local;
+only the contractions over the batch (dW = H^T dZ, db = sum_rows dZ, the
+loss) need combining.  With the seed 1/B_global the SUM all-reduce yields
+the global-batch gradient (pin F15).
+
+Gradients land in one flat fp32 buffer laid out per parameter; buckets are
+contiguous runs of parameters (one layer's dW and db) all-reduced on a
+communication stream as soon as dlvm_grad_run records the gradient-ready
+event of the bucket's last gradient, so the all-reduce of layer L overlaps
+the adjoint of layers L-1..1 (the planner emits the dW GEMMs in reverse
+layer order)."""
+
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+
+def flat_layout(shapes: Sequence[Tuple[int, ...]], align: int = 64) -> Tuple[List[int], int]:
+    """Element offsets of each gradient in the flat buffer (each 256-byte
+    aligned, as the C ABI wants 16-byte-aligned outputs) and the total size."""
+    offs, n = [], 0
+    for s in shapes:
+        offs.append(n)
+        k = 1
+        for d in s:
+            k *= d
+        n += (k + align - 1) // align * align
+    return offs, n
+
+
+def layer_buckets(n_grads: int, per_bucket: int = 2) -> List[List[int]]:
+    """Buckets of consecutive gradients: (dW_l, db_l) pairs for MLPs."""
+    return [list(range(i, min(i + per_bucket, n_grads))) for i in range(0, n_grads, per_bucket)]
+
+
+class GradBuffer:
+    """Flat gradient storage + per-gradient views (torch tensors)."""
+
+    def __init__(self, shapes: Sequence[Tuple[int, ...]], device, dtype=None):
+        import torch
+        self.shapes = [tuple(s) for s in shapes]
+        self.offsets, total = flat_layout(self.shapes)
+        self.flat = torch.zeros(total, dtype=dtype or torch.float32, device=device)
+        self.views = []
+        for o, s in zip(self.offsets, self.shapes):
+            k = 1
+            for d in s:
+                k *= d
+            self.views.append(self.flat[o:o + k].view(s))
+
+    def bucket_slice(self, bucket: Sequence[int]):
+        lo = self.offsets[bucket[0]]
+        last = bucket[-1]
+        k = 1
+        for d in self.shapes[last]:
+            k *= d
+        return self.flat[lo:self.offsets[last] + k]
+
+
+def allreduce_buckets(buf: GradBuffer, buckets: Sequence[Sequence[int]], group=None, order=None,
+                      comm_stream=None, ready_events=None):
+    """All-reduce (SUM) each bucket.  With `comm_stream` and `ready_events`
+    (one torch.cuda.Event per gradient), bucket b is issued on the comm
+    stream after waiting for the events of its gradients.  Returns the async
+    work handles (the caller makes its stream wait on them)."""
+    import torch.distributed as dist
+    works = []
+    seq = order if order is not None else range(len(buckets))
+    for b in seq:
+        bucket = buckets[b]
+        if comm_stream is not None:
+            import torch
+            with torch.cuda.stream(comm_stream):
+                if ready_events is not None:
+                    for g in bucket:
+                        comm_stream.wait_event(ready_events[g])
+                works.append(dist.all_reduce(buf.bucket_slice(bucket), op=dist.ReduceOp.SUM, group=group,
+                                             async_op=True))
+        else:
+            works.append(dist.all_reduce(buf.bucket_slice(bucket), op=dist.ReduceOp.SUM, group=group,
+                                         async_op=True))
+    return works
+
+
+class DataParallelStep:
+    """One fwd+adjoint step of a gradient handle on this rank's batch shard,
+    then the bucketed gradient all-reduce (NCCL), overlapped with the adjoint."""
+
+    def __init__(self, fn, n_grads: int, device, group=None, per_bucket: int = 2, world_size: int = 1):
+        import torch
+        self.fn = fn
+        self.n_grads = n_grads
+        self.device = device
+        self.group = group
+        self.world_size = world_size
+        _, outs = fn.signature(1)
+        self.grads = GradBuffer([s for s, _ in outs[:n_grads]], device)
+        self.kept = [torch.empty(s, dtype=torch.float32, device=device) for s, _ in outs[n_grads:]]
+        self.outputs = self.grads.views + self.kept
+        self.buckets = layer_buckets(n_grads, per_bucket)
+        # gradients become ready in reverse layer order: issue the last bucket first
+        self.order = list(reversed(range(len(self.buckets))))
+        self.events = [torch.cuda.Event() for _ in range(n_grads)]
+        for e in self.events:
+            e.record()  # torch creates CUDA events lazily; the C ABI needs real handles
+        self.comm = torch.cuda.Stream(device=device) if world_size > 1 else None
+
+    def step(self, inputs, seed, stream=None):
+        import torch
+        st = stream or torch.cuda.current_stream(self.device)
+        self.fn.grad_run(inputs, seed=seed, outputs=self.outputs, stream=st.cuda_stream,
+                         events=self.events if self.comm is not None else None)
+        if self.comm is None:
+            return self.outputs
+        works = allreduce_buckets(self.grads, self.buckets, self.group, self.order, self.comm, self.events)
+        for w in works:
+            w.wait()  # makes the current stream wait for the collective
+        st.wait_stream(self.comm)
+        return self.outputs

@@ -400,3 +400,34 @@ def test_parse_errors(text):
 def test_verify_errors(text):
     with pytest.raises(VerifyError):
         oracle.parse(text)
+
+
+# --- bf16 policy helper (reading A15) ---------------------------------------
+
+def test_bf16_round_ties_to_even_and_torch():
+    from oracle.interp import bf16_round
+    one = 1.0
+    assert bf16_round(np.array([one]))[0] == 1.0
+    assert bf16_round(np.array([1 + 2.0 ** -8]))[0] == 1.0                  # tie -> even (down)
+    assert bf16_round(np.array([1 + 3 * 2.0 ** -8]))[0] == 1 + 2.0 ** -6    # tie -> even (up)
+    assert bf16_round(np.array([1 + 2.0 ** -8 + 2.0 ** -20]))[0] == 1 + 2.0 ** -7
+    import torch
+    x = np.random.default_rng(9).standard_normal(10000) * 10.0 ** np.random.default_rng(8).integers(-30, 30, 10000)
+    want = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(bf16_round(x), want)
+
+
+def test_bf16_policy_dot_exact_on_bf16_inputs():
+    """Under the bf16 policy a dot of bf16-representable operands equals the
+    unrounded dot (rounding is then the identity)."""
+    from oracle.interp import bf16_round
+    rng = np.random.default_rng(10)
+    a, b = bf16_round(rng.normal(size=(4, 6))), bf16_round(rng.normal(size=(6, 3)))
+    text = ('module "d"\nstage raw\nfunc @f: (<4 x 6 x f32>, <6 x 3 x f32>) -> <4 x 3 x f32> {\n'
+            "'entry(%a: <4 x 6 x f32>, %b: <6 x 3 x f32>):\n    %r = dot %a: <4 x 6 x f32>, %b: <6 x 3 x f32>\n"
+            "    return %r: <4 x 3 x f32>\n}\n")
+    m = oracle.parse(text)
+    np.testing.assert_array_equal(oracle.run(m, "f", [a, b], dot_policy="bf16")[0], a @ b)
+    c = a + 1e-3  # not bf16-representable: the policy result differs from the exact one
+    assert not np.array_equal(oracle.run(m, "f", [c, b], dot_policy="bf16")[0], c @ b)
+    np.testing.assert_array_equal(oracle.run(m, "f", [c, b], dot_policy="bf16")[0], bf16_round(c) @ b)
