@@ -104,8 +104,10 @@ dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_
                               dlvm_tensor* out_types);
 
 /* Text of the typed primal (which=0), the generated gradient function after
- * dead-code elimination (which=1) in the .dl syntax of Fig. 3, or the launch
- * plan of the primal (2) / gradient (3).  Writes at most `cap` bytes
+ * dead-code elimination (which=1) in the .dl syntax of Fig. 3, the launch
+ * plan of the primal (2) / gradient (3), or the element-wise program
+ * signatures of the primal (4) / gradient (5) launches (one per line, the
+ * keys of the compile-time specialisations).  Writes at most `cap` bytes
  * including the NUL; *needed receives the full size including the NUL. */
 dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);
 

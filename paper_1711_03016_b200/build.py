@@ -30,7 +30,7 @@ def sources():
 
 def headers():
     return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "kernels", "*.h"))
-            + glob.glob(os.path.join(CSRC, "kernels", "*.cuh")) + [os.path.join(ROOT, "include", "dlvm.h")])
+            + glob.glob(os.path.join(CSRC, "kernels", "*.cuh")) + glob.glob(os.path.join(CSRC, "kernels", "*.inc")) + [os.path.join(ROOT, "include", "dlvm.h")])
 
 
 def _compile(src: str, is_cu: bool, newest_header: float) -> str:

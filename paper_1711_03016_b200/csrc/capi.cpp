@@ -17,6 +17,7 @@
 #include "../../include/dlvm.h"
 #include "ir.h"
 #include "kernels/kernels.h"
+#include "kernels/spec_registry.h"
 #include "plan.h"
 
 using namespace dlvm;
@@ -30,6 +31,7 @@ struct dlvm_fn_s {
   dlvm_options opts{};
   int n_grads = 0;
   std::vector<void*> launch_events[2];
+  bool specialize = true;
 };
 
 namespace {
@@ -195,7 +197,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     if (st.kind == Step::EW) {
       EwParams p;
       to_dev(st.ew, b, &p);
-      e = launch_ew(p, st.ew.bx, st.ew.by, stream);
+      EwLaunchFn sf = fn->specialize ? find_ew_spec(st.ew.sig.c_str(), st.ew.vec) : nullptr;
+      e = sf ? sf(p, st.ew.bx, st.ew.by, stream) : launch_ew(p, st.ew.bx, st.ew.by, stream);
     } else if (st.kind == Step::GEMM) {
       const GemmStep& g = st.gemm;
       GemmParams gp;
@@ -221,8 +224,10 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);
       bool aligned = (reinterpret_cast<uintptr_t>(gp.a) % 16 == 0) && (reinterpret_cast<uintptr_t>(gp.b) % 16 == 0);
-      if (g.tensor_core && aligned && gp.bf16)
-        e = launch_gemm_tc(gp, stream);
+      if (g.tensor_core && aligned && gp.bf16) {
+        GemmLaunchFn sf = fn->specialize ? find_gemm_spec(g.epi.sig.c_str(), g.bn) : nullptr;
+        e = sf ? sf(gp, stream) : launch_gemm_tc(gp, stream);
+      }
       else {
         if (g.tensor_core) return fail(DLVM_ERR_RUNTIME, "tensor-core dot operand misaligned");
         e = launch_gemm_simt(gp, stream);
@@ -306,6 +311,7 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
     auto* h = new (std::nothrow) dlvm_fn_s;
     if (!h) return fail(DLVM_ERR_RUNTIME, "out of host memory");
     h->opts = o;
+    h->specialize = (o.flags & DLVM_NO_SPECIALIZE) == 0;
     h->primal = *src;
     if (decl) {
       h->grad = differentiate(*src, *decl->grad, decl->name);
@@ -373,8 +379,21 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
         s = fn->planned[w] ? fn->plan[w].str() : "unsupported: " + fn->plan_error[w] + "\n";
         break;
       }
+      case 4:
+      case 5: {
+        int w = which - 4;
+        if (w == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        if (!fn->planned[w]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[w]);
+        for (const Step& st : fn->plan[w].steps) {
+          if (st.kind == Step::EW)
+            s += "EW " + std::to_string(st.ew.vec) + " " + st.ew.sig + "\n";
+          else if (st.kind == Step::GEMM && st.gemm.tensor_core)
+            s += "GEMM " + std::to_string(st.gemm.bn) + " " + st.gemm.epi.sig + "\n";
+        }
+        break;
+      }
       default:
-        return fail(DLVM_ERR_USAGE, "which must be 0..3");
+        return fail(DLVM_ERR_USAGE, "which must be 0..5");
     }
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());

@@ -15,7 +15,13 @@
 // and rows r = (blockIdx.y*rpt + k)*by + ty, k < rpt.  With VEC = 4 every
 // full-stride operand moves as one 16-byte (f32) / 8-byte (bf16) / 4-byte
 // (bool) access per thread, coalesced across the warp.
-#include "ew_device.cuh"
+//
+// Two instantiations of the same body: P = void interprets p.prog (slots in
+// local memory); P = spec::Prog<...> is a compile-time program (registers).
+#include <type_traits>
+
+#include "ew_spec.cuh"
+#include "spec_registry.h"
 
 namespace dlvm {
 
@@ -27,9 +33,21 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
-template <int VEC>
+struct VmTraits {
+  static constexpr int kSlots = kMaxSlots;
+};
+
+template <class T, bool S>
+__host__ __device__ constexpr int num_red_slots() {
+  if constexpr (S) return T::Reds::n; else return kMaxReduces;
+}
+
+template <int VEC, class P>
 __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParams p) {
-  const EwProgram& P = p.prog;
+  constexpr bool SPEC = !std::is_void_v<P>;
+  using T = std::conditional_t<SPEC, spec::Traits<std::conditional_t<SPEC, P, spec::Prog<0, 0, spec::St<>, spec::Rd<>>>>, VmTraits>;
+  constexpr int NS = T::kSlots;
+  const EwProgram& Pg = p.prog;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int bx = blockDim.x, by = blockDim.y;
   const int nd = p.ndims;
@@ -38,20 +56,37 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   for (int d = 0; d < nd - 1; ++d) R *= p.dims[d];
   const int64_t c = ((int64_t)blockIdx.x * bx + tx) * VEC;
   const bool cval = c < C;
-  const int n_in = P.n_in;
-  float v[kMaxSlots][VEC];
-  for (int i = 0; i < P.n_lits; ++i)
+  const int n_in = SPEC ? 0 : Pg.n_in;
+  float v[NS][VEC];
+  if constexpr (SPEC) {
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) v[n_in + i][j] = P.lits[i];
-
-  bool has_row = false, has_colall = false;
-  for (int q = 0; q < P.n_reduces; ++q) {
-    has_row |= P.reduce_kind[q] == RED_ROW;
-    has_colall |= P.reduce_kind[q] != RED_ROW;
+    for (int i = 0; i < T::kLit; ++i)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[T::kIn + i][j] = Pg.lits[i];
+  } else {
+    for (int i = 0; i < Pg.n_lits; ++i)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[n_in + i][j] = Pg.lits[i];
   }
-  float acc[kMaxReduces][VEC];
+  const int n_red = SPEC ? 0 : Pg.n_reduces;
+  auto red_slot = [&](int q) -> int {
+    if constexpr (SPEC) return T::Reds::at(2 * q); else return Pg.reduce_slot[q];
+  };
+  auto red_kind = [&](int q) -> int {
+    if constexpr (SPEC) return T::Reds::at(2 * q + 1); else return Pg.reduce_kind[q];
+  };
+  constexpr int NRS = num_red_slots<T, SPEC>();
+  const int nred = SPEC ? NRS : n_red;
+  bool has_row = false, has_colall = false;
 #pragma unroll
-  for (int q = 0; q < kMaxReduces; ++q)
+  for (int q = 0; q < NRS; ++q)
+    if (q < nred) {
+      has_row |= red_kind(q) == RED_ROW;
+      has_colall |= red_kind(q) != RED_ROW;
+    }
+  float acc[NRS > 0 ? NRS : 1][VEC];
+#pragma unroll
+  for (int q = 0; q < (NRS > 0 ? NRS : 1); ++q)
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[q][j] = 0.f;
   __shared__ float red_s[256 * 4];
@@ -60,9 +95,9 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   for (int k = 0; k < p.rpt; ++k) {
     const int64_t r = ((int64_t)blockIdx.y * p.rpt + k) * by + ty;
     const bool valid = cval && r < R;
-    float rowv[kMaxReduces];
+    float rowv[NRS > 0 ? NRS : 1];
 #pragma unroll
-    for (int q = 0; q < kMaxReduces; ++q) rowv[q] = 0.f;
+    for (int q = 0; q < (NRS > 0 ? NRS : 1); ++q) rowv[q] = 0.f;
     if (valid) {
       int64_t idx[3] = {0, 0, 0};
       int64_t rr = r;
@@ -70,22 +105,38 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
         idx[d] = rr % p.dims[d];
         rr /= p.dims[d];
       }
-      for (int i = 0; i < n_in; ++i) {
+      auto load = [&](int i) {
         const EwDevIn& in = p.in[i];
         int64_t off = c * in.s[nd - 1];
         for (int d = 0; d < nd - 1; ++d) off += idx[d] * in.s[d];
         vm_load<VEC>(in, off, in.s[nd - 1], v[i]);
+      };
+      if constexpr (SPEC) {
+#pragma unroll
+        for (int i = 0; i < T::kIn; ++i) load(i);
+        T::template exec<VEC>(v);
+#pragma unroll
+        for (int s = 0; s < T::Stores::n; ++s) {
+          const EwDevOut& o = p.out[s];
+          int64_t off = c * o.s[nd - 1];
+          for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
+          vm_store<VEC>(o, off, o.s[nd - 1], v[T::Stores::at(s)]);
+        }
+      } else {
+        for (int i = 0; i < n_in; ++i) load(i);
+        vm_exec<VEC>(Pg, v);
+        for (int s = 0; s < Pg.n_stores; ++s) {
+          const EwDevOut& o = p.out[s];
+          int64_t off = c * o.s[nd - 1];
+          for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
+          vm_store<VEC>(o, off, o.s[nd - 1], v[Pg.store_slot[s]]);
+        }
       }
-      vm_exec<VEC>(P, v);
-      for (int s = 0; s < P.n_stores; ++s) {
-        const EwDevOut& o = p.out[s];
-        int64_t off = c * o.s[nd - 1];
-        for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
-        vm_store<VEC>(o, off, o.s[nd - 1], v[P.store_slot[s]]);
-      }
-      for (int q = 0; q < P.n_reduces; ++q) {
-        const float* x = v[P.reduce_slot[q]];
-        if (P.reduce_kind[q] == RED_ROW) {
+#pragma unroll
+      for (int q = 0; q < NRS; ++q) {
+        if (q >= nred) break;
+        const float* x = v[red_slot(q)];
+        if (red_kind(q) == RED_ROW) {
           float s = 0.f;
 #pragma unroll
           for (int j = 0; j < VEC; ++j) s = __fadd_rn(s, x[j]);
@@ -97,8 +148,9 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
       }
     }
     if (has_row) {  // block-uniform: every thread takes part
-      for (int q = 0; q < P.n_reduces; ++q) {
-        if (P.reduce_kind[q] != RED_ROW) continue;
+#pragma unroll
+      for (int q = 0; q < NRS; ++q) {
+        if (q >= nred || red_kind(q) != RED_ROW) continue;
         float s = warp_sum(rowv[q]);
         if ((tx & 31) == 0) row_s[ty][tx >> 5] = s;
         __syncthreads();
@@ -112,8 +164,10 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
     }
   }
   if (!has_colall) return;
-  for (int q = 0; q < P.n_reduces; ++q) {
-    const uint8_t kind = P.reduce_kind[q];
+#pragma unroll
+  for (int q = 0; q < NRS; ++q) {
+    if (q >= nred) break;
+    const int kind = red_kind(q);
     if (kind == RED_ROW) continue;
     if (kind == RED_COL) {
 #pragma unroll
@@ -159,14 +213,45 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* 
   for (; i < n; ++i) dst[i] = f2bf(src[i]);
 }
 
+template <int VEC, class P>
+cudaError_t launch_spec_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
+  dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
+  ew_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+// ---------------------------------------------------------- registry
+#define DLVM_SPEC_EW(VEC, SIG, ...) {SIG, VEC, &launch_spec_ew<VEC, __VA_ARGS__>},
+#define DLVM_SPEC_GEMM(IDX, BN, SIG, ...)
+namespace {
+using namespace spec;
+const EwSpecEntry kEwSpecs[] = {
+#include "spec_programs.inc"
+    {nullptr, 0, nullptr}};
+}  // namespace
+#undef DLVM_SPEC_EW
+#undef DLVM_SPEC_GEMM
+
+EwLaunchFn find_ew_spec(const char* sig, int vec) {
+  for (const EwSpecEntry* e = kEwSpecs; e->sig; ++e)
+    if (e->vec == vec && std::strcmp(e->sig, sig) == 0) return e->fn;
+  return nullptr;
+}
+
+int num_ew_specs() {
+  int n = 0;
+  for (const EwSpecEntry* e = kEwSpecs; e->sig; ++e) ++n;
+  return n;
+}
 
 cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
   dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
   if (p.vec == 4)
-    ew_kernel<4><<<grid, block, 0, stream>>>(p);
+    ew_kernel<4, void><<<grid, block, 0, stream>>>(p);
   else
-    ew_kernel<1><<<grid, block, 0, stream>>>(p);
+    ew_kernel<1, void><<<grid, block, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

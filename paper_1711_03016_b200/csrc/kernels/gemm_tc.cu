@@ -1,455 +1,38 @@
-// tcgen05 tensor-core GEMM for `dot` under the bf16 policy (K5 of SURVEY.md
-// §2.5; Table 1 "dot"; reading A15: bf16 operands, fp32 accumulation).
-//
-// C[M,N] = A[M,K] . B[K,N], bf16 operands read by TMA (cp.async.bulk.tensor,
-// 128-byte swizzle) into a 4-stage shared-memory ring guarded by mbarriers;
-// one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
-// N=BN, K=16) accumulating in TMEM (two BN-column accumulators so the
-// epilogue of tile i overlaps the main loop of tile i+1); four epilogue warps
-// read TMEM with tcgen05.ld.32x32b and run the fused element-wise epilogue
-// program (bias, activation, activation derivative, column/row/full partial
-// sums) before storing -- "linear algebra fusion" of P:L231-236 done on the
-// accumulator tile.  `transpose` of an operand is absorbed into the UMMA
-// descriptor major bit (A K- or M-major, B K- or N-major), so the adjoint
-// dots dY.W^T and X^T.dY read W and X in place.
-//
-// Warp roles (256 threads, persistent over tiles, 1 CTA/SM):
-//   warp 0: TMA producer   warp 1: MMA issuer   warp 2: TMEM allocator
-//   warps 4-7: epilogue (TMEM lanes 32*(warp%4) .. +31 = tile rows)
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
-#include <mutex>
-
-#include "ew_device.cuh"
+// tcgen05 GEMM entry points (kernel template in gemm_tc.cuh): the generic
+// instantiation whose epilogue interprets the planner's program, and the
+// lookup of compile-time epilogue specialisations (gemm_tc_spec*.cu).
+#include "gemm_tc.cuh"
 
 namespace dlvm {
 
-namespace {
-
-constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 256;
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-
-struct TcParams {
-  CUtensorMap tma_a;
-  CUtensorMap tma_b;
-  GemmParams g;
-  int32_t tiles_m, tiles_n;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
-                                            int32_t c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-// UMMA shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-// instruction descriptor for kind::f16: bf16 x bf16 -> f32, M=128, N=n
-__host__ __device__ constexpr uint32_t umma_idesc(int n, bool a_mn, bool b_mn) {
-  return (1u << 4)                       // D format f32
-         | (1u << 7)                     // A format bf16
-         | (1u << 10)                    // B format bf16
-         | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K)
-         | ((b_mn ? 1u : 0u) << 16)      // B major (0 = K)
-         | ((uint32_t)(n >> 3) << 17)    // N >> 3
-         | ((uint32_t)(BM >> 4) << 24);  // M >> 4
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-__device__ __forceinline__ float warp_sum(float x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
-  return x;
-}
-
-// 32 lanes x 32 columns -> lane l holds the sum over lanes of column l
-__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const bool upper = (lane & w) != 0;
-      float send = upper ? v[i] : v[i + w];
-      float keep = upper ? v[i + w] : v[i];
-      float recv = __shfl_xor_sync(0xffffffffu, send, w);
-      v[i] = __fadd_rn(keep, recv);
-    }
-  }
-  return v[0];
-}
-
-template <int BN>
-__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
-  constexpr int B_STAGE_BYTES = BN * BK * 2;
-  constexpr uint32_t STAGE_TX = A_STAGE_BYTES + B_STAGE_BYTES;
-  constexpr int TMEM_COLS = 2 * BN;  // 256 or 512
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sA = base;
-  const uint32_t sB = base + STAGES * A_STAGE_BYTES;
-  const uint32_t sBar = sB + STAGES * B_STAGE_BYTES;  // full[S], empty[S], tfull[2], tempty[2]
-  const uint32_t full_bar = sBar, empty_bar = sBar + 8 * STAGES, tfull_bar = sBar + 16 * STAGES,
-                 tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * STAGES + 32);
-  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * STAGES + 64);  // [kMaxReduces][4][BN]
-  float* allred = colred + kMaxReduces * 4 * BN;                                       // [4]
-
-  const GemmParams& g = P.g;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = P.tiles_m * P.tiles_n;
-  const int num_kb = (int)((g.K + BK - 1) / BK);
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(tfull_bar + 8 * s, 1);
-      mbar_init(tempty_bar + 8 * s, 128);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_b)) : "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int tm = t % P.tiles_m, tn = t / P.tiles_m;
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(empty_bar + 8 * s, ph ^ 1);
-          const uint32_t fb = full_bar + 8 * s;
-          mbar_expect_tx(fb, STAGE_TX);
-          const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
-          const int k0 = kb * BK;
-          if (g.a_kmajor) {
-            tma_load_2d(a_dst, &P.tma_a, fb, k0, m0);
-          } else {
-            tma_load_2d(a_dst, &P.tma_a, fb, m0, k0);
-            tma_load_2d(a_dst + 8192, &P.tma_a, fb, m0 + 64, k0);
-          }
-          if (g.b_kmajor) {
-            tma_load_2d(b_dst, &P.tma_b, fb, k0, n0);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, &P.tma_b, fb, n0 + 64 * c, k0);
-          }
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = umma_idesc(BN, !g.a_kmajor, !g.b_kmajor);
-      int s = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const int as = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(tempty_bar + 8 * as, aph ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(full_bar + 8 * s, ph);
-          tc_fence_after();
-          const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = g.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
-            const uint64_t bd = g.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
-          }
-          umma_commit(empty_bar + 8 * s);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-        umma_commit(tfull_bar + 8 * as);
-      }
-    }
-  } else if (warp >= 4) {  // ---------------- epilogue
-    const int q = warp & 3;           // TMEM lane quarter
-    const int et = threadIdx.x - 128;  // 0..127
-    const EwParams& E = g.epi;
-    const EwProgram& Pg = E.prog;
-    float v[kMaxSlots][4];
-    for (int i = 0; i < Pg.n_lits; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[Pg.n_in + i][j] = Pg.lits[i];
-    bool has_col = false, has_row = false, has_all = false;
-    for (int r = 0; r < Pg.n_reduces; ++r) {
-      has_col |= Pg.reduce_kind[r] == RED_COL;
-      has_row |= Pg.reduce_kind[r] == RED_ROW;
-      has_all |= Pg.reduce_kind[r] == RED_ALL;
-    }
-    int it = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const int tm = t % P.tiles_m, tn = t / P.tiles_m;
-      const int64_t m = (int64_t)tm * BM + 32 * q + lane;
-      const bool mval = m < g.M;
-      const int as = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(tfull_bar + 8 * as, aph);
-      tc_fence_after();
-      float rowacc[kMaxReduces] = {0.f, 0.f, 0.f, 0.f};
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        float acc[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * 32, acc);
-        const int64_t nb = (int64_t)tn * BN + ch * 32;
-        float rv[kMaxReduces][32];
-#pragma unroll
-        for (int gq = 0; gq < 8; ++gq) {
-          const int64_t n = nb + gq * 4;
-          const bool full4 = mval && n + 3 < g.N;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) v[0][j] = acc[gq * 4 + j];
-          if (full4 && E.vec == 4) {
-            for (int s = 1; s < Pg.n_in; ++s) vm_load<4>(E.in[s], m * E.in[s].s[0] + n * E.in[s].s[1], E.in[s].s[1], v[s]);
-          } else {
-            for (int s = 1; s < Pg.n_in; ++s)
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                v[s][j] = (mval && n + j < g.N) ? ld1(E.in[s].ptr, m * E.in[s].s[0] + (n + j) * E.in[s].s[1], E.in[s].st) : 0.f;
-          }
-          vm_exec<4>(Pg, v);
-          if (full4 && E.vec == 4) {
-            for (int s = 0; s < Pg.n_stores; ++s)
-              vm_store<4>(E.out[s], m * E.out[s].s[0] + n * E.out[s].s[1], E.out[s].s[1], v[Pg.store_slot[s]]);
-          } else if (mval) {
-            for (int s = 0; s < Pg.n_stores; ++s)
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (n + j < g.N) st1(E.out[s].ptr, m * E.out[s].s[0] + (n + j) * E.out[s].s[1], E.out[s].st, v[Pg.store_slot[s]][j]);
-          }
-          for (int r = 0; r < Pg.n_reduces; ++r)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) rv[r][gq * 4 + j] = (mval && n + j < g.N) ? v[Pg.reduce_slot[r]][j] : 0.f;
-        }
-        for (int r = 0; r < Pg.n_reduces; ++r) {
-          const uint8_t kind = Pg.reduce_kind[r];
-          float tmp[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) tmp[i] = rv[r][i];
-          if (kind == RED_COL) {
-            float cs = transpose_reduce32(tmp, lane);
-            colred[(r * 4 + q) * BN + ch * 32 + lane] = cs;
-          } else {
-            float s = 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) s = __fadd_rn(s, tmp[i]);
-            rowacc[r] = __fadd_rn(rowacc[r], s);
-          }
-        }
-      }
-      // accumulator buffer free for the next tile's MMAs
-      tc_fence_before();
-      mbar_arrive(tempty_bar + 8 * as);
-      if (has_row && mval)
-        for (int r = 0; r < Pg.n_reduces; ++r)
-          if (Pg.reduce_kind[r] == RED_ROW) E.red[r][m * E.gx + tn] = rowacc[r];
-      if (has_col || has_all) {
-        for (int r = 0; r < Pg.n_reduces; ++r) {
-          if (Pg.reduce_kind[r] != RED_ALL) continue;
-          float s = warp_sum(rowacc[r]);
-          if (lane == 0) allred[r * 4 + q] = s;
-        }
-        epi_bar();
-        for (int r = 0; r < Pg.n_reduces; ++r) {
-          if (Pg.reduce_kind[r] == RED_COL) {
-            for (int c = et; c < BN; c += 128) {
-              const int64_t n = (int64_t)tn * BN + c;
-              if (n >= g.N) continue;
-              float s = 0.f;
-              for (int w = 0; w < 4; ++w) s = __fadd_rn(s, colred[(r * 4 + w) * BN + c]);
-              E.red[r][(int64_t)tm * g.N + n] = s;
-            }
-          } else if (Pg.reduce_kind[r] == RED_ALL && et == 0) {
-            float s = 0.f;
-            for (int w = 0; w < 4; ++w) s = __fadd_rn(s, allred[r * 4 + w]);
-            E.red[r][(int64_t)tm * E.gx + tn] = s;
-          }
-        }
-        epi_bar();
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
-  }
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
-// 2-D bf16 tensor map: inner dim (contiguous) `inner`, outer dim `outer`
-// with row pitch `ld` elements, box {64, box_outer}, 128-byte swizzle
-bool encode(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
-  auto fn = get_encode();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {64u, (cuuint32_t)box_outer};
-  cuuint32_t es[2] = {1u, 1u};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-template <int BN>
-constexpr int smem_bytes() {
-  return 1024 + STAGES * (A_STAGE_BYTES + BN * BK * 2) + 16 * STAGES + 64 + (kMaxReduces * 4 * BN + 16) * 4;
-}
-
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
-template <int BN>
-cudaError_t launch_bn(TcParams& tp, cudaStream_t stream) {
-  static bool configured = false;
-  constexpr int SMEM = smem_bytes<BN>();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  const int tiles = tp.tiles_m * tp.tiles_n;
-  const int grid = std::min(tiles, num_sms());
-  gemm_tc_kernel<BN><<<grid, NUM_THREADS, SMEM, stream>>>(tp);
-  return cudaGetLastError();
-}
-
-}  // namespace
+const GemmSpecEntry* gemm_spec_table_0();
+const GemmSpecEntry* gemm_spec_table_1();
+const GemmSpecEntry* gemm_spec_table_2();
+const GemmSpecEntry* gemm_spec_table_3();
 
 bool gemm_tc_available() { return get_encode() != nullptr; }
 
 cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream) {
-  TcParams tp;
-  memset(&tp, 0, sizeof(tp));
-  tp.g = p;
-  const int BN = p.bn;
-  bool ok;
-  if (p.a_kmajor)  // A [M,K], K contiguous: map {K, M}, box {64, 128}
-    ok = encode(&tp.tma_a, p.a, p.K, p.M, p.a_s0, BM);
-  else  // A stored [K][M]: map {M, K}, box {64, 64}
-    ok = encode(&tp.tma_a, p.a, p.M, p.K, p.a_s1, 64);
-  if (!ok) return cudaErrorInvalidValue;
-  if (p.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN}
-    ok = encode(&tp.tma_b, p.b, p.K, p.N, p.b_s1, BN);
-  else  // B stored [K][N]: map {N, K}, box {64, 64}
-    ok = encode(&tp.tma_b, p.b, p.N, p.K, p.b_s0, 64);
-  if (!ok) return cudaErrorInvalidValue;
-  tp.tiles_m = (int)((p.M + BM - 1) / BM);
-  tp.tiles_n = (int)((p.N + BN - 1) / BN);
-  if (BN == 256) return launch_bn<256>(tp, stream);
-  return launch_bn<128>(tp, stream);
+  if (p.bn == 256) return launch_prog<256, void>(p, stream);
+  return launch_prog<128, void>(p, stream);
+}
+
+GemmLaunchFn find_gemm_spec(const char* sig, int bn) {
+  const GemmSpecEntry* tabs[4] = {gemm_spec_table_0(), gemm_spec_table_1(), gemm_spec_table_2(),
+                                  gemm_spec_table_3()};
+  for (auto* t : tabs)
+    for (const GemmSpecEntry* e = t; e->sig; ++e)
+      if (e->fn && e->bn == bn && std::strcmp(e->sig, sig) == 0) return e->fn;
+  return nullptr;
+}
+
+int num_gemm_specs() {
+  int n = 0;
+  const GemmSpecEntry* tabs[4] = {gemm_spec_table_0(), gemm_spec_table_1(), gemm_spec_table_2(),
+                                  gemm_spec_table_3()};
+  for (auto* t : tabs)
+    for (const GemmSpecEntry* e = t; e->sig; ++e) n += e->fn != nullptr;
+  return n;
 }
 
 }  // namespace dlvm

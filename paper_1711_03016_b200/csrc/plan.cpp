@@ -40,6 +40,19 @@ bool TensorRef::contiguous() const {
   return nchunks == 1;
 }
 
+std::string program_signature(const EwProgram& p) {
+  std::ostringstream o;
+  o << "i" << (int)p.n_in << "l" << (int)p.n_lits << "|";
+  for (int k = 0; k < p.n_ins; ++k)
+    o << (k ? ";" : "") << (int)p.ins[k].op << "," << (int)p.ins[k].a << "," << (int)p.ins[k].b << ","
+      << (int)p.ins[k].c;
+  o << "|s";
+  for (int k = 0; k < p.n_stores; ++k) o << (k ? "," : "") << (int)p.store_slot[k];
+  o << "|r";
+  for (int k = 0; k < p.n_reduces; ++k) o << (k ? "," : "") << (int)p.reduce_slot[k] << ":" << (int)p.reduce_kind[k];
+  return o.str();
+}
+
 int Plan::launches() const {
   int n = 0;
   for (auto& s : steps) n += (s.kind == Step::EW || s.kind == Step::GEMM) ? 1 : 0;
@@ -739,9 +752,10 @@ struct Planner {
     plan.bufs.clear();
     plan.workspace_bytes = 0;
     // group_use: read by a (non-dot) kernel, through views
-    for (auto& n : nodes) {
+    for (auto& n : nodes) {  // reads by another kernel (values a group stores itself stay in registers)
       if (n.is_dot || n.merged_into >= 0) continue;
-      for (int v : n.reads) vi[v].group_use = true;
+      for (int v : n.reads)
+        if (!n.stored.count(v)) vi[v].group_use = true;
     }
     for (int i = 0; i < f.num_args(); ++i) {
       bool seed = plan.seed_is_input && i == f.num_args() - 1;
@@ -1218,6 +1232,7 @@ struct Planner {
       }
       fg.prog.n_stores = (uint8_t)fg.stores.size();
       ew_launch(fg);
+      fg.sig = program_signature(fg.prog);
       Step s;
       s.kind = Step::EW;
       s.ew = fg;
@@ -1262,6 +1277,7 @@ struct Planner {
         s.ew.prog.reduce_kind[ri.slot_index] = ri.kind;
       }
       ew_launch(s.ew);
+      s.ew.sig = program_signature(s.ew.prog);
       int64_t C = s.ew.dims[s.ew.ndims - 1], R = 1;
       for (int d = 0; d < s.ew.ndims - 1; ++d) R *= s.ew.dims[d];
       std::ostringstream d;
@@ -1339,6 +1355,7 @@ struct Planner {
     int64_t gx = (gm.N + gm.bn - 1) / gm.bn, gy = (gm.M + gm.bm - 1) / gm.bm;
     gm.epi.gx = gx;
     gm.epi.gy = gy;
+    gm.epi.sig = program_signature(gm.epi.prog);
     std::ostringstream d;
     d << (gm.tensor_core ? "gemm tcgen05 bf16" : (bf ? "gemm simt bf16" : "gemm simt f32")) << " %"
       << f.names[dv] << " M=" << gm.M << " N=" << gm.N << " K=" << gm.K << " A:" << (gm.a_kmajor ? "K" : "M")

@@ -74,6 +74,7 @@ struct EwGroup {
   std::vector<IterRef> stores;   // prog.stores[k] -> stores[k]
   std::vector<IterRef> reduces;  // prog.reduces[k] -> partial buffer (contiguous)
   std::string desc;
+  std::string sig;               // program_signature(prog): key of compile-time specialisations
 };
 
 struct GemmStep {
@@ -119,5 +120,10 @@ struct PlanOptions {
 };
 
 Plan make_plan(const Function& f, const PlanOptions& opt);
+
+// "i<n_in>l<n_lits>|op,a,b,c;...|s<slot>,...|r<slot>:<kind>,..." -- everything
+// about a program that is fixed at compile time in a specialisation
+// (pointers, strides, sizes, storage types and literal values are not).
+std::string program_signature(const EwProgram& p);
 
 }  // namespace dlvm

@@ -284,3 +284,22 @@ def test_random_programs(seed):
     emu = f32_emulation(gm, "g", ins64)   # fp32 conditioning of this random program
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, bg, emu)):
         assert_f32_parity(g, r, b, what=f"random grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
+
+
+@pytest.mark.parametrize("case", ["c2", "c3", "c5"])
+def test_specialized_programs_bit_identical_to_interpreter(case):
+    """Compile-time specialised programs (spec_programs.inc) and the generic
+    interpreter evaluate the same ops in the same order: bit-identical."""
+    import paper_1711_03016_b200 as P
+    if case == "c2":
+        w, prec = W.c2(256, 4096), "f32"
+    elif case == "c3":
+        w, prec = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)]), "bf16"
+    else:
+        w, prec = W._mlp_workload(5, "c5s", 256, [(512, 512, "tanh")] * 2, ("normal",), ("uniform", -0.5, 0.5),
+                                  1.0 / 256, "bf16", 256), "bf16"
+    ins = w.inputs()
+    a = gpu_run(w.text, w.fn, w.grad, ins, seed=w.seed(), dot_precision=prec)
+    b = gpu_run(w.text, w.fn, w.grad, ins, seed=w.seed(), dot_precision=prec, flags=P.DLVM_NO_SPECIALIZE)
+    for x, y in zip(a["primal"] + a["grad"], b["primal"] + b["grad"]):
+        np.testing.assert_array_equal(x, y)
