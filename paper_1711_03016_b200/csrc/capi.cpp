@@ -197,8 +197,12 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     if (st.kind == Step::EW) {
       EwParams p;
       to_dev(st.ew, b, &p);
-      EwLaunchFn sf = fn->specialize ? find_ew_spec(st.ew.sig.c_str(), st.ew.vec) : nullptr;
-      e = sf ? sf(p, st.ew.bx, st.ew.by, stream) : launch_ew(p, st.ew.bx, st.ew.by, stream);
+      if (st.ew.finalize) {
+        e = launch_finalize(p, stream);
+      } else {
+        EwLaunchFn sf = fn->specialize ? find_ew_spec(st.ew.sig.c_str(), st.ew.vec) : nullptr;
+        e = sf ? sf(p, st.ew.bx, st.ew.by, stream) : launch_ew(p, st.ew.bx, st.ew.by, stream);
+      }
     } else if (st.kind == Step::GEMM) {
       const GemmStep& g = st.gemm;
       GemmParams gp;

@@ -200,6 +200,42 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   }
 }
 
+// Deterministic finalize of reduction partials: out[e] = sum_k P[k*cs + e*es]
+// in a fixed order (threadIdx.y strides the chunks, then a fixed-order sum
+// over threadIdx.y), written to every home of the reduced value.
+__global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EwParams p) {
+  __shared__ float part[256];
+  const int ex = blockDim.x, cy = blockDim.y;
+  const int64_t e = (int64_t)blockIdx.x * ex + threadIdx.x;
+  const EwDevIn& in = p.in[0];
+  const float* P = reinterpret_cast<const float*>(in.ptr);
+  float s = 0.f;
+  if (e < p.dims[0]) {
+    const float* q = P + e * in.s[0];
+    int k = threadIdx.y;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (; k + 3 * cy < in.nchunks; k += 4 * cy) {
+      a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
+      a1 = __fadd_rn(a1, __ldg(q + (int64_t)(k + cy) * in.chunk_stride));
+      a2 = __fadd_rn(a2, __ldg(q + (int64_t)(k + 2 * cy) * in.chunk_stride));
+      a3 = __fadd_rn(a3, __ldg(q + (int64_t)(k + 3 * cy) * in.chunk_stride));
+    }
+    for (; k < in.nchunks; k += cy) a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
+    s = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
+  }
+  part[threadIdx.y * ex + threadIdx.x] = s;
+  __syncthreads();
+  for (int w = cy / 2; w > 0; w >>= 1) {  // fixed-order tree over threadIdx.y
+    if (threadIdx.y < w) part[threadIdx.y * ex + threadIdx.x] =
+        __fadd_rn(part[threadIdx.y * ex + threadIdx.x], part[(threadIdx.y + w) * ex + threadIdx.x]);
+    __syncthreads();
+  }
+  if (threadIdx.y == 0 && e < p.dims[0]) {
+    const float t = part[threadIdx.x];
+    for (int o = 0; o < p.prog.n_stores; ++o) st1(p.out[o].ptr, e * p.out[o].s[0], p.out[o].st, t);
+  }
+}
+
 __global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* __restrict__ dst, int64_t n) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
@@ -252,6 +288,14 @@ cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
     ew_kernel<4, void><<<grid, block, 0, stream>>>(p);
   else
     ew_kernel<1, void><<<grid, block, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream) {
+  const int64_t n = p.dims[0];
+  dim3 block = n >= 32 ? dim3(32, 8) : dim3(1, 256);
+  dim3 grid((unsigned)((n + block.x - 1) / block.x));
+  finalize_kernel<<<grid, block, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

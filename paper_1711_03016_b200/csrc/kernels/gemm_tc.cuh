@@ -16,7 +16,8 @@
 //
 // Warp roles (256 threads, persistent over tiles, 1 CTA/SM):
 //   warp 0: TMA producer   warp 1: MMA issuer   warp 2: TMEM allocator
-//   warps 4-7: epilogue (TMEM lanes 32*(warp%4) .. +31 = tile rows)
+//   warps 4-11: epilogue (TMEM lanes 32*(warp%4) .. +31 = tile rows; two
+//               warps per lane quarter split the tile's column chunks)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,7 +32,7 @@ namespace dlvm {
 
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 256;
+constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 384;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
@@ -124,7 +125,77 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// RV consecutive rows m0.. of column n of an epilogue operand: one storage-
+// type branch and one 64-bit offset per batch; rows >= nrow are skipped.
+template <int RV>
+__device__ __forceinline__ void epi_load(const EwDevIn& in, int64_t m0, int64_t n, int nrow, float* v) {
+  const int64_t base = m0 * in.s[0] + n * in.s[1];
+  const int64_t rs = in.s[0];
+  if (in.st == (uint8_t)SType::F32) {
+    const float* p = reinterpret_cast<const float*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = j < nrow ? __ldg(p + j * rs) : 0.f;
+  } else if (in.st == (uint8_t)SType::BF16) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = j < nrow ? __uint_as_float(((unsigned)__ldg(p + j * rs)) << 16) : 0.f;
+  } else {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = (j < nrow && __ldg(p + j * rs)) ? 1.f : 0.f;
+  }
+}
+
+template <int RV>
+__device__ __forceinline__ void epi_store(const EwDevOut& o, int64_t m0, int64_t n, int nrow, const float* v) {
+  const int64_t base = m0 * o.s[0] + n * o.s[1];
+  const int64_t rs = o.s[0];
+  if (o.st == (uint8_t)SType::F32) {
+    float* p = reinterpret_cast<float*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = v[j];
+  } else if (o.st == (uint8_t)SType::BF16) {
+    unsigned short* p = reinterpret_cast<unsigned short*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = f2bf(v[j]);
+  } else {
+    unsigned char* p = reinterpret_cast<unsigned char*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = v[j] != 0.f ? 1 : 0;
+  }
+}
+
+// Tile raster: groups of GROUP_M tile-rows, N fastest inside a group, so the
+// ~148 tiles in flight share a few A row-panels and all of B through L2
+// (a plain M-fastest order re-reads A once per N tile).
+constexpr int GROUP_M = 8;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int* tm, int* tn) {
+  const int per_group = GROUP_M * tiles_n;
+  const int grp = t / per_group;
+  const int first = grp * GROUP_M;
+  const int gsz = min(GROUP_M, tiles_m - first);
+  const int r = t - grp * per_group;
+  *tm = first + r % gsz;
+  *tn = r / gsz;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
@@ -148,9 +219,11 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
   return v[0];
 }
 
+constexpr int kEpiReds = 2;  // reductions per GEMM epilogue (smem budget); more -> not fused
+
 template <class T, bool S>
 __host__ __device__ constexpr int epi_num_reds() {
-  if constexpr (S) return T::Reds::n; else return kMaxReduces;
+  if constexpr (S) return T::Reds::n; else return kEpiReds;
 }
 
 struct VmEpiTraits {
@@ -177,9 +250,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const uint32_t full_bar = sBar, empty_bar = sBar + 8 * STAGES, tfull_bar = sBar + 16 * STAGES,
                  tempty_bar = tfull_bar + 16;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * STAGES + 32);
-  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * STAGES + 64);  // [kMaxReduces][4][BN]
-  float* allred = colred + kMaxReduces * 4 * BN;                                       // [kMaxReduces][4]
-  float* xpose = allred + kMaxReduces * 4;                                             // [4][32][33]
+  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * STAGES + 64);  // [kEpiReds][4][BN]
+  float* rowred = colred + kEpiReds * 4 * BN;                                          // [kEpiReds][2][BM]
+  float* allred = rowred + kEpiReds * 2 * BM;                                          // [kEpiReds][8]
+  float* xpose = allred + kEpiReds * 8;                                                // [8][32][17]
 
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -193,7 +267,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + 8 * s, 1);
-      mbar_init(tempty_bar + 8 * s, 128);
+      mbar_init(tempty_bar + 8 * s, 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_a)) : "memory");
@@ -214,7 +288,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int tm = t % P.tiles_m, tn = t / P.tiles_m;
+        int tm, tn;
+        tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(empty_bar + 8 * s, ph ^ 1);
@@ -273,22 +348,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
-    // Each warp owns 32 accumulator rows (TMEM lanes 32q..32q+31).  A 32x32
-    // chunk is transposed through shared memory so that lane l then handles
-    // column l of all 32 rows: every load/store of an [M, N] operand is a
-    // coalesced 32-element row segment, bias rows are one value per lane, and
-    // column sums accumulate in registers.
-    const int q = warp & 3;
-    const int et = threadIdx.x - 128;  // 0..127
+    // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (tile rows) and the
+    // 16-column chunks ch = h, h+2, ...  A 32x16 chunk is transposed through
+    // shared memory so lane l handles column l%16 of rows 16*(l/16)..+15,
+    // RV rows at a time in registers: every load/store of an [M, N] operand
+    // is a coalesced 16-element row segment and RV independent loads are in
+    // flight per lane; column sums accumulate in registers.
+    const int ew = warp - 4;
+    const int q = ew & 3, h = ew >> 2;
+    const int et = threadIdx.x - 128;  // 0..255
+    const int col = lane & 15, rg = lane >> 4;
     const EwParams& E = g.epi;
     const EwProgram& Pg = E.prog;
-    float* X = xpose + q * 32 * 33;
-    float v[NS][1];
+    float* X = xpose + ew * 32 * 17;
+    constexpr int RV = SPEC ? (NS <= 12 ? 8 : 4) : 4;
+    float v[NS][RV];
     if constexpr (SPEC) {
 #pragma unroll
-      for (int i = 0; i < T::kLit; ++i) v[T::kIn + i][0] = Pg.lits[i];
+      for (int i = 0; i < T::kLit; ++i)
+#pragma unroll
+        for (int j = 0; j < RV; ++j) v[T::kIn + i][j] = Pg.lits[i];
     } else {
-      for (int i = 0; i < Pg.n_lits; ++i) v[Pg.n_in + i][0] = Pg.lits[i];
+      for (int i = 0; i < Pg.n_lits; ++i)
+#pragma unroll
+        for (int j = 0; j < RV; ++j) v[Pg.n_in + i][j] = Pg.lits[i];
     }
     auto red_slot = [&](int r) -> int {
       if constexpr (SPEC) return T::Reds::at(2 * r); else return Pg.reduce_slot[r];
@@ -307,8 +390,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       }
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-      const int tm = t % P.tiles_m, tn = t / P.tiles_m;
-      const int64_t mb = (int64_t)tm * BM + 32 * q;  // first row of this warp's slab
+      int tm, tn;
+      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      const int64_t mb = (int64_t)tm * BM + 32 * q + 16 * rg;  // first row of this lane's 16
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull_bar + 8 * as, aph);
@@ -316,95 +400,106 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
 #pragma unroll
       for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        float acc[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * 32, acc);
+      for (int ch = h; ch < BN / 16; ch += 2) {
+        float acc[16];
+        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * 16, acc);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) X[lane * 33 + j] = acc[j];
+        for (int j = 0; j < 16; ++j) X[lane * 17 + j] = acc[j];
         __syncwarp();
-        const int64_t n = (int64_t)tn * BN + ch * 32 + lane;
+        const int64_t n = (int64_t)tn * BN + ch * 16 + col;
         const bool nval = n < g.N;
         float colacc[NRS > 0 ? NRS : 1];
 #pragma unroll
         for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) colacc[r] = 0.f;
-#pragma unroll 2
-        for (int rr = 0; rr < 32; ++rr) {
-          const int64_t m = mb + rr;
-          const bool ok = nval && m < g.M;
-          float rv[NRS > 0 ? NRS : 1];
 #pragma unroll
-          for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rv[r] = 0.f;
-          if (ok) {
-            v[0][0] = X[rr * 33 + lane];
-            if constexpr (SPEC) {
+        for (int b = 0; b < 16 / RV; ++b) {
+          const int64_t m0 = mb + b * RV;
 #pragma unroll
-              for (int s = 1; s < T::kIn; ++s) v[s][0] = ld1(E.in[s].ptr, m * E.in[s].s[0] + n * E.in[s].s[1], E.in[s].st);
-              T::template exec<1>(v);
+          for (int j = 0; j < RV; ++j) v[0][j] = X[(16 * rg + b * RV + j) * 17 + col];
+          // rows m0..m0+RV-1 valid?  (uniform fast path when the whole batch is inside)
+          const int64_t left = g.M - m0;
+          const int nrow = !nval ? 0 : (left >= RV ? RV : (left > 0 ? (int)left : 0));
+          if constexpr (SPEC) {
 #pragma unroll
-              for (int s = 0; s < T::Stores::n; ++s)
-                st1(E.out[s].ptr, m * E.out[s].s[0] + n * E.out[s].s[1], E.out[s].st, v[T::Stores::at(s)][0]);
-            } else {
-              for (int s = 1; s < Pg.n_in; ++s) vm_load<1>(E.in[s], m * E.in[s].s[0] + n * E.in[s].s[1], 0, v[s]);
-              vm_exec<1>(Pg, v);
-              for (int s = 0; s < Pg.n_stores; ++s)
-                st1(E.out[s].ptr, m * E.out[s].s[0] + n * E.out[s].s[1], E.out[s].st, v[Pg.store_slot[s]][0]);
-            }
+            for (int s = 1; s < T::kIn; ++s) epi_load<RV>(E.in[s], m0, n, nrow, v[s]);
+            T::template exec<RV>(v);
 #pragma unroll
-            for (int r = 0; r < NRS; ++r)
-              if (r < nred) rv[r] = v[red_slot(r)][0];
+            for (int s = 0; s < T::Stores::n; ++s) epi_store<RV>(E.out[s], m0, n, nrow, v[T::Stores::at(s)]);
+          } else {
+            for (int s = 1; s < Pg.n_in; ++s) epi_load<RV>(E.in[s], m0, n, nrow, v[s]);
+            vm_exec<RV>(Pg, v);
+            for (int s = 0; s < Pg.n_stores; ++s) epi_store<RV>(E.out[s], m0, n, nrow, v[Pg.store_slot[s]]);
           }
+          bool okj[RV];
+#pragma unroll
+          for (int j = 0; j < RV; ++j) okj[j] = j < nrow;
 #pragma unroll
           for (int r = 0; r < NRS; ++r) {
             if (r >= nred) break;
             const int kind = red_kind(r);
-            if (kind == RED_COL) {
-              colacc[r] = __fadd_rn(colacc[r], rv[r]);
-            } else if (kind == RED_ROW) {
-              const float s = warp_sum(rv[r]);
-              if (lane == rr) rowacc[r] = __fadd_rn(rowacc[r], s);
-            } else {
-              allacc[r] = __fadd_rn(allacc[r], rv[r]);
+            const int sl = red_slot(r);
+#pragma unroll
+            for (int j = 0; j < RV; ++j) {
+              const float x = okj[j] ? v[sl][j] : 0.f;
+              if (kind == RED_COL) {
+                colacc[r] = __fadd_rn(colacc[r], x);
+              } else if (kind == RED_ALL) {
+                allacc[r] = __fadd_rn(allacc[r], x);
+              } else {  // row sum over this chunk's 16 columns (lanes of the same row group)
+                float s = x;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+                if ((lane & 15) == b * RV + j) rowacc[r] = __fadd_rn(rowacc[r], s);
+              }
             }
           }
         }
         if (has_col) {
 #pragma unroll
-          for (int r = 0; r < NRS; ++r)
-            if (r < nred && red_kind(r) == RED_COL) colred[(r * 4 + q) * BN + ch * 32 + lane] = colacc[r];
+          for (int r = 0; r < NRS; ++r) {
+            if (r >= nred || red_kind(r) != RED_COL) continue;
+            const float s = __fadd_rn(colacc[r], __shfl_xor_sync(0xffffffffu, colacc[r], 16));
+            if (lane < 16) colred[(r * 4 + q) * BN + ch * 16 + lane] = s;  // rows 32q..32q+31
+          }
         }
         __syncwarp();
       }
       // accumulator buffer free for the next tile's MMAs
       tc_fence_before();
       mbar_arrive(tempty_bar + 8 * as);
-      if (has_row) {
-        const int64_t m = mb + lane;
-#pragma unroll
-        for (int r = 0; r < NRS; ++r)
-          if (r < nred && red_kind(r) == RED_ROW && m < g.M) E.red[r][m * E.gx + tn] = rowacc[r];
-      }
-      if (has_col || has_all) {
+      if (has_row || has_all) {
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
-          if (r >= nred || red_kind(r) != RED_ALL) continue;
-          const float s = warp_sum(allacc[r]);
-          if (lane == 0) allred[r * 4 + q] = s;
+          if (r >= nred) break;
+          if (red_kind(r) == RED_ROW) rowred[(r * 2 + h) * BM + 32 * q + 16 * rg + (lane & 15)] = rowacc[r];
+          if (red_kind(r) == RED_ALL) {
+            const float s = warp_sum(allacc[r]);
+            if (lane == 0) allred[r * 8 + ew] = s;
+          }
         }
+      }
+      if (has_col || has_row || has_all) {
         epi_bar();
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
           if (r >= nred) break;
-          if (red_kind(r) == RED_COL) {
-            for (int c = et; c < BN; c += 128) {
+          const int kind = red_kind(r);
+          if (kind == RED_COL) {
+            for (int c = et; c < BN; c += 256) {
               const int64_t n = (int64_t)tn * BN + c;
               if (n >= g.N) continue;
               float s = 0.f;
               for (int w = 0; w < 4; ++w) s = __fadd_rn(s, colred[(r * 4 + w) * BN + c]);
               E.red[r][(int64_t)tm * g.N + n] = s;
             }
-          } else if (red_kind(r) == RED_ALL && et == 0) {
+          } else if (kind == RED_ROW) {
+            if (et < BM) {
+              const int64_t m = (int64_t)tm * BM + et;
+              if (m < g.M) E.red[r][m * E.gx + tn] = __fadd_rn(rowred[(r * 2) * BM + et], rowred[(r * 2 + 1) * BM + et]);
+            }
+          } else if (et == 0) {
             float s = 0.f;
-            for (int w = 0; w < 4; ++w) s = __fadd_rn(s, allred[r * 4 + w]);
+            for (int w = 0; w < 8; ++w) s = __fadd_rn(s, allred[r * 8 + w]);
             E.red[r][(int64_t)tm * E.gx + tn] = s;
           }
         }
@@ -451,7 +546,7 @@ bool encode(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int
 template <int BN>
 constexpr int smem_bytes() {
   return 1024 + STAGES * (A_STAGE_BYTES + BN * BK * 2) + 16 * STAGES + 64 +
-         (kMaxReduces * 4 * BN + kMaxReduces * 4 + 4 * 32 * 33) * 4;
+         (kEpiReds * 4 * BN + kEpiReds * 2 * BM + kEpiReds * 8 + 8 * 32 * 17) * 4;
 }
 
 int num_sms() {

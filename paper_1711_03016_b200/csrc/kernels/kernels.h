@@ -56,6 +56,9 @@ cudaError_t launch_gemm_simt(const GemmParams& p, cudaStream_t stream);
 cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream);
 bool gemm_tc_available();
 
+// sum of reduction partials (p.in[0] with nchunks > 1) into p.out[*]
+cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream);
+
 cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
 
 }  // namespace dlvm

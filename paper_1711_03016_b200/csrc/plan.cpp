@@ -83,6 +83,7 @@ size_t stype_size(SType t) { return t == SType::F32 ? 4 : t == SType::BF16 ? 2 :
 [[noreturn]] void unsupported(const std::string& m) { throw Error(kStatusUnsupported, 0, 0, m); }
 
 using Map = std::vector<int>;  // value dim -> iteration dim, or -1 (index 0)
+constexpr int kGemmEpiReds = 2;  // gemm_tc.cuh kEpiReds
 
 Map identity(int r) {
   Map m(r);
@@ -701,6 +702,9 @@ struct Planner {
         for (int v : G.inl)
           if (is_view(def(v)) && def(v)->ops[0].value == dv) via_view = true;
         if (via_view) break;
+        int n_red = 0;  // the GEMM epilogue has smem for kGemmEpiReds reductions
+        for (auto& r : G.roots) n_red += r.kind == Root::Reduce;
+        if (n_red > kGemmEpiReds) break;
         bool ok = true;
         for (int v : G.reads) {
           if (v == dv) continue;
@@ -1233,6 +1237,7 @@ struct Planner {
       fg.prog.n_stores = (uint8_t)fg.stores.size();
       ew_launch(fg);
       fg.sig = program_signature(fg.prog);
+      fg.finalize = true;
       Step s;
       s.kind = Step::EW;
       s.ew = fg;

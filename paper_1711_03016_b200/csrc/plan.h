@@ -75,6 +75,7 @@ struct EwGroup {
   std::vector<IterRef> reduces;  // prog.reduces[k] -> partial buffer (contiguous)
   std::string desc;
   std::string sig;               // program_signature(prog): key of compile-time specialisations
+  bool finalize = false;         // sum of reduction partials (dedicated kernel)
 };
 
 struct GemmStep {

@@ -166,7 +166,7 @@ def test_tcgen05_dot_majors(M, K, N, ta, tb):
     assert_f32_parity(res["primal"][0], ref, np.abs(A) @ np.abs(B), what=f"dot {M}x{K}x{N} ta={ta} tb={tb}")
 
 
-def _check_c3(w, policy_tol=1e-3):
+def _check_c3(w, policy_tol=2e-2):
     """bf16 policy (reading A15).  Network-level parity is checked against the
     oracle under the same policy (every dot operand rounded to bf16, float64
     arithmetic): the unrounded comparison is ill-conditioned for gradients
