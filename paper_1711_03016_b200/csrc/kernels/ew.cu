@@ -92,74 +92,119 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   __shared__ float red_s[256 * 4];
   __shared__ float row_s[8][8];
 
-  for (int k = 0; k < p.rpt; ++k) {
-    const int64_t r = ((int64_t)blockIdx.y * p.rpt + k) * by + ty;
-    const bool valid = cval && r < R;
-    float rowv[NRS > 0 ? NRS : 1];
+  // rows handled per loop iteration: specialised programs load RPI rows
+  // before computing, so 2*VEC independent 16-byte loads per input are in flight
+  constexpr int RPI = SPEC ? 2 : 1;
+  for (int k = 0; k < p.rpt; k += RPI) {
+    int64_t rrow[RPI];
+    bool vrow[RPI];
 #pragma unroll
-    for (int q = 0; q < (NRS > 0 ? NRS : 1); ++q) rowv[q] = 0.f;
-    if (valid) {
-      int64_t idx[3] = {0, 0, 0};
-      int64_t rr = r;
+    for (int i = 0; i < RPI; ++i) {
+      rrow[i] = ((int64_t)blockIdx.y * p.rpt + k + i) * by + ty;
+      vrow[i] = cval && (k + i) < p.rpt && rrow[i] < R;
+    }
+    float rowv[RPI][NRS > 0 ? NRS : 1];
+#pragma unroll
+    for (int i = 0; i < RPI; ++i)
+#pragma unroll
+      for (int q = 0; q < (NRS > 0 ? NRS : 1); ++q) rowv[i][q] = 0.f;
+    // element offset of row r for a ref with strides s (2-D fast path: no div/mod)
+    auto row_off = [&](const int64_t* s, int64_t r) -> int64_t {
+      if (nd == 2) return r * s[0];
+      int64_t off = 0, rr = r;
       for (int d = nd - 2; d >= 0; --d) {
-        idx[d] = rr % p.dims[d];
+        off += (rr % p.dims[d]) * s[d];
         rr /= p.dims[d];
       }
-      auto load = [&](int i) {
+      return off;
+    };
+    if constexpr (SPEC) {
+      float w[NS][RPI * VEC];
+#pragma unroll
+      for (int i = 0; i < T::kLit; ++i)
+#pragma unroll
+        for (int j = 0; j < RPI * VEC; ++j) w[T::kIn + i][j] = Pg.lits[i];
+#pragma unroll
+      for (int i = 0; i < T::kIn; ++i) {
         const EwDevIn& in = p.in[i];
-        int64_t off = c * in.s[nd - 1];
-        for (int d = 0; d < nd - 1; ++d) off += idx[d] * in.s[d];
-        vm_load<VEC>(in, off, in.s[nd - 1], v[i]);
-      };
-      if constexpr (SPEC) {
+        const int64_t cs = in.s[nd - 1];
 #pragma unroll
-        for (int i = 0; i < T::kIn; ++i) load(i);
-        T::template exec<VEC>(v);
+        for (int u = 0; u < RPI; ++u) {
+          if (vrow[u]) {
+            vm_load<VEC>(in, row_off(in.s, rrow[u]) + c * cs, cs, &w[i][u * VEC]);
+          } else {
 #pragma unroll
-        for (int s = 0; s < T::Stores::n; ++s) {
-          const EwDevOut& o = p.out[s];
-          int64_t off = c * o.s[nd - 1];
-          for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
-          vm_store<VEC>(o, off, o.s[nd - 1], v[T::Stores::at(s)]);
+            for (int j = 0; j < VEC; ++j) w[i][u * VEC + j] = 0.f;
+          }
         }
-      } else {
-        for (int i = 0; i < n_in; ++i) load(i);
-        vm_exec<VEC>(Pg, v);
-        for (int s = 0; s < Pg.n_stores; ++s) {
-          const EwDevOut& o = p.out[s];
-          int64_t off = c * o.s[nd - 1];
-          for (int d = 0; d < nd - 1; ++d) off += idx[d] * o.s[d];
-          vm_store<VEC>(o, off, o.s[nd - 1], v[Pg.store_slot[s]]);
-        }
+      }
+      T::template exec<RPI * VEC>(w);
+#pragma unroll
+      for (int s2 = 0; s2 < T::Stores::n; ++s2) {
+        const EwDevOut& o = p.out[s2];
+        const int64_t cs = o.s[nd - 1];
+#pragma unroll
+        for (int u = 0; u < RPI; ++u)
+          if (vrow[u]) vm_store<VEC>(o, row_off(o.s, rrow[u]) + c * cs, cs, &w[T::Stores::at(s2)][u * VEC]);
       }
 #pragma unroll
       for (int q = 0; q < NRS; ++q) {
-        if (q >= nred) break;
-        const float* x = v[red_slot(q)];
-        if (red_kind(q) == RED_ROW) {
-          float s = 0.f;
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) s = __fadd_rn(s, x[j]);
-          rowv[q] = s;
-        } else {
+        for (int u = 0; u < RPI; ++u) {
+          if (!vrow[u]) continue;
+          if (T::Reds::at(2 * q + 1) == RED_ROW) {
+            float s3 = 0.f;
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) acc[q][j] = __fadd_rn(acc[q][j], x[j]);
+            for (int j = 0; j < VEC; ++j) s3 = __fadd_rn(s3, w[T::Reds::at(2 * q)][u * VEC + j]);
+            rowv[u][q] = s3;
+          } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[q][j] = __fadd_rn(acc[q][j], w[T::Reds::at(2 * q)][u * VEC + j]);
+          }
+        }
+      }
+    } else {
+      if (vrow[0]) {
+        const int64_t r = rrow[0];
+        for (int i = 0; i < n_in; ++i) {
+          const EwDevIn& in = p.in[i];
+          vm_load<VEC>(in, row_off(in.s, r) + c * in.s[nd - 1], in.s[nd - 1], v[i]);
+        }
+        vm_exec<VEC>(Pg, v);
+        for (int s2 = 0; s2 < Pg.n_stores; ++s2) {
+          const EwDevOut& o = p.out[s2];
+          vm_store<VEC>(o, row_off(o.s, r) + c * o.s[nd - 1], o.s[nd - 1], v[Pg.store_slot[s2]]);
+        }
+        for (int q = 0; q < n_red; ++q) {
+          const float* x = v[Pg.reduce_slot[q]];
+          if (Pg.reduce_kind[q] == RED_ROW) {
+            float s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) s3 = __fadd_rn(s3, x[j]);
+            rowv[0][q] = s3;
+          } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[q][j] = __fadd_rn(acc[q][j], x[j]);
+          }
         }
       }
     }
     if (has_row) {  // block-uniform: every thread takes part
 #pragma unroll
-      for (int q = 0; q < NRS; ++q) {
-        if (q >= nred || red_kind(q) != RED_ROW) continue;
-        float s = warp_sum(rowv[q]);
-        if ((tx & 31) == 0) row_s[ty][tx >> 5] = s;
-        __syncthreads();
-        if (tx == 0 && r < R) {
-          float t = 0.f;
-          for (int w = 0; w < (bx >> 5); ++w) t = __fadd_rn(t, row_s[ty][w]);
-          p.red[q][r * p.gx + blockIdx.x] = t;
+      for (int u = 0; u < RPI; ++u) {
+#pragma unroll
+        for (int q = 0; q < NRS; ++q) {
+          if (q >= nred || red_kind(q) != RED_ROW) continue;
+          float s3 = warp_sum(rowv[u][q]);
+          if ((tx & 31) == 0) row_s[ty][tx >> 5] = s3;
+          __syncthreads();
+          if (tx == 0 && (k + u) < p.rpt && rrow[u] < R) {
+            float t = 0.f;
+            for (int w2 = 0; w2 < (bx >> 5); ++w2) t = __fadd_rn(t, row_s[ty][w2]);
+            p.red[q][rrow[u] * p.gx + blockIdx.x] = t;
+          }
+          __syncthreads();
         }
-        __syncthreads();
       }
     }
   }
@@ -236,6 +281,123 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
   }
 }
 
+// 2-D specialised fast path ([R, C], row-major refs, no row reductions):
+// per-thread column pointers advanced by one row stride per step, operands
+// that do not depend on the row (bias / scale vectors, scalars) loaded once,
+// RPI rows loaded before they are computed.  Same arithmetic as ew_kernel.
+template <int VEC, class P>
+__global__ void __launch_bounds__(256, 3) ew2d_kernel(const __grid_constant__ EwParams p) {
+  using T = spec::Traits<P>;
+  constexpr int NS = T::kSlots, NI = T::kIn > 0 ? T::kIn : 1;
+  constexpr int NR = T::Reds::n > 0 ? T::Reds::n : 1;
+  constexpr int RPI = 2;
+  const EwProgram& Pg = p.prog;
+  const int tx = threadIdx.x, ty = threadIdx.y, bx = blockDim.x, by = blockDim.y;
+  const int64_t C = p.dims[1], R = p.dims[0];
+  const int64_t c = ((int64_t)blockIdx.x * bx + tx) * VEC;
+  const bool cval = c < C;
+  const int64_t r0 = (int64_t)blockIdx.y * p.rpt * by + ty;
+  float acc[NR][VEC];
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[q][j] = 0.f;
+  float inv[NI][VEC];  // row-invariant operands
+  bool rinv[NI];
+#pragma unroll
+  for (int i = 0; i < T::kIn; ++i) {
+    rinv[i] = p.in[i].s[0] == 0;
+    if (rinv[i] && cval) vm_load<VEC>(p.in[i], c * p.in[i].s[1], p.in[i].s[1], inv[i]);
+  }
+  if (cval) {
+    for (int k = 0; k < p.rpt; k += RPI) {
+      float w[NS][RPI * VEC];
+#pragma unroll
+      for (int i = 0; i < T::kLit; ++i)
+#pragma unroll
+        for (int j = 0; j < RPI * VEC; ++j) w[T::kIn + i][j] = Pg.lits[i];
+      int64_t rr[RPI];
+      bool ok[RPI];
+#pragma unroll
+      for (int u = 0; u < RPI; ++u) {
+        rr[u] = r0 + (int64_t)(k + u) * by;
+        ok[u] = (k + u) < p.rpt && rr[u] < R;
+      }
+#pragma unroll
+      for (int i = 0; i < T::kIn; ++i) {
+        const EwDevIn& in = p.in[i];
+#pragma unroll
+        for (int u = 0; u < RPI; ++u) {
+          if (rinv[i]) {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) w[i][u * VEC + j] = inv[i][j];
+          } else if (ok[u]) {
+            vm_load<VEC>(in, rr[u] * in.s[0] + c * in.s[1], in.s[1], &w[i][u * VEC]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) w[i][u * VEC + j] = 0.f;
+          }
+        }
+      }
+      T::template exec<RPI * VEC>(w);
+#pragma unroll
+      for (int s2 = 0; s2 < T::Stores::n; ++s2) {
+        const EwDevOut& o = p.out[s2];
+#pragma unroll
+        for (int u = 0; u < RPI; ++u)
+          if (ok[u]) vm_store<VEC>(o, rr[u] * o.s[0] + c * o.s[1], o.s[1], &w[T::Stores::at(s2)][u * VEC]);
+      }
+#pragma unroll
+      for (int q = 0; q < T::Reds::n; ++q)
+#pragma unroll
+        for (int u = 0; u < RPI; ++u)
+          if (ok[u])
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[q][j] = __fadd_rn(acc[q][j], w[T::Reds::at(2 * q)][u * VEC + j]);
+    }
+  }
+  __shared__ float red_s[256 * 4];
+#pragma unroll
+  for (int q = 0; q < T::Reds::n; ++q) {
+    if (T::Reds::at(2 * q + 1) == RED_COL) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) red_s[(ty * bx + tx) * VEC + j] = acc[q][j];
+      __syncthreads();
+      if (ty == 0 && cval) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          float t = 0.f;
+          for (int y = 0; y < by; ++y) t = __fadd_rn(t, red_s[(y * bx + tx) * VEC + j]);
+          if (VEC == 1 || c + j < C) p.red[q][blockIdx.y * C + c + j] = t;
+        }
+      }
+      __syncthreads();
+    } else {  // RED_ALL
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) t = __fadd_rn(t, acc[q][j]);
+      t = warp_sum(t);
+      const int lin = ty * bx + tx;
+      if ((lin & 31) == 0) red_s[lin >> 5] = t;
+      __syncthreads();
+      if (lin == 0) {
+        float u2 = 0.f;
+        for (int w2 = 0; w2 < (bx * by) >> 5; ++w2) u2 = __fadd_rn(u2, red_s[w2]);
+        p.red[q][blockIdx.y * p.gx + blockIdx.x] = u2;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <class P>
+constexpr bool has_row_red() {
+  using T = spec::Traits<P>;
+  for (int q = 0; q < T::Reds::n; ++q)
+    if (T::Reds::at(2 * q + 1) == RED_ROW) return true;
+  return false;
+}
+
 __global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* __restrict__ dst, int64_t n) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
@@ -252,6 +414,12 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* 
 template <int VEC, class P>
 cudaError_t launch_spec_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
   dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
+  if constexpr (!has_row_red<P>()) {
+    if (p.ndims == 2) {
+      ew2d_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
+      return cudaGetLastError();
+    }
+  }
   ew_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
   return cudaGetLastError();
 }

@@ -16,10 +16,13 @@
 
 namespace dlvm {
 
+// sech^2(z) = 4 t / (1 + t)^2 with t = exp(-2|z|) in (0, 1]: no cancellation,
+// relative error a few ulp (expf <= 2 ulp, __fdividef <= 2 ulp for the
+// denominator range [1, 4] here), far inside the 1e-5 tolerance (reading A12).
 __device__ __forceinline__ float vm_sech2(float z) {
   float t = expf(-2.0f * fabsf(z));
   float d = __fadd_rn(1.0f, t);
-  return __fdiv_rn(__fmul_rn(4.0f, t), __fmul_rn(d, d));
+  return __fdividef(__fmul_rn(4.0f, t), __fmul_rn(d, d));
 }
 
 __device__ __forceinline__ float vm_apply(uint8_t op, float a, float b, float c) {
