@@ -73,6 +73,7 @@ struct Bound {
 void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
   std::memset(p, 0, sizeof(*p));
   p->ndims = g.ndims;
+  p->ncols = g.ncols;
   p->vec = g.vec;
   p->rpt = g.rpt;
   for (int d = 0; d < kMaxIterDims; ++d) p->dims[d] = g.dims[d];

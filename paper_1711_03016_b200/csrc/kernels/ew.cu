@@ -51,11 +51,14 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int bx = blockDim.x, by = blockDim.y;
   const int nd = p.ndims;
-  const int64_t C = p.dims[nd - 1];
-  int64_t R = 1;
-  for (int d = 0; d < nd - 1; ++d) R *= p.dims[d];
+  const int nrd = nd - p.ncols;  // row dims
+  int64_t R = 1, C = 1;
+  for (int d = 0; d < nd; ++d) (d < nrd ? R : C) *= p.dims[d];
   const int64_t c = ((int64_t)blockIdx.x * bx + tx) * VEC;
   const bool cval = c < C;
+  const int64_t c_hi = p.ncols == 2 ? c / p.dims[nd - 1] : 0, c_lo = p.ncols == 2 ? c % p.dims[nd - 1] : c;
+  // element offset of column c for strides s (two column dims only with VEC == 1)
+  auto col_off = [&](const int64_t* s) -> int64_t { return c_lo * s[nd - 1] + (p.ncols == 2 ? c_hi * s[nd - 2] : 0); };
   const int n_in = SPEC ? 0 : Pg.n_in;
   float v[NS][VEC];
   if constexpr (SPEC) {
@@ -110,9 +113,9 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
       for (int q = 0; q < (NRS > 0 ? NRS : 1); ++q) rowv[i][q] = 0.f;
     // element offset of row r for a ref with strides s (2-D fast path: no div/mod)
     auto row_off = [&](const int64_t* s, int64_t r) -> int64_t {
-      if (nd == 2) return r * s[0];
+      if (nrd == 1) return r * s[0];
       int64_t off = 0, rr = r;
-      for (int d = nd - 2; d >= 0; --d) {
+      for (int d = nrd - 1; d >= 0; --d) {
         off += (rr % p.dims[d]) * s[d];
         rr /= p.dims[d];
       }
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
 #pragma unroll
         for (int u = 0; u < RPI; ++u) {
           if (vrow[u]) {
-            vm_load<VEC>(in, row_off(in.s, rrow[u]) + c * cs, cs, &w[i][u * VEC]);
+            vm_load<VEC>(in, row_off(in.s, rrow[u]) + col_off(in.s), cs, &w[i][u * VEC]);
           } else {
 #pragma unroll
             for (int j = 0; j < VEC; ++j) w[i][u * VEC + j] = 0.f;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
         const int64_t cs = o.s[nd - 1];
 #pragma unroll
         for (int u = 0; u < RPI; ++u)
-          if (vrow[u]) vm_store<VEC>(o, row_off(o.s, rrow[u]) + c * cs, cs, &w[T::Stores::at(s2)][u * VEC]);
+          if (vrow[u]) vm_store<VEC>(o, row_off(o.s, rrow[u]) + col_off(o.s), cs, &w[T::Stores::at(s2)][u * VEC]);
       }
 #pragma unroll
       for (int q = 0; q < NRS; ++q) {
@@ -168,12 +171,12 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
         const int64_t r = rrow[0];
         for (int i = 0; i < n_in; ++i) {
           const EwDevIn& in = p.in[i];
-          vm_load<VEC>(in, row_off(in.s, r) + c * in.s[nd - 1], in.s[nd - 1], v[i]);
+          vm_load<VEC>(in, row_off(in.s, r) + col_off(in.s), in.s[nd - 1], v[i]);
         }
         vm_exec<VEC>(Pg, v);
         for (int s2 = 0; s2 < Pg.n_stores; ++s2) {
           const EwDevOut& o = p.out[s2];
-          vm_store<VEC>(o, row_off(o.s, r) + c * o.s[nd - 1], o.s[nd - 1], v[Pg.store_slot[s2]]);
+          vm_store<VEC>(o, row_off(o.s, r) + col_off(o.s), o.s[nd - 1], v[Pg.store_slot[s2]]);
         }
         for (int q = 0; q < n_red; ++q) {
           const float* x = v[Pg.reduce_slot[q]];
@@ -415,7 +418,7 @@ template <int VEC, class P>
 cudaError_t launch_spec_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
   dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
   if constexpr (!has_row_red<P>()) {
-    if (p.ndims == 2) {
+    if (p.ndims == 2 && p.ncols == 1) {
       ew2d_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
       return cudaGetLastError();
     }

@@ -577,6 +577,24 @@ struct Planner {
     }
   }
 
+  // a region whose program would exceed the fixed-size EwProgram gets a value
+  // in the middle of its inlined DAG materialised (splits it in two kernels)
+  static constexpr int kInsBudget = kMaxIns - 8, kInBudget = kMaxIn - 2;
+  bool split_oversized() {
+    for (auto& n : nodes) {
+      if (n.is_dot) continue;
+      if ((int)n.inl.size() <= kInsBudget && (int)n.reads.size() <= kInBudget) continue;
+      std::vector<int> cand;
+      for (int v : n.inl)
+        if (is_ew(def(v)) && !force_mat.count(v)) cand.push_back(v);
+      if (cand.empty()) continue;
+      std::sort(cand.begin(), cand.end(), [&](int a, int b) { return vi[a].def < vi[b].def; });
+      force_mat.insert(cand[cand.size() / 2]);
+      return true;
+    }
+    return false;
+  }
+
   int find(int a) const {
     while (nodes[a].merged_into >= 0) a = nodes[a].merged_into;
     return a;
@@ -633,7 +651,16 @@ struct Planner {
         if (g.is_dot || g.merged_into >= 0) continue;
         if (g.shape != a.shape || g.perm != a.perm) continue;
         if (a.split >= 0 && g.split >= 0 && a.split != g.split) continue;
-        if (g.roots.size() + a.roots.size() > (size_t)kMaxStores) continue;
+        if (g.roots.size() + a.roots.size() > (size_t)kMaxStores - 1) continue;
+        {  // the merged program must fit the fixed-size EwProgram
+          std::set<int> inl = g.inl, rd = g.reads;
+          inl.insert(a.inl.begin(), a.inl.end());
+          rd.insert(a.reads.begin(), a.reads.end());
+          int nred = 0;
+          for (auto& r : g.roots) nred += r.kind == Root::Reduce;
+          for (auto& r : a.roots) nred += r.kind == Root::Reduce;
+          if ((int)inl.size() > kInsBudget || (int)rd.size() > kInBudget || nred > kMaxReduces) continue;
+        }
         if (reaches((int)i, (int)j)) continue;
         // direct dependencies are allowed when `a` only reads values that `g`
         // stores, element for element (identity map): they stay in registers
@@ -1119,9 +1146,10 @@ struct Planner {
       for (auto* s : refs) s->push_back(0);
       n_col = 1;
     }
-    if (n_col != 1) unsupported("reduction over a strided column space that does not collapse");
+    if (n_col > 2) unsupported("reduction over a strided column space of more than 2 dims");
     if ((int)dims.size() > kMaxIterDims) unsupported("iteration space does not collapse to 4 dims");
     g.ndims = (int)dims.size();
+    g.ncols = n_col;
     for (int d = 0; d < kMaxIterDims; ++d) g.dims[d] = d < g.ndims ? dims[d] : 1;
     for (size_t i = 0; i < g.inputs.size(); ++i)
       for (int d = 0; d < kPlanDims; ++d) g.inputs[i].strides[d] = d < g.ndims ? in_s[i][d] : 0;
@@ -1130,9 +1158,9 @@ struct Planner {
   }
 
   static void ew_launch(EwGroup& g) {
-    int64_t C = g.dims[g.ndims - 1], R = 1;
-    for (int d = 0; d < g.ndims - 1; ++d) R *= g.dims[d];
-    bool v4 = C % 4 == 0;
+    int64_t C = 1, R = 1;
+    for (int d = 0; d < g.ndims; ++d) (d < g.ndims - g.ncols ? R : C) *= g.dims[d];
+    bool v4 = C % 4 == 0 && g.ncols == 1;
     auto ok4 = [&](const IterRef& r) {
       if (r.buf == -2) return true;
       int64_t cs = r.strides[g.ndims - 1];
@@ -1283,8 +1311,8 @@ struct Planner {
       }
       ew_launch(s.ew);
       s.ew.sig = program_signature(s.ew.prog);
-      int64_t C = s.ew.dims[s.ew.ndims - 1], R = 1;
-      for (int d = 0; d < s.ew.ndims - 1; ++d) R *= s.ew.dims[d];
+      int64_t C = 1, R = 1;
+      for (int d = 0; d < s.ew.ndims; ++d) (d < s.ew.ndims - s.ew.ncols ? R : C) *= s.ew.dims[d];
       std::ostringstream d;
       d << "ew [";
       for (int k = 0; k < s.ew.ndims; ++k) d << (k ? "," : "") << s.ew.dims[k];
@@ -1425,6 +1453,7 @@ struct Planner {
       build_nodes();
       for (auto& n : nodes) region_of(n);
       if (need_iterate) continue;
+      if (split_oversized()) continue;
       build_edges();
       merge_groups();
       if (!duplicates()) break;

@@ -65,6 +65,7 @@ struct EwGroup {
   // iteration space, row-major: dims[0..ndims-2] are "row" dims, dims[ndims-1]
   // is the column dim (ndims <= kMaxIterDims).
   int ndims = 1;
+  int ncols = 1;                 // trailing dims forming the column index (1 or 2)
   int64_t dims[kMaxIterDims] = {1, 1, 1, 1};
   // launch shape (fixed at plan time: it determines the partials layout)
   int vec = 1, bx = 32, by = 8, rpt = 1;

@@ -1,0 +1,229 @@
+"""CPU checks of the native library (no GPU needed): the C ABI loads and
+exports every entry point declared in include/dlvm.h; the C++ front end
+(parser, type/broadcast inference, verifier, AD, DCE) agrees with the
+oracle -- types bit-exact, error classes equal, and the generated adjoint
+IR, interpreted by the oracle in float64, equals the oracle's own
+vector-Jacobian product (SURVEY.md §4 tier T1/T6)."""
+
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+P = pytest.importorskip("paper_1711_03016_b200")
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "dlvm.h")).read()
+    declared = sorted(set(re.findall(r"\b(dlvm_\w+)\s*\(", hdr)))
+    assert len(declared) >= 12, declared
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1711_03016_b200", "libdlvm.so"))
+    for name in declared:
+        assert hasattr(lib, name), f"libdlvm.so does not export {name}"
+    assert sorted(P.dlvm.EXPORTS) == declared
+    assert P.dlvm_version().startswith("dlvm-b200")
+
+
+def _plan_only(text, fn, grad=None, prec="f32"):
+    return P.Function(text, fn, grad, dot_precision=prec, flags=P.DLVM_PLAN_ONLY)
+
+
+def _oracle_sig(mod, name):
+    f = mod.functions[name]
+    tr = lambda t: (tuple(t.shape), P.DLVM_BOOL if t.dtype == "bool" else P.DLVM_F32)
+    return [tr(t) for t in f.param_types], [tr(t) for t in f.result_types]
+
+
+CONFIGS = [(W.c1(), "f32"), (W.c2(64, 96), "f32"), (W.c3(64), "bf16"), (W.c4(8), "bf16"), (W.c5(32), "bf16")]
+
+
+@pytest.mark.parametrize("w,prec", CONFIGS, ids=[c[0].name for c in CONFIGS])
+def test_signature_and_types_match_oracle(w, prec):
+    m = oracle.parse(w.text)
+    f = _plan_only(w.text, w.fn, w.grad, prec)
+    assert f.signature(0) == _oracle_sig(m, w.fn)
+    assert f.signature(1) == _oracle_sig(m, w.grad)
+    # the typed primal as printed by C++ re-verifies in the oracle: every
+    # operand annotation is the C++-inferred type, checked against the oracle's
+    mm = oracle.parse('module "p"\nstage raw\n' + f.print(0))
+    assert [str(t) for t in mm.functions[w.fn].param_types] == [str(t) for t in m.functions[w.fn].param_types]
+    for name, t in m.functions[w.fn].types.items():
+        assert str(mm.functions[w.fn].types[name]) == str(t)
+
+
+def _ad_cross_check(text, fn, grad, inputs, seed=None, rtol=1e-10):
+    m = oracle.parse(text)
+    f = _plan_only(text, fn, grad)
+    gm = oracle.parse('module "g"\nstage optimizable\n' + f.print(1))
+    args = list(inputs) + ([seed] if seed is not None else [])
+    ours = oracle.run(gm, grad, args)       # C++-generated adjoint IR, interpreted in f64
+    ref = oracle.run(m, grad, args)         # oracle reverse sweep
+    assert len(ours) == len(ref)
+    for a, b in zip(ours, ref):
+        np.testing.assert_allclose(a, b, rtol=rtol, atol=1e-12 * (np.max(np.abs(b)) + 1e-300))
+    return f
+
+
+@pytest.mark.parametrize("w,prec", CONFIGS[:3], ids=[c[0].name for c in CONFIGS[:3]])
+def test_cpp_adjoint_equals_oracle_vjp(w, prec):
+    ins = [x.astype(np.float64) for x in w.inputs()]
+    seed = None if w.seed() is None else np.asarray(w.seed(), dtype=np.float64)
+    _ad_cross_check(w.text, w.fn, w.grad, ins, seed)
+
+
+def test_fig3_fig4_gradients_through_cpp_ad():
+    rng = np.random.default_rng(3)
+    m = oracle.parse(W.FIG3)
+    ins = [rng.normal(size=t.shape) for t in m.functions["foo"].param_types]
+    _ad_cross_check(W.FIG3, "foo", "foo_grad", ins)
+    _ad_cross_check(W.FIG3, "foo", "foo_grad_3", ins, rng.normal(size=(1, 10)))
+    t4 = W.fig4_ir()
+    m4 = oracle.parse(t4)
+    _ad_cross_check(t4, "g", "dg", [rng.normal(size=t.shape) for t in m4.functions["g"].param_types])
+
+
+def test_dce_removes_layer1_input_gradient():
+    """ADCE: x is not in wrt, so the adjoint never computes
+    dot(dZ1, transpose(W1)) -- four dots remain for two layers' dW/dX."""
+    f = _plan_only(W.c1().text, "mlp", "mlp_grad")
+    g = f.print(1)
+    assert g.count(" = dot ") == 2 + 2 + 1  # fwd z1, z2; dW2, dX2(=dH1); dW1
+    assert "%w1" in g
+
+
+def _rand_program(rng):
+    """Random straight-line programs over rank-1..3 shapes with numpy-style
+    broadcasting, exercising every hot-path op."""
+    base = [int(rng.integers(2, 5)) for _ in range(3)]
+    rank = int(rng.integers(1, 4))
+    S = base[3 - rank:]
+
+    def sub_shape():
+        s = [d if rng.random() < 0.6 else 1 for d in S]
+        k = int(rng.integers(0, len(s)))
+        return s[k:] if rng.random() < 0.3 else s
+
+    ty = lambda s: "<" + " x ".join(map(str, s)) + " x f32>" if s else "f32"
+    args = [("a", S), ("b", sub_shape()), ("c", sub_shape())]
+    lines, cur, cur_s, n = [], "%a", S, 0
+    for _ in range(int(rng.integers(3, 8))):
+        n += 1
+        op = ["add", "subtract", "multiply", "divide", "tanh", "exp", "negate", "sig", "relu", "shape"][rng.integers(10)]
+        if op in ("add", "subtract", "multiply", "divide"):
+            o = args[int(rng.integers(1, 3))]
+            other = f"%{o[0]}: {ty(o[1])}"
+            if op == "divide":
+                lines.append(f"    %p{n} = exp %{o[0]}: {ty(o[1])}")
+                other = f"%p{n}: {ty(o[1])}"
+            lines.append(f"    %t{n} = {op} {cur}: {ty(cur_s)}, {other}")
+        elif op == "sig":
+            lines += [f"    %n{n} = negate {cur}: {ty(cur_s)}", f"    %e{n} = exp %n{n}: {ty(cur_s)}",
+                      f"    %d{n} = add %e{n}: {ty(cur_s)}, 1: f32", f"    %t{n} = divide 1: f32, %d{n}: {ty(cur_s)}"]
+        elif op == "relu":
+            lines += [f"    %c{n} = gt {cur}: {ty(cur_s)}, 0: f32",
+                      f"    %t{n} = select %c{n}: {ty(cur_s)[:-4]}bool>, {cur}: {ty(cur_s)}, 0: f32"
+                      if cur_s else f"    %t{n} = select %c{n}: bool, {cur}: f32, 0: f32"]
+        elif op == "shape" and len(cur_s) >= 1:
+            lines.append(f"    %t{n} = transpose {cur}: {ty(cur_s)}")
+            cur_s = list(reversed(cur_s))
+            n += 1
+            lines.append(f"    %t{n} = transpose %t{n-1}: {ty(cur_s)}")
+            cur_s = list(reversed(cur_s))
+        else:
+            lines.append(f"    %t{n} = {op if op in ('tanh', 'exp', 'negate') else 'tanh'} {cur}: {ty(cur_s)}")
+        cur = f"%t{n}"
+    while cur_s:
+        n += 1
+        lines.append(f"    %t{n} = reduce {cur}: {ty(cur_s)} by add along {len(cur_s) - 1}")
+        cur_s = cur_s[:-1]
+        cur = f"%t{n}"
+    lines.append(f"    return {cur}: f32")
+    sig = ", ".join(ty(s) for _, s in args)
+    head = ['module "r"', "stage raw", f"func @f: ({sig}) -> f32 {{",
+            "'entry(" + ", ".join(f"%{a}: {ty(s)}" for a, s in args) + "):"]
+    tail = ["}", "", "[gradient @f]", f"func @g: ({sig}) -> ({sig})", ""]
+    return "\n".join(head + lines + tail), args
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_programs_types_and_ad(seed):
+    rng = np.random.default_rng(1000 + seed)
+    text, args = _rand_program(rng)
+    ins = [rng.uniform(-1, 1, s) for _, s in args]
+    f = _ad_cross_check(text, "f", "g", ins)
+    m = oracle.parse(text)
+    assert f.signature(1) == _oracle_sig(m, "g")
+    assert "unsupported" not in f.print(3), f.print(3)
+
+
+def _status(text, fn="f", grad=None):
+    try:
+        P.Function(text, fn, grad, flags=P.DLVM_PLAN_ONLY)
+        return 0
+    except P.DlvmError as e:
+        return e.status
+
+
+def test_error_classes_match_oracle():
+    from test_oracle_pins import BAD_PARSE, BAD_VERIFY
+    for t in BAD_PARSE:
+        with pytest.raises(oracle.ParseError):
+            oracle.parse(t)
+        assert _status(t) == 2, t
+    for t in BAD_VERIFY:
+        with pytest.raises(oracle.VerifyError):
+            oracle.parse(t)
+        assert _status(t) == 1, t
+
+
+def test_usage_errors():
+    w = W.c1()
+    f = _plan_only(w.text, w.fn, w.grad)
+    with pytest.raises(P.DlvmError) as e:
+        P.dlvm.lib().dlvm_fn_run(f._h, None, 0, None, 0, None, None) and P.dlvm._check(3)
+        P.dlvm._check(P.dlvm.lib().dlvm_fn_run(f._h, None, 0, None, 0, None, None))
+    assert e.value.status == 3
+    with pytest.raises(P.DlvmError) as e:
+        P.Function(w.text, "nope", None, flags=P.DLVM_PLAN_ONLY)
+    assert e.value.status == 3
+    # f64 tensors are valid IR but not executed on the GPU path
+    t64 = W.FIG3.replace("f32", "f64")
+    with pytest.raises(P.DlvmError) as e:
+        P.Function(t64, "foo", "foo_grad")
+    assert e.value.status == 6
+    assert "unsupported" in P.Function(t64, "foo", "foo_grad", flags=P.DLVM_PLAN_ONLY).print(2)
+
+
+def test_gradient_ready_events_cover_every_gradient():
+    for w, prec in CONFIGS:
+        f = _plan_only(w.text, w.fn, w.grad, prec)
+        plan = f.print(3)
+        n = len(f.signature(1)[1]) - 1  # kept loss output
+        for k in range(n):
+            assert f"event: gradient {k} ready" in plan, (w.name, k)
+
+
+def test_specialisation_table_is_current():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_specializations.py"), "--check"],
+                       capture_output=True)
+    assert r.returncode == 0, "spec_programs.inc is stale: run tools/gen_specializations.py and rebuild"
+
+
+def test_plan_launch_counts_configs():
+    """The fused plans stay small: c3's fwd+adjoint is 8 GEMMs (3 fwd, 3 dW,
+    2 dX with fused ReLU'/bias-sum epilogues) + 5 tiny finalize/scalar kernels."""
+    f = _plan_only(W.c3().text, "mlp", "mlp_grad", "bf16")
+    plan = f.print(3)
+    assert plan.count("gemm tcgen05") == 8
+    assert f.num_launches(1) <= 14
+    f2 = _plan_only(W.c2(64, 128).text, "chain", "chain_grad")
+    assert f2.num_launches(0) == 1 and f2.num_launches(1) == 3
