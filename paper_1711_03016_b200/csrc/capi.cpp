@@ -228,6 +228,16 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       gp.bn = g.bn;
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);
+      for (int i = 1; i < gp.epi.prog.n_in && gp.n_pf < 4; ++i) {  // row-contiguous [M, N] epilogue inputs
+        const EwDevIn& r = gp.epi.in[i];
+        if (r.nchunks != 1 || r.s[1] != 1 || r.s[0] == 0) continue;
+        const int es = r.st == (uint8_t)SType::F32 ? 4 : r.st == (uint8_t)SType::BF16 ? 2 : 1;
+        if (reinterpret_cast<uintptr_t>(r.ptr) % 16 || (r.s[0] * es) % 16) continue;
+        gp.pf_ptr[gp.n_pf] = r.ptr;
+        gp.pf_row_bytes[gp.n_pf] = r.s[0] * es;
+        gp.pf_esize[gp.n_pf] = es;
+        ++gp.n_pf;
+      }
       bool aligned = (reinterpret_cast<uintptr_t>(gp.a) % 16 == 0) && (reinterpret_cast<uintptr_t>(gp.b) % 16 == 0);
       if (g.tensor_core && aligned && gp.bf16) {
         GemmLaunchFn sf = fn->specialize ? find_gemm_spec(g.epi.sig.c_str(), g.bn) : nullptr;

@@ -13,8 +13,16 @@ const GemmSpecEntry* gemm_spec_table_3();
 bool gemm_tc_available() { return get_encode() != nullptr; }
 
 cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream) {
-  if (p.bn == 256) return launch_prog<256, void>(p, stream);
-  return launch_prog<128, void>(p, stream);
+  const EwProgram& e = p.epi.prog;
+  const int cw = epi_chunk_width(e.n_in + e.n_lits + e.n_ins);
+  if (p.bn == 256) {
+    if (cw == 16) return launch_prog<256, VmEpi<16>>(p, stream);
+    if (cw == 8) return launch_prog<256, VmEpi<8>>(p, stream);
+    return launch_prog<256, VmEpi<4>>(p, stream);
+  }
+  if (cw == 16) return launch_prog<128, VmEpi<16>>(p, stream);
+  if (cw == 8) return launch_prog<128, VmEpi<8>>(p, stream);
+  return launch_prog<128, VmEpi<4>>(p, stream);
 }
 
 GemmLaunchFn find_gemm_spec(const char* sig, int bn) {

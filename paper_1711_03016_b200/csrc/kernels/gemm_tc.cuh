@@ -181,6 +181,160 @@ __device__ __forceinline__ void epi_store(const EwDevOut& o, int64_t m0, int64_t
   }
 }
 
+
+template <int CW>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+  if constexpr (CW == 16) {
+    tmem_ld16(taddr, v);
+  } else if constexpr (CW == 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+  }
+}
+
+// CW consecutive columns n0.. of row m of an epilogue operand.  `full`: the
+// whole segment is in bounds and 16-byte vector accesses are legal.
+template <int CW>
+__device__ __forceinline__ void epi_row_load(const EwDevIn& in, int64_t m, int64_t n0, int ncol, bool full,
+                                             float* v) {
+  const int64_t off = m * in.s[0] + n0 * in.s[1];
+  if (in.s[1] == 0) {  // constant along the row (column vector / scalar)
+    const float x = ncol > 0 ? ld1(in.ptr, off, in.st) : 0.f;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) v[j] = x;
+    return;
+  }
+  if (full && in.s[1] == 1) {
+    if (in.st == (uint8_t)SType::F32) {
+      const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(in.ptr) + off);
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k) {
+        const float4 x = __ldg(p + k);
+        v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+      }
+      return;
+    }
+    if (in.st == (uint8_t)SType::BF16) {
+      unsigned w[CW / 2];
+      const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + off;
+      if constexpr (CW >= 8) {
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+          w[4 * k] = x.x; w[4 * k + 1] = x.y; w[4 * k + 2] = x.z; w[4 * k + 3] = x.w;
+        }
+      } else {
+        const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = x.x; w[1] = x.y;
+      }
+#pragma unroll
+      for (int k = 0; k < CW / 2; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+      }
+      return;
+    }
+    unsigned w[CW / 4];
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + off;
+    if constexpr (CW == 16) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    } else if constexpr (CW == 8) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = x.x; w[1] = x.y;
+    } else {
+      w[0] = __ldg(reinterpret_cast<const unsigned*>(p));
+    }
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) {
+      v[4 * k] = (w[k] & 0xffu) ? 1.f : 0.f;
+      v[4 * k + 1] = (w[k] & 0xff00u) ? 1.f : 0.f;
+      v[4 * k + 2] = (w[k] & 0xff0000u) ? 1.f : 0.f;
+      v[4 * k + 3] = (w[k] & 0xff000000u) ? 1.f : 0.f;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < CW; ++j) v[j] = j < ncol ? ld1(in.ptr, off + j * in.s[1], in.st) : 0.f;
+}
+
+template <int CW>
+__device__ __forceinline__ void epi_row_store(const EwDevOut& o, int64_t m, int64_t n0, int ncol, bool full,
+                                              const float* v) {
+  const int64_t off = m * o.s[0] + n0 * o.s[1];
+  if (full && o.s[1] == 1) {  // widest aligned stores of the row segment
+    if (o.st == (uint8_t)SType::F32) {
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k) st4(o.ptr, off + 4 * k, o.st, v + 4 * k);
+    } else if (o.st == (uint8_t)SType::BF16) {
+      unsigned w[CW / 2];
+#pragma unroll
+      for (int k = 0; k < CW / 2; ++k) w[k] = (unsigned)f2bf(v[2 * k]) | ((unsigned)f2bf(v[2 * k + 1]) << 16);
+      unsigned short* p = reinterpret_cast<unsigned short*>(o.ptr) + off;
+      if constexpr (CW >= 8) {
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k)
+          *reinterpret_cast<uint4*>(p + 8 * k) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+      } else {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+      }
+    } else {
+      unsigned w[CW / 4];
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k)
+        w[k] = (v[4 * k] != 0.f ? 1u : 0u) | (v[4 * k + 1] != 0.f ? 0x100u : 0u) |
+               (v[4 * k + 2] != 0.f ? 0x10000u : 0u) | (v[4 * k + 3] != 0.f ? 0x1000000u : 0u);
+      unsigned char* p = reinterpret_cast<unsigned char*>(o.ptr) + off;
+      if constexpr (CW == 16) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else if constexpr (CW == 8) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+      } else {
+        *reinterpret_cast<unsigned*>(p) = w[0];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < CW; ++j)
+    if (j < ncol) st1(o.ptr, off + j * o.s[1], o.st, v[j]);
+}
+
+// Column sums over the 32 lanes of CW values per lane (fixed butterfly
+// order): returns the sum for column *col; lanes < CW hold distinct columns.
+template <int CW>
+__device__ __forceinline__ float col_butterfly(float (&x)[CW], int lane, int* col) {
+  int base = 0;
+#pragma unroll
+  for (int k = 0, w = CW / 2; w >= 1; ++k, w /= 2) {
+    const bool up = (lane >> k) & 1;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? x[i] : x[i + w];
+      const float keep = up ? x[i + w] : x[i];
+      x[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1 << k));
+    }
+    if (up) base += w;
+  }
+#pragma unroll
+  for (int s = CW; s < 32; s *= 2) x[0] = __fadd_rn(x[0], __shfl_xor_sync(0xffffffffu, x[0], s));
+  *col = base;
+  return x[0];
+}
+
 // Tile raster: groups of GROUP_M tile-rows, N fastest inside a group, so the
 // ~148 tiles in flight share a few A row-panels and all of B through L2
 // (a plain M-fastest order re-reads A once per N tile).
@@ -226,13 +380,28 @@ __host__ __device__ constexpr int epi_num_reds() {
   if constexpr (S) return T::Reds::n; else return kEpiReds;
 }
 
+// Interpreted epilogue programs, instantiated per column-chunk width CW (the
+// same width a specialised program of the same size uses, so both sum their
+// reductions in the same order and stay bit-identical).
+template <int CW>
+struct VmEpi {};
 struct VmEpiTraits {
   static constexpr int kSlots = kMaxSlots;
 };
+template <class P>
+struct vm_cw {
+  static constexpr int value = 0;
+};
+template <int CW>
+struct vm_cw<VmEpi<CW>> {
+  static constexpr int value = CW;
+};
+__host__ __device__ constexpr int epi_chunk_width(int slots) { return slots <= 6 ? 16 : (slots <= 12 ? 8 : 4); }
 
 template <int BN, class PROG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
-  constexpr bool SPEC = !std::is_void_v<PROG>;
+  constexpr int VMCW = vm_cw<PROG>::value;
+  constexpr bool SPEC = VMCW == 0;
   using T = std::conditional_t<SPEC, spec::Traits<std::conditional_t<SPEC, PROG, spec::Prog<0, 0, spec::St<>, spec::Rd<>>>>,
                                VmEpiTraits>;
   constexpr int NS = T::kSlots;
@@ -283,14 +452,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        int tm, tn;
-        tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
-        const int m0 = tm * BM, n0 = tn * BN;
+  if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      const int m0 = tm * BM, n0 = tn * BN;
+      for (int i = 0; i < g.n_pf; ++i) {
+        const int64_t cols = min((int64_t)BN, g.N - n0);
+        const uint32_t bytes = (uint32_t)((cols * g.pf_esize[i] + 15) & ~15);
+        for (int r = lane; r < BM && m0 + r < g.M; r += 32) {
+          const char* a = reinterpret_cast<const char*>(g.pf_ptr[i]) + (int64_t)(m0 + r) * g.pf_row_bytes[i] +
+                          (int64_t)n0 * g.pf_esize[i];
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+        }
+      }
+      if (lane == 0) {
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(empty_bar + 8 * s, ph ^ 1);
           const uint32_t fb = full_bar + 8 * s;
@@ -315,6 +493,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           }
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
@@ -348,30 +527,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
-    // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (tile rows) and the
-    // 16-column chunks ch = h, h+2, ...  A 32x16 chunk is transposed through
-    // shared memory so lane l handles column l%16 of rows 16*(l/16)..+15,
-    // RV rows at a time in registers: every load/store of an [M, N] operand
-    // is a coalesced 16-element row segment and RV independent loads are in
-    // flight per lane; column sums accumulate in registers.
+    // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (lane = tile row, the
+    // native tcgen05.ld 32x32b layout) and the CW-column chunks ch = h, h+2, ...
+    // Each lane loads / stores its row segment of CW consecutive elements
+    // with vector accesses; column sums use a shuffle butterfly.
     const int ew = warp - 4;
     const int q = ew & 3, h = ew >> 2;
     const int et = threadIdx.x - 128;  // 0..255
-    const int col = lane & 15, rg = lane >> 4;
     const EwParams& E = g.epi;
     const EwProgram& Pg = E.prog;
-    float* X = xpose + ew * 32 * 17;
-    constexpr int RV = SPEC ? (NS <= 12 ? 8 : 4) : 4;
-    float v[NS][RV];
+    constexpr int CW = SPEC ? epi_chunk_width(NS) : VMCW;
+    constexpr int NSV = SPEC ? NS : (CW == 16 ? 6 : (CW == 8 ? 12 : kMaxSlots));  // interpreter slots
+    float v[NSV][CW];
     if constexpr (SPEC) {
 #pragma unroll
       for (int i = 0; i < T::kLit; ++i)
 #pragma unroll
-        for (int j = 0; j < RV; ++j) v[T::kIn + i][j] = Pg.lits[i];
+        for (int j = 0; j < CW; ++j) v[T::kIn + i][j] = Pg.lits[i];
     } else {
       for (int i = 0; i < Pg.n_lits; ++i)
 #pragma unroll
-        for (int j = 0; j < RV; ++j) v[Pg.n_in + i][j] = Pg.lits[i];
+        for (int j = 0; j < CW; ++j) v[Pg.n_in + i][j] = Pg.lits[i];
     }
     auto red_slot = [&](int r) -> int {
       if constexpr (SPEC) return T::Reds::at(2 * r); else return Pg.reduce_slot[r];
@@ -388,11 +564,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         has_row |= red_kind(r) == RED_ROW;
         has_all |= red_kind(r) == RED_ALL;
       }
+    const bool vec_ok = E.vec == 4;
     int it = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       int tm, tn;
       tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
-      const int64_t mb = (int64_t)tm * BM + 32 * q + 16 * rg;  // first row of this lane's 16
+      const int64_t m = (int64_t)tm * BM + 32 * q + lane;
+      const bool mval = m < g.M;
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull_bar + 8 * as, aph);
@@ -400,69 +578,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
 #pragma unroll
       for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
-      for (int ch = h; ch < BN / 16; ch += 2) {
-        float acc[16];
-        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * 16, acc);
+      for (int ch = h; ch < BN / CW; ch += 2) {
+        const int64_t n0 = (int64_t)tn * BN + ch * CW;
+        const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
+        const bool full = mval && ncol == CW && vec_ok;
+        tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
+        if constexpr (SPEC) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) X[lane * 17 + j] = acc[j];
-        __syncwarp();
-        const int64_t n = (int64_t)tn * BN + ch * 16 + col;
-        const bool nval = n < g.N;
-        float colacc[NRS > 0 ? NRS : 1];
+          for (int s2 = 1; s2 < T::kIn; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          T::template exec<CW>(v);
 #pragma unroll
-        for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) colacc[r] = 0.f;
+          for (int s2 = 0; s2 < T::Stores::n; ++s2)
+            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
+        } else {
+          for (int s2 = 1; s2 < Pg.n_in; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          vm_exec<CW>(Pg, v);
+          for (int s2 = 0; s2 < Pg.n_stores; ++s2)
+            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[Pg.store_slot[s2]]);
+        }
 #pragma unroll
-        for (int b = 0; b < 16 / RV; ++b) {
-          const int64_t m0 = mb + b * RV;
+        for (int r = 0; r < NRS; ++r) {
+          if (r >= nred) break;
+          const int kind = red_kind(r);
+          float x[CW];
 #pragma unroll
-          for (int j = 0; j < RV; ++j) v[0][j] = X[(16 * rg + b * RV + j) * 17 + col];
-          // rows m0..m0+RV-1 valid?  (uniform fast path when the whole batch is inside)
-          const int64_t left = g.M - m0;
-          const int nrow = !nval ? 0 : (left >= RV ? RV : (left > 0 ? (int)left : 0));
-          if constexpr (SPEC) {
-#pragma unroll
-            for (int s = 1; s < T::kIn; ++s) epi_load<RV>(E.in[s], m0, n, nrow, v[s]);
-            T::template exec<RV>(v);
-#pragma unroll
-            for (int s = 0; s < T::Stores::n; ++s) epi_store<RV>(E.out[s], m0, n, nrow, v[T::Stores::at(s)]);
+          for (int j = 0; j < CW; ++j) x[j] = (mval && j < ncol) ? v[red_slot(r)][j] : 0.f;
+          if (kind == RED_COL) {
+            int col;
+            const float cs = col_butterfly<CW>(x, lane, &col);
+            if (lane < CW) colred[(r * 4 + q) * BN + ch * CW + col] = cs;
           } else {
-            for (int s = 1; s < Pg.n_in; ++s) epi_load<RV>(E.in[s], m0, n, nrow, v[s]);
-            vm_exec<RV>(Pg, v);
-            for (int s = 0; s < Pg.n_stores; ++s) epi_store<RV>(E.out[s], m0, n, nrow, v[Pg.store_slot[s]]);
-          }
-          bool okj[RV];
+            float s3 = 0.f;
 #pragma unroll
-          for (int j = 0; j < RV; ++j) okj[j] = j < nrow;
-#pragma unroll
-          for (int r = 0; r < NRS; ++r) {
-            if (r >= nred) break;
-            const int kind = red_kind(r);
-            const int sl = red_slot(r);
-#pragma unroll
-            for (int j = 0; j < RV; ++j) {
-              const float x = okj[j] ? v[sl][j] : 0.f;
-              if (kind == RED_COL) {
-                colacc[r] = __fadd_rn(colacc[r], x);
-              } else if (kind == RED_ALL) {
-                allacc[r] = __fadd_rn(allacc[r], x);
-              } else {  // row sum over this chunk's 16 columns (lanes of the same row group)
-                float s = x;
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-                if ((lane & 15) == b * RV + j) rowacc[r] = __fadd_rn(rowacc[r], s);
-              }
-            }
+            for (int j = 0; j < CW; ++j) s3 = __fadd_rn(s3, x[j]);
+            if (kind == RED_ROW)
+              rowacc[r] = __fadd_rn(rowacc[r], s3);
+            else
+              allacc[r] = __fadd_rn(allacc[r], s3);
           }
         }
-        if (has_col) {
-#pragma unroll
-          for (int r = 0; r < NRS; ++r) {
-            if (r >= nred || red_kind(r) != RED_COL) continue;
-            const float s = __fadd_rn(colacc[r], __shfl_xor_sync(0xffffffffu, colacc[r], 16));
-            if (lane < 16) colred[(r * 4 + q) * BN + ch * 16 + lane] = s;  // rows 32q..32q+31
-          }
-        }
-        __syncwarp();
       }
       // accumulator buffer free for the next tile's MMAs
       tc_fence_before();
@@ -471,10 +625,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
           if (r >= nred) break;
-          if (red_kind(r) == RED_ROW) rowred[(r * 2 + h) * BM + 32 * q + 16 * rg + (lane & 15)] = rowacc[r];
+          if (red_kind(r) == RED_ROW) rowred[(r * 2 + h) * BM + 32 * q + lane] = rowacc[r];
           if (red_kind(r) == RED_ALL) {
-            const float s = warp_sum(allacc[r]);
-            if (lane == 0) allred[r * 8 + ew] = s;
+            const float s3 = warp_sum(allacc[r]);
+            if (lane == 0) allred[r * 8 + ew] = s3;
           }
         }
       }
@@ -488,19 +642,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             for (int c = et; c < BN; c += 256) {
               const int64_t n = (int64_t)tn * BN + c;
               if (n >= g.N) continue;
-              float s = 0.f;
-              for (int w = 0; w < 4; ++w) s = __fadd_rn(s, colred[(r * 4 + w) * BN + c]);
-              E.red[r][(int64_t)tm * g.N + n] = s;
+              float s3 = 0.f;
+              for (int w2 = 0; w2 < 4; ++w2) s3 = __fadd_rn(s3, colred[(r * 4 + w2) * BN + c]);
+              E.red[r][(int64_t)tm * g.N + n] = s3;
             }
           } else if (kind == RED_ROW) {
             if (et < BM) {
-              const int64_t m = (int64_t)tm * BM + et;
-              if (m < g.M) E.red[r][m * E.gx + tn] = __fadd_rn(rowred[(r * 2) * BM + et], rowred[(r * 2 + 1) * BM + et]);
+              const int64_t mm = (int64_t)tm * BM + et;
+              if (mm < g.M)
+                E.red[r][mm * E.gx + tn] = __fadd_rn(rowred[(r * 2) * BM + et], rowred[(r * 2 + 1) * BM + et]);
             }
           } else if (et == 0) {
-            float s = 0.f;
-            for (int w = 0; w < 8; ++w) s = __fadd_rn(s, allred[r * 8 + w]);
-            E.red[r][(int64_t)tm * E.gx + tn] = s;
+            float s3 = 0.f;
+            for (int w2 = 0; w2 < 8; ++w2) s3 = __fadd_rn(s3, allred[r * 8 + w2]);
+            E.red[r][(int64_t)tm * E.gx + tn] = s3;
           }
         }
         epi_bar();

@@ -51,6 +51,12 @@ struct GemmParams {
   int32_t bf16;        // operand element type: 1 bf16, 0 f32
   int32_t bm, bn;      // tile; defines the epilogue partial layout
   EwParams epi;        // ndims 2, dims {M, N}; slot 0 = accumulator
+  // epilogue inputs with contiguous rows (e.g. the saved ReLU mask): the TMA
+  // producer prefetches each tile's rows into L2 while the tile's MMAs run
+  int32_t n_pf;
+  const void* pf_ptr[4];
+  int64_t pf_row_bytes[4];  // row stride in bytes
+  int32_t pf_esize[4];      // element size in bytes
 };
 
 cudaError_t launch_gemm_simt(const GemmParams& p, cudaStream_t stream);

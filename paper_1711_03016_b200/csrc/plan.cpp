@@ -906,6 +906,15 @@ struct Planner {
       return (int)inputs.size() - 1;
     }
     int emit(uint8_t op, int a, int b, int c) {
+      // identities the AD emits to broadcast (multiply by a splat 1, add a
+      // splat 0): broadcasting is done by the index maps, so they are exact no-ops
+      auto is_lit = [&](int s, float x) { return s >= 100 && s < 200 && lits[s - 100] == x; };
+      if (op == VM_MUL && is_lit(b, 1.0f)) return a;
+      if (op == VM_MUL && is_lit(a, 1.0f)) return b;
+      if (op == VM_ADD && is_lit(b, 0.0f) && !is_lit(a, 0.0f) && a >= 200) return a;
+      // common subexpressions (the AD emits g*r twice for multiply(r, r))
+      for (size_t k = 0; k < ins.size(); ++k)
+        if (ins[k].op == op && raw[k][0] == a && raw[k][1] == b && raw[k][2] == c) return 200 + (int)k;
       if ((int)ins.size() >= kMaxIns) unsupported("fused kernel program too long");
       ins.push_back(EwIns{op, 0, 0, 0});
       raw.push_back({a, b, c});
