@@ -177,7 +177,7 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         b.ptr[k] = seed->data;
         break;
       case BufferSlot::Work:
-        if (s.cast_of >= 0 && in[s.cast_of].dtype == DLVM_BF16)
+        if (s.cast_of >= 0 && in[s.cast_of].dtype == DLVM_BF16 && s.cast_ld == 0)
           b.ptr[k] = in[s.cast_of].data;
         else
           b.ptr[k] = static_cast<char*>(workspace) + s.offset;
@@ -192,7 +192,7 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
   };
   for (const Step& st : P.steps) {
     cudaError_t e = cudaSuccess;
-    const bool is_launch = st.kind == Step::EW || st.kind == Step::GEMM;
+    const bool is_launch = st.kind == Step::EW || st.kind == Step::GEMM || (st.kind == Step::CAST && st.cast.ld);
     if (is_launch && (e = mark(li++)) != cudaSuccess)
       return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
     if (st.kind == Step::EW) {
@@ -248,7 +248,11 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         e = launch_gemm_simt(gp, stream);
       }
     } else if (st.kind == Step::CAST) {
-      if (in[st.cast.input].dtype == DLVM_F32)
+      const bool f32 = in[st.cast.input].dtype == DLVM_F32;
+      if (st.cast.ld)
+        e = launch_pack_bf16(in[st.cast.input].data, f32, st.cast.numel / st.cast.cols, st.cast.cols,
+                             b.ptr[st.cast.dst_buf], st.cast.ld, stream);
+      else if (f32)
         e = launch_cast_bf16(static_cast<const float*>(in[st.cast.input].data), b.ptr[st.cast.dst_buf],
                              st.cast.numel, stream);
     } else if (st.kind == Step::EVENT) {
@@ -265,6 +269,7 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
 
 // minimum bytes a launch moves: each distinct input read once, each output written once
 double step_bytes(const Plan& P, const Step& st) {
+  if (st.kind == Step::CAST) return (double)st.cast.numel * 2 + (double)(st.cast.numel / st.cast.cols) * st.cast.ld * 2;
   const EwGroup& g = st.kind == Step::GEMM ? st.gemm.epi : st.ew;
   auto esz = [&](int buf, SType fallback) {
     SType t = buf >= 0 ? P.bufs[buf].st : fallback;
@@ -475,7 +480,7 @@ dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t 
   const Plan& P = fn->plan[which];
   int li = 0;
   for (const Step& st : P.steps) {
-    if (st.kind != Step::EW && st.kind != Step::GEMM) continue;
+    if (st.kind != Step::EW && st.kind != Step::GEMM && !(st.kind == Step::CAST && st.cast.ld)) continue;
     if (li++ != i) continue;
     if (buf && cap) {
       size_t n = std::min(cap - 1, st.desc.size());

@@ -470,6 +470,27 @@ cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+__global__ void pack_bf16_kernel(const void* __restrict__ src, int src_f32, int64_t rows, int64_t cols,
+                                 unsigned short* __restrict__ dst, int64_t ld) {
+  const int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
+  if (r >= rows) return;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ld; c += (int64_t)gridDim.x * blockDim.x) {
+    unsigned short v = 0;
+    if (c < cols)
+      v = src_f32 ? f2bf(__ldg(reinterpret_cast<const float*>(src) + r * cols + c))
+                  : __ldg(reinterpret_cast<const unsigned short*>(src) + r * cols + c);
+    dst[r * ld + c] = v;
+  }
+}
+
+cudaError_t launch_pack_bf16(const void* src, bool src_f32, int64_t rows, int64_t cols, void* dst, int64_t ld,
+                             cudaStream_t stream) {
+  dim3 block(128, 4), grid((unsigned)std::min<int64_t>((ld + 127) / 128, 8), (unsigned)((rows + 3) / 4));
+  pack_bf16_kernel<<<grid, block, 0, stream>>>(src, src_f32 ? 1 : 0, rows, cols,
+                                               reinterpret_cast<unsigned short*>(dst), ld);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream) {
   int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
   cast_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(src, reinterpret_cast<unsigned short*>(dst), n);

@@ -313,6 +313,69 @@ __device__ __forceinline__ void epi_row_store(const EwDevOut& o, int64_t m, int6
     if (j < ncol) st1(o.ptr, off + j * o.s[1], o.st, v[j]);
 }
 
+
+// Raw 16-byte words of a row segment (prefetched one chunk ahead, decoded
+// when the chunk is computed).  Sized for f32 (CW/4 uint4).
+template <int CW>
+struct RawSeg {
+  uint4 w[CW / 4];
+};
+
+// an operand whose CW-column row segment is one contiguous vector access
+__device__ __forceinline__ bool seg_vector(const EwDevIn& in) { return in.s[1] == 1 && in.s[0] != 0; }
+
+template <int CW>
+__device__ __forceinline__ void epi_row_fetch(const EwDevIn& in, int64_t m, int64_t n0, RawSeg<CW>& r) {
+  const int64_t off = m * in.s[0] + n0;
+  if (in.st == (uint8_t)SType::F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(in.ptr) + off);
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) r.w[k] = __ldg(p + k);
+  } else if (in.st == (uint8_t)SType::BF16) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + off;
+    if constexpr (CW >= 8) {
+#pragma unroll
+      for (int k = 0; k < CW / 8; ++k) r.w[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+    } else {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      r.w[0] = make_uint4(x.x, x.y, 0, 0);
+    }
+  } else {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + off;
+    if constexpr (CW == 16) {
+      r.w[0] = __ldg(reinterpret_cast<const uint4*>(p));
+    } else if constexpr (CW == 8) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      r.w[0] = make_uint4(x.x, x.y, 0, 0);
+    } else {
+      r.w[0] = make_uint4(__ldg(reinterpret_cast<const unsigned*>(p)), 0, 0, 0);
+    }
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void epi_row_decode(const EwDevIn& in, const RawSeg<CW>& r, float* v) {
+  const unsigned* w = reinterpret_cast<const unsigned*>(r.w);
+  if (in.st == (uint8_t)SType::F32) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(w[j]);
+  } else if (in.st == (uint8_t)SType::BF16) {
+#pragma unroll
+    for (int k = 0; k < CW / 2; ++k) {
+      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) {
+      v[4 * k] = (w[k] & 0xffu) ? 1.f : 0.f;
+      v[4 * k + 1] = (w[k] & 0xff00u) ? 1.f : 0.f;
+      v[4 * k + 2] = (w[k] & 0xff0000u) ? 1.f : 0.f;
+      v[4 * k + 3] = (w[k] & 0xff000000u) ? 1.f : 0.f;
+    }
+  }
+}
+
 // Column sums over the 32 lanes of CW values per lane (fixed butterfly
 // order): returns the sum for column *col; lanes < CW hold distinct columns.
 template <int CW>
@@ -387,6 +450,7 @@ template <int CW>
 struct VmEpi {};
 struct VmEpiTraits {
   static constexpr int kSlots = kMaxSlots;
+  static constexpr int kIn = 0, kLit = 0;
 };
 template <class P>
 struct vm_cw {
@@ -578,14 +642,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
 #pragma unroll
       for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
+      constexpr int NPF = SPEC && T::kIn > 1 ? T::kIn - 1 : 1;
+      RawSeg<CW> pf[NPF];  // next chunk's row segments of the vector operands
+      auto seg_full = [&](int ch) {
+        const int64_t n0 = (int64_t)tn * BN + ch * CW;
+        return mval && vec_ok && n0 + CW <= g.N;
+      };
+      if constexpr (SPEC) {
+        if (seg_full(h))
+#pragma unroll
+          for (int s2 = 1; s2 < T::kIn; ++s2)
+            if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + h * CW, pf[s2 - 1]);
+      }
       for (int ch = h; ch < BN / CW; ch += 2) {
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
         const bool full = mval && ncol == CW && vec_ok;
+        RawSeg<CW> cur[NPF];
+        if constexpr (SPEC) {
+#pragma unroll
+          for (int s2 = 0; s2 < NPF; ++s2) cur[s2] = pf[s2];
+          if (ch + 2 < BN / CW && seg_full(ch + 2))
+#pragma unroll
+            for (int s2 = 1; s2 < T::kIn; ++s2)
+              if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, n0 + 2 * CW, pf[s2 - 1]);
+        }
         tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
         if constexpr (SPEC) {
 #pragma unroll
-          for (int s2 = 1; s2 < T::kIn; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          for (int s2 = 1; s2 < T::kIn; ++s2) {
+            if (full && seg_vector(E.in[s2]))
+              epi_row_decode<CW>(E.in[s2], cur[s2 - 1], v[s2]);
+            else
+              epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          }
           T::template exec<CW>(v);
 #pragma unroll
           for (int s2 = 0; s2 < T::Stores::n; ++s2)

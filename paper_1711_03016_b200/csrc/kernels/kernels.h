@@ -68,4 +68,8 @@ cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream);
 
 cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
 
+// [rows, cols] f32 or bf16 (src_f32) -> bf16 rows of `ld` elements (ld >= cols)
+cudaError_t launch_pack_bf16(const void* src, bool src_f32, int64_t rows, int64_t cols, void* dst, int64_t ld,
+                             cudaStream_t stream);
+
 }  // namespace dlvm

@@ -55,7 +55,7 @@ std::string program_signature(const EwProgram& p) {
 
 int Plan::launches() const {
   int n = 0;
-  for (auto& s : steps) n += (s.kind == Step::EW || s.kind == Step::GEMM) ? 1 : 0;
+  for (auto& s : steps) n += (s.kind == Step::EW || s.kind == Step::GEMM || (s.kind == Step::CAST && s.cast.ld)) ? 1 : 0;
   return n;
 }
 
@@ -763,15 +763,38 @@ struct Planner {
     plan.bufs.push_back(b);
     return (int)plan.bufs.size() - 1;
   }
-  Home make_home(int buf, int v, SType st) {
+  Home make_home(int buf, int v, SType st, int64_t ld = 0) {
     Home h;
     h.buf = buf;
     h.st = st;
     h.ref.buf = buf;
     h.ref.shape = ty(v).shape;
     h.ref.strides = contig_strides(ty(v).shape);
+    if (ld > 0) {  // padded row stride for the last dim
+      int r = (int)h.ref.shape.size();
+      int64_t s = ld;
+      h.ref.strides[r - 1] = 1;
+      for (int i = r - 2; i >= 0; --i) {
+        h.ref.strides[i] = s;
+        s *= h.ref.shape[i];
+      }
+    }
     h.ref.st = st;
     return h;
+  }
+  // Workspace tensors of rank >= 2 get their rows padded to 64 elements: a TMA
+  // box row (128 B) then never straddles two L2 lines (a 1000-element row
+  // costs ~35-60% GEMM throughput, tools/gemm_probe.py).
+  static int64_t padded_ld(const Type& t) {
+    if (t.rank() < 2) return 0;
+    int64_t c = t.shape.back();
+    if (c % 64 == 0 || c < 64) return 0;
+    return (c + 63) / 64 * 64;
+  }
+  size_t padded_bytes(const Type& t, SType st) const {
+    int64_t ld = padded_ld(t);
+    int64_t n = ld ? t.numel() / t.shape.back() * ld : t.numel();
+    return (size_t)n * stype_size(st);
   }
   int output_buf(int k) const {
     for (size_t b = 0; b < plan.bufs.size(); ++b)
@@ -820,12 +843,12 @@ struct Planner {
         x.homes.push_back(make_home(output_buf(x.out_home), (int)v,
                                     ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
       } else if (need32) {
-        int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * stype_size(natural((int)v)), natural((int)v));
-        x.homes.push_back(make_home(b, (int)v, natural((int)v)));
+        int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(v), natural((int)v)), natural((int)v));
+        x.homes.push_back(make_home(b, (int)v, natural((int)v), padded_ld(ty(v))));
       }
       if (x.dot_use && opt.policy == Policy::BF16) {
-        int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * 2, SType::BF16);
-        x.homes.push_back(make_home(b, (int)v, SType::BF16));
+        int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(v), SType::BF16), SType::BF16);
+        x.homes.push_back(make_home(b, (int)v, SType::BF16, padded_ld(ty(v))));
       }
       if (x.homes.empty() && !(is_dot && fused_dot_group.count((int)v))) {
         int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * stype_size(natural((int)v)), natural((int)v));
@@ -837,10 +860,11 @@ struct Planner {
     if (opt.policy == Policy::BF16) {
       for (int i = 0; i < f.num_args(); ++i) {
         if (!vi[i].dot_use || ty(i).dtype != DType::F32) continue;
-        int b = add_buf(BufferSlot::Work, -1, ty(i).numel() * 2, SType::BF16);
+        int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(i), SType::BF16), SType::BF16);
         plan.bufs[b].cast_of = i;
+        plan.bufs[b].cast_ld = padded_ld(ty(i));
         cast_buf[i] = b;
-        vi[i].homes.push_back(make_home(b, i, SType::BF16));
+        vi[i].homes.push_back(make_home(b, i, SType::BF16, padded_ld(ty(i))));
         plan.input_feeds_only_dot[i] = (vi[i].group_use || !vi[i].outs.empty()) ? 0 : 1;
       }
     }
@@ -1294,7 +1318,10 @@ struct Planner {
       s.cast.input = i;
       s.cast.dst_buf = cast_buf[i];
       s.cast.numel = ty(i).numel();
-      s.desc = "cast %" + f.names[i] + " f32->bf16 (skipped when passed as bf16)";
+      s.cast.cols = ty(i).rank() ? ty(i).shape.back() : 1;
+      s.cast.ld = plan.bufs[cast_buf[i]].cast_ld;
+      s.desc = s.cast.ld ? "pack %" + f.names[i] + " to bf16 rows of " + std::to_string(s.cast.ld)
+                         : "cast %" + f.names[i] + " f32->bf16 (skipped when passed as bf16)";
       plan.steps.push_back(s);
     }
     for (int ni : order) {

@@ -34,6 +34,7 @@ struct BufferSlot {
   size_t bytes = 0;
   SType st = SType::F32;
   int cast_of = -1;    // Work buffer holding a bf16 cast of Input `cast_of` (see CastStep)
+  int64_t cast_ld = 0; // ... with rows padded to this many elements (0: dense)
 };
 
 // Strided view of a buffer: element (i_0..i_{r-1}) of the value lives at
@@ -88,10 +89,11 @@ struct GemmStep {
   EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator
 };
 
-struct CastStep {                // bf16 copy of an f32 input, skipped if the caller passed bf16
+struct CastStep {                // bf16 copy of an input (cast from f32 and/or rows padded to ld)
   int input = -1;
   int dst_buf = -1;
   int64_t numel = 0;
+  int64_t cols = 0, ld = 0;      // ld > 0: destination rows padded to ld elements (always runs)
 };
 
 struct Step {
