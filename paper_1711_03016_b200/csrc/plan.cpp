@@ -127,6 +127,7 @@ struct VInfo {
   bool group_use = false;  // read by an element-wise kernel
   std::vector<Home> homes; // materialised copies
   int out_home = -1;       // output index this value is produced into directly
+  std::vector<int> more_outs;  // further outputs returning the same stored value (extra stores, no copy)
 };
 
 struct Root {
@@ -398,12 +399,19 @@ struct Planner {
 
   // outputs produced in place by their producer (no copy kernel)
   void alias_outputs() {
-    for (auto& x : vi) x.out_home = -1;
+    for (auto& x : vi) {
+      x.out_home = -1;
+      x.more_outs.clear();
+    }
     std::set<int> used;
     for (size_t k = 0; k < f.ret.size(); ++k) {
       const Operand& o = f.ret[k];
       if (o.is_lit()) continue;
       int v = o.value;
+      if (used.count(v) && vi[v].out_home >= 0 && produced(v) && vi[v].mat) {
+        vi[v].more_outs.push_back((int)k);  // returned again: one more store by its producer
+        continue;
+      }
       if (used.count(v) || vi[v].arg >= 0) continue;
       // follow single-use contiguous shapeCast views back to their producer
       std::vector<int> chain{v};
@@ -490,6 +498,9 @@ struct Planner {
         n.shape = o.type.shape;
       } else {
         if (vi[o.value].out_home == (int)k) continue;  // produced in place
+        if (std::find(vi[o.value].more_outs.begin(), vi[o.value].more_outs.end(), (int)k) !=
+            vi[o.value].more_outs.end())
+          continue;  // an extra store of the producer
         r.kind = Root::Copy;
         r.v = o.value;
         r.out = (int)k;
@@ -842,6 +853,8 @@ struct Planner {
       if (x.out_home >= 0) {
         x.homes.push_back(make_home(output_buf(x.out_home), (int)v,
                                     ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
+        for (int k : x.more_outs)
+          x.homes.push_back(make_home(output_buf(k), (int)v, ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
       } else if (need32) {
         int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(v), natural((int)v)), natural((int)v));
         x.homes.push_back(make_home(b, (int)v, natural((int)v), padded_ld(ty(v))));

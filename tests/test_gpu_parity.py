@@ -303,3 +303,30 @@ def test_specialized_programs_bit_identical_to_interpreter(case):
     b = gpu_run(w.text, w.fn, w.grad, ins, seed=w.seed(), dot_precision=prec, flags=P.DLVM_NO_SPECIALIZE)
     for x, y in zip(a["primal"] + a["grad"], b["primal"] + b["grad"]):
         np.testing.assert_array_equal(x, y)
+
+
+def test_sgd_update_two_outputs_one_kernel():
+    """H12: W' = W - lr*G (element-wise IR), returned as the fp32 master and
+    as a bf16 copy (output dtype policy, dlvm.h) -- one kernel, in place."""
+    import torch
+    import paper_1711_03016_b200 as P
+    shapes = [(300, 520), (1, 520)]
+    text = W.sgd_ir(shapes, 1e-3, [True, False])
+    f = P.Function(text, "sgd", None)
+    assert f.num_launches(0) == 2
+    rng = np.random.default_rng(21)
+    host = []
+    for s in shapes:
+        host += [rng.normal(size=s).astype(np.float32), rng.normal(size=s).astype(np.float32)]
+    dev = torch.device("cuda:0")
+    ins = [torch.from_numpy(x).to(dev) for x in host]
+    wb = torch.empty(shapes[0], dtype=torch.bfloat16, device=dev)
+    outs = [ins[0], wb, ins[2]]  # in place on the masters
+    f.run(ins, outputs=outs)
+    torch.cuda.synchronize()
+    m = oracle.parse(text)
+    ref = oracle.run(m, "sgd", [x.astype(np.float64) for x in host])
+    assert_f32_parity(outs[0].cpu().double().numpy(), ref[0], what="W master")
+    assert_f32_parity(outs[2].cpu().double().numpy(), ref[3], what="b master")
+    got_b = wb.cpu().to(torch.float64).numpy()
+    np.testing.assert_array_equal(got_b, oracle.interp.bf16_round(outs[0].cpu().numpy()))

@@ -300,4 +300,27 @@ def fig4_ir(B: int = 4, I: int = 6, O: int = 5) -> str:
         f"func @dg: ({X}, {W}, {Bv}) -> ({W}, {Bv}, {V})", ""])
 
 
+def sgd_ir(shapes: Sequence[Tuple[int, ...]], lr: float = 1e-3, copies: Sequence[bool] = (),
+           module: str = "sgd") -> str:
+    """The SGD update of SURVEY §8(a) H12 as DLVM IR (P:L213 element-wise
+    binary ops): for every parameter p_i with gradient g_i,
+    p_i' = subtract(p_i, multiply(g_i, lr)); returned once, and a second
+    time when copies[i] (the caller requests that output as the bf16
+    operand copy the next step's dots read)."""
+    params, body, rets, rtypes = [], [], [], []
+    for i, s in enumerate(shapes):
+        T = _ty(s)
+        params += [(f"p{i}", T), (f"g{i}", T)]
+        body += [f"    %u{i} = multiply %g{i}: {T}, {lr!r}: f32", f"    %n{i} = subtract %p{i}: {T}, %u{i}: {T}"]
+        rets.append(f"%n{i}: {T}")
+        rtypes.append(T)
+        if i < len(copies) and copies[i]:
+            rets.append(f"%n{i}: {T}")
+            rtypes.append(T)
+    sig = ", ".join(t for _, t in params)
+    return "\n".join([f'module "{module}"', "stage raw", f"func @sgd: ({sig}) -> ({', '.join(rtypes)}) {{",
+                      "'entry(" + ", ".join(f"%{n}: {t}" for n, t in params) + "):"] + body +
+                     ["    return (" + ", ".join(rets) + ")", "}", ""])
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
