@@ -53,7 +53,7 @@ def peaks():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -61,6 +61,7 @@ class ClockSampler:
         self.gpu = gpu
         self.proc = None
         self.path = None
+        self.window = None  # (t0, t1) wall-clock seconds of the timed region
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -69,6 +70,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(1.0)  # nvidia-smi start-up, so samples cover the timed region
         except OSError:
             self.proc = None
         return self
@@ -82,23 +84,41 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        """Median SM clock and active throttle reasons of the samples taken
+        inside the timed window (all samples if the window caught none)."""
+        import datetime
         if not self.path or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         rows = []
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
+            if len(parts) >= 9:
                 rows.append(parts)
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+
+        def ts(r):
+            try:
+                return datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                return None
+
+        inside = rows
+        if self.window:
+            t0, t1 = self.window
+            w = [r for r in rows if ts(r) is not None and t0 - 0.06 <= ts(r) <= t1 + 0.06]
+            if w:
+                inside = w
+        num = lambda x: x.replace(".", "", 1).isdigit()
+        sm = [float(r[1]) for r in inside if num(r[1])]
+        mx = [float(r[2]) for r in inside if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower().startswith("active")})
-        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({n for r in inside for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        pw = [float(r[3]) for r in inside if num(r[3])]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(inside), "samples_total": len(rows),
+                "power_w_max": max(pw) if pw else None}
 
 
 # ------------------------------------------------------------- workloads
@@ -361,7 +381,9 @@ def main():
         step()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
+        t0 = time.time()
         ms = time_steps(step, K, dev, world)
+        clk.window = (t0, time.time())
     clocks = clk.summary()
     value = w.global_batch / (ms * 1e-3)
     # per-kernel breakdown (separate short pass with inter-launch events)

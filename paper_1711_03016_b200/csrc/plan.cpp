@@ -662,7 +662,7 @@ struct Planner {
         if (g.is_dot || g.merged_into >= 0) continue;
         if (g.shape != a.shape || g.perm != a.perm) continue;
         if (a.split >= 0 && g.split >= 0 && a.split != g.split) continue;
-        if (g.roots.size() + a.roots.size() > (size_t)kMaxStores - 1) continue;
+        if (store_count(g) + store_count(a) > kMaxStores) continue;
         {  // the merged program must fit the fixed-size EwProgram
           std::set<int> inl = g.inl, rd = g.reads;
           inl.insert(a.inl.begin(), a.inl.end());
@@ -698,6 +698,20 @@ struct Planner {
         break;
       }
     }
+  }
+
+  // stores a group will issue (homes are assigned later: estimate)
+  int store_count(const Node& n) const {
+    int c = 0;
+    for (auto& r : n.roots) {
+      if (r.kind == Root::Store) {
+        const VInfo& x = vi[r.v];
+        c += 1 + (int)x.more_outs.size() + (x.dot_use && opt.policy == Policy::BF16 ? 1 : 0);
+      } else if (r.kind != Root::Reduce) {
+        c += 1;
+      }
+    }
+    return c;
   }
 
   // an inlined element-wise value computed by two kernels is materialised,

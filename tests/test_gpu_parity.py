@@ -327,6 +327,6 @@ def test_sgd_update_two_outputs_one_kernel():
     m = oracle.parse(text)
     ref = oracle.run(m, "sgd", [x.astype(np.float64) for x in host])
     assert_f32_parity(outs[0].cpu().double().numpy(), ref[0], what="W master")
-    assert_f32_parity(outs[2].cpu().double().numpy(), ref[3], what="b master")
+    assert_f32_parity(outs[2].cpu().double().numpy(), ref[2], what="b master")
     got_b = wb.cpu().to(torch.float64).numpy()
     np.testing.assert_array_equal(got_b, oracle.interp.bf16_round(outs[0].cpu().numpy()))
