@@ -115,7 +115,10 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
  * need; the caller passes a buffer at least this large (256-byte aligned). */
 dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes);
 
-/* Number of kernel launches one run (which=0) / grad run (which=1) issues. */
+/* Number of kernel launches one run (which=0) / grad run (which=1) issues
+ * with every output bound as f32.  Binding an output that a single-partial
+ * reduction produces as bf16 adds one small finalize launch for it (not
+ * covered by dlvm_fn_launch_events). */
 dlvm_status dlvm_fn_num_launches(dlvm_fn fn, int which, int* launches);
 
 /* Execute the primal function on `cuda_stream` (a cudaStream_t; NULL = the

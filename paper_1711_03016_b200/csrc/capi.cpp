@@ -101,7 +101,11 @@ void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
     for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
     d.st = st;
   }
-  for (size_t i = 0; i < g.reduces.size(); ++i) p->red[i] = static_cast<float*>(b.ptr[g.reduces[i].buf]);
+  for (size_t i = 0; i < g.reduces.size(); ++i) {
+    const int hb = g.reduces[i].direct_buf;
+    const bool direct = hb >= 0 && b.st[hb] == (uint8_t)SType::F32;
+    p->red[i] = static_cast<float*>(b.ptr[direct ? hb : g.reduces[i].buf]);
+  }
 }
 
 // epilogue vectorisation along n: every ref must allow 4-wide access
@@ -192,8 +196,9 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
   };
   for (const Step& st : P.steps) {
     cudaError_t e = cudaSuccess;
-    const bool is_launch = st.kind == Step::EW || st.kind == Step::GEMM || (st.kind == Step::CAST && st.cast.ld);
-    if (is_launch && (e = mark(li++)) != cudaSuccess)
+    if (st.kind == Step::EW && st.ew.finalize && st.ew.direct_buf >= 0 && b.st[st.ew.direct_buf] == (uint8_t)SType::F32)
+      continue;  // the producer wrote the single partial into the f32 home
+    if (st.counted_launch() && (e = mark(li++)) != cudaSuccess)
       return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
     if (st.kind == Step::EW) {
       EwParams p;
@@ -245,7 +250,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       }
       else {
         if (g.tensor_core) return fail(DLVM_ERR_RUNTIME, "tensor-core dot operand misaligned");
-        e = launch_gemm_simt(gp, stream);
+        GemmLaunchFn sf = fn->specialize ? find_simt_spec(g.epi.sig.c_str(), g.bm) : nullptr;
+        e = sf ? sf(gp, stream) : launch_gemm_simt(gp, stream);
       }
     } else if (st.kind == Step::CAST) {
       const bool f32 = in[st.cast.input].dtype == DLVM_F32;
@@ -409,6 +415,8 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
             s += "EW " + std::to_string(st.ew.vec) + " " + st.ew.sig + "\n";
           else if (st.kind == Step::GEMM && st.gemm.tensor_core)
             s += "GEMM " + std::to_string(st.gemm.bn) + " " + st.gemm.epi.sig + "\n";
+          else if (st.kind == Step::GEMM)
+            s += "SIMT " + std::to_string(st.gemm.bm) + " " + st.gemm.epi.sig + "\n";
         }
         break;
       }
@@ -480,7 +488,7 @@ dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t 
   const Plan& P = fn->plan[which];
   int li = 0;
   for (const Step& st : P.steps) {
-    if (st.kind != Step::EW && st.kind != Step::GEMM && !(st.kind == Step::CAST && st.cast.ld)) continue;
+    if (!st.counted_launch()) continue;
     if (li++ != i) continue;
     if (buf && cap) {
       size_t n = std::min(cap - 1, st.desc.size());

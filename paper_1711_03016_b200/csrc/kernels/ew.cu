@@ -432,6 +432,7 @@ cudaError_t launch_spec_ew(const EwParams& p, int bx, int by, cudaStream_t strea
 // ---------------------------------------------------------- registry
 #define DLVM_SPEC_EW(VEC, SIG, ...) {SIG, VEC, &launch_spec_ew<VEC, __VA_ARGS__>},
 #define DLVM_SPEC_GEMM(IDX, BN, SIG, ...)
+#define DLVM_SPEC_SIMT(BM, SIG, ...)
 namespace {
 using namespace spec;
 const EwSpecEntry kEwSpecs[] = {
@@ -440,6 +441,7 @@ const EwSpecEntry kEwSpecs[] = {
 }  // namespace
 #undef DLVM_SPEC_EW
 #undef DLVM_SPEC_GEMM
+#undef DLVM_SPEC_SIMT
 
 EwLaunchFn find_ew_spec(const char* sig, int vec) {
   for (const EwSpecEntry* e = kEwSpecs; e->sig; ++e)

@@ -15,11 +15,13 @@ constexpr GemmLaunchFn pick_gemm() {
 using namespace spec;
 #define DLVM_SPEC_EW(VEC, SIG, ...)
 #define DLVM_SPEC_GEMM(IDX, BN, SIG, ...) {SIG, BN, pick_gemm<IDX, BN, __VA_ARGS__>()},
+#define DLVM_SPEC_SIMT(BM, SIG, ...)
 const GemmSpecEntry kTable[] = {
 #include "spec_programs.inc"
     {nullptr, 0, nullptr}};
 #undef DLVM_SPEC_EW
 #undef DLVM_SPEC_GEMM
+#undef DLVM_SPEC_SIMT
 }  // namespace
 
 const GemmSpecEntry* gemm_spec_table_1() { return kTable; }

@@ -55,7 +55,7 @@ std::string program_signature(const EwProgram& p) {
 
 int Plan::launches() const {
   int n = 0;
-  for (auto& s : steps) n += (s.kind == Step::EW || s.kind == Step::GEMM || (s.kind == Step::CAST && s.cast.ld)) ? 1 : 0;
+  for (auto& s : steps) n += s.counted_launch() ? 1 : 0;
   return n;
 }
 
@@ -1293,10 +1293,15 @@ struct Planner {
     for (auto& ri : reds) {
       int64_t n_out = ri.kind == RED_COL ? C : ri.kind == RED_ROW ? R : 1;
       int64_t nch = ri.kind == RED_COL ? gy : ri.kind == RED_ROW ? gx : gx * gy;
-      int pbuf = add_buf(BufferSlot::Work, -1, (size_t)(n_out * nch) * 4, SType::F32);
       Step& prod = plan.steps[step_index];
       EwGroup& pg = prod.kind == Step::GEMM ? prod.gemm.epi : prod.ew;
+      const auto& homes = vi[ri.value].homes;
+      // one partial: its layout is the value's own [n_out] row, so the
+      // producer writes an f32 home directly and the finalize is skipped
+      const int direct = nch == 1 && homes.size() == 1 && homes[0].st == SType::F32 ? homes[0].buf : -1;
+      int pbuf = add_buf(BufferSlot::Work, -1, (size_t)(n_out * nch) * 4, SType::F32);
       pg.reduces[ri.slot_index].buf = pbuf;
+      pg.reduces[ri.slot_index].direct_buf = direct;
       EwGroup fg;
       fg.ndims = 1;
       fg.dims[0] = n_out;
@@ -1326,11 +1331,13 @@ struct Planner {
       ew_launch(fg);
       fg.sig = program_signature(fg.prog);
       fg.finalize = true;
+      fg.direct_buf = direct;
       Step s;
       s.kind = Step::EW;
       s.ew = fg;
       s.desc = "finalize %" + f.names[ri.value] + " (" + std::to_string(nch) + " partials x " +
-               std::to_string(n_out) + ") of " + who;
+               std::to_string(n_out) + ") of " + who +
+               (direct >= 0 ? " [only when the output is bound as bf16; else written by the producer]" : "");
       s.ew.desc = s.desc;
       plan.steps.push_back(s);
     }
@@ -1427,7 +1434,10 @@ struct Planner {
     int64_t ldb = gm.b_kmajor ? gm.b.strides[1] : gm.b.strides[0];
     gm.tensor_core = bf && lda % 8 == 0 && ldb % 8 == 0 && gm.a.offset % 8 == 0 && gm.b.offset % 8 == 0 &&
                      gm.M >= 128 && gm.N >= 64 && gm.K >= 64;
-    gm.bm = gm.tensor_core ? 128 : 64;
+    // SIMT: 32-row tiles when 64-row tiles would not fill the SMs twice over
+    // (the tile fixes the epilogue partial layout, so it is chosen here)
+    const int64_t simt_tiles64 = ((gm.M + 63) / 64) * ((gm.N + 63) / 64);
+    gm.bm = gm.tensor_core ? 128 : (simt_tiles64 < 2 * 148 ? 32 : 64);
     gm.bn = gm.tensor_core ? (gm.N >= 256 ? 256 : 128) : 64;
     Node epi;
     if (n.fused_epilogue >= 0) epi = nodes[n.fused_epilogue];
@@ -1480,8 +1490,13 @@ struct Planner {
       const std::vector<IterRef>* st =
           s.kind == Step::EW ? &s.ew.stores : s.kind == Step::GEMM ? &s.gemm.epi.stores : nullptr;
       if (!st) continue;
-      for (auto& r : *st) {
-        const BufferSlot& b = plan.bufs[r.buf];
+      const EwGroup& g = s.kind == Step::EW ? s.ew : s.gemm.epi;
+      std::vector<int> written;
+      for (auto& r : *st) written.push_back(r.buf);
+      for (auto& r : g.reduces)  // single-partial reductions write their home directly
+        if (r.direct_buf >= 0) written.push_back(r.direct_buf);
+      for (int buf : written) {
+        const BufferSlot& b = plan.bufs[buf];
         if (b.kind == BufferSlot::Output && b.index < opt.n_grads) last[b.index] = (int)si;
       }
     }

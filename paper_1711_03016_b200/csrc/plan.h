@@ -60,6 +60,9 @@ struct IterRef {
   int nchunks = 1;
   int64_t chunk_stride = 0;
   SType st = SType::F32;
+  // reductions with a single partial: the value's f32 home, which the
+  // producer writes directly when that buffer is bound as f32 at run time
+  int direct_buf = -1;
 };
 
 struct EwGroup {
@@ -78,6 +81,7 @@ struct EwGroup {
   std::string desc;
   std::string sig;               // program_signature(prog): key of compile-time specialisations
   bool finalize = false;         // sum of reduction partials (dedicated kernel)
+  int direct_buf = -1;           // finalize: skipped when this buffer is bound as f32 (producer wrote it)
 };
 
 struct GemmStep {
@@ -103,6 +107,13 @@ struct Step {
   CastStep cast;
   int event_index = -1;          // EVENT: gradient index whose value is final
   std::string desc;
+  // a kernel launch counted by num_launches / launch events (conditional
+  // finalizes of single-partial reductions are not: they run only when the
+  // reduced output is bound as bf16)
+  bool counted_launch() const {
+    if (kind == EW) return !(ew.finalize && ew.direct_buf >= 0);
+    return kind == GEMM || (kind == CAST && cast.ld);
+  }
 };
 
 struct Plan {

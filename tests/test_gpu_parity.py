@@ -330,3 +330,43 @@ def test_sgd_update_two_outputs_one_kernel():
     assert_f32_parity(outs[2].cpu().double().numpy(), ref[2], what="b master")
     got_b = wb.cpu().to(torch.float64).numpy()
     np.testing.assert_array_equal(got_b, oracle.interp.bf16_round(outs[0].cpu().numpy()))
+
+
+def test_single_partial_reduction_output_bound_as_bf16():
+    """c1's db2 / db1 (and the kept loss) come from single-partial epilogue
+    reductions, which the GEMM writes straight into an f32 output; bound as
+    bf16 (dlvm.h: an f32 output may be requested as bf16) the conditional
+    finalize runs instead and must store bf16_round of the same f32 value."""
+    import torch
+    import paper_1711_03016_b200 as P
+    w = W.c1()
+    f = P.Function(w.text, w.fn, w.grad)
+    dev = torch.device("cuda:0")
+    ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
+    seed = torch.tensor(np.float32(w.seed()), device=dev)
+    ref = [o.cpu().numpy() for o in f.grad_run(ins, seed=seed)]
+    outs = f._outputs(1, dev, None)
+    bf = [1, 3, 4]  # db1 [1,128], db2 [1,10], loss
+    for k in bf:
+        outs[k] = torch.empty(outs[k].shape, dtype=torch.bfloat16, device=dev)
+    f.grad_run(ins, seed=seed, outputs=outs)
+    torch.cuda.synchronize()
+    for k, (o, r) in enumerate(zip(outs, ref)):
+        got = o.cpu().to(torch.float32).numpy()
+        want = bf16_round(r) if k in bf else r
+        assert np.array_equal(got.reshape(-1).view(np.uint32), np.asarray(want, np.float32).reshape(-1).view(np.uint32)), k
+
+
+def test_simt_split_k_shapes():
+    """SIMT dot (fp32 policy) on SM-starved grids, where K is split over a
+    thread-block cluster and summed through distributed shared memory, plus a
+    ragged tail in every dimension (A17 term bound)."""
+    for (M, K, N) in [(7, 1531, 13), (32, 784, 128), (1, 4096, 1), (65, 300, 70)]:
+        text = _dot_ir(M, K, N, False, False)
+        rng = np.random.default_rng(M * 7 + K)
+        a, b = rng.normal(size=(M, K)).astype(np.float32), rng.normal(size=(K, N)).astype(np.float32)
+        res = gpu_run(text, "f", None, [a, b], which="primal")
+        m = oracle.parse(text)
+        ins64 = [a.astype(np.float64), b.astype(np.float64)]
+        ref = oracle.run(m, "f", ins64)
+        assert_f32_parity(res["primal"][0], ref[0], term_bound(m, "f", ins64)[0], what=f"dot {M}x{K}x{N}")
