@@ -21,6 +21,13 @@ What it computes (PAPER.md = P, SPEC.md = S, line numbers):
                   reverse sweep over the chain rule, one VJP
                   rule per opcode (rule table, unbroadcast
                   S:L344-352).
+  * `canonical` - adjoint code generation: a gradient
+                  declaration canonicalised to IR (copy the primal body, then
+                  emit the adjoint rules as instructions in reverse order).
+                  Used for higher-order gradients (Fig. 4
+                  `d2g_dw2`): a declaration whose source is a declaration
+                  differentiates the source's canonical body.  First-order
+                  IR from it must equal `grad` (two independent routes).
   * `fd_grad`   - central finite differences used to pin `grad`.
 
 Parity pins live in tests/test_oracle_*.py (-m "not gpu").  Nothing here is
@@ -32,9 +39,10 @@ from .infer import broadcast_shapes, infer_module, expected_gradient_type
 from .interp import run, run_function
 from .vjp import grad, grad_function
 from .fd import fd_grad
+from .adjoint import canonical, adjoint_text
 
 __all__ = [
     "parse", "ParseError", "VerifyError", "Module", "Function", "Inst", "Operand",
     "TensorType", "broadcast_shapes", "infer_module", "expected_gradient_type",
-    "run", "run_function", "grad", "grad_function", "fd_grad",
+    "run", "run_function", "grad", "grad_function", "fd_grad", "canonical", "adjoint_text",
 ]

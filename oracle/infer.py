@@ -247,9 +247,10 @@ def infer_module(mod: Module) -> None:
         if src is None:
             raise VerifyError(cfg.line, cfg.col, f"unknown function @{cfg.source}")
         if not src.has_body:
-            raise VerifyError(cfg.line, cfg.col,
-                              f"gradient of a body-less function @{cfg.source} "
-                              "is not supported")
+            # higher order: the source is itself a gradient
+            # declaration; differentiate its canonical body (adjoint.py)
+            from .adjoint import canonical
+            src = canonical(mod, cfg.source, (fn.name,))
         params, results = expected_gradient_type(src, cfg)
         if list(fn.param_types) != params or list(fn.result_types) != results:
             raise VerifyError(fn.line, fn.col,

@@ -152,6 +152,9 @@ def grad_function(mod: Module, gfn: Function, inputs: Sequence, dot_policy=None)
     the seed last when `seedable` (Fig. 3 `@foo_grad_3`)."""
     cfg = gfn.gradient
     src = mod.functions[cfg.source]
+    if not src.has_body:  # higher order: differentiate the generated gradient function
+        from .adjoint import canonical
+        src = canonical(mod, cfg.source)
     n = len(src.param_types)
     seed = inputs[n] if cfg.seedable else None
     return grad(src, list(inputs[:n]), cfg.wrt, cfg.keeping,
