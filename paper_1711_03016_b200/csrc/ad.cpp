@@ -316,6 +316,28 @@ Function differentiate(const Function& src, const GradConfig& cfg, const std::st
   return g;
 }
 
+namespace {
+Function canonical_rec(const Module& m, const std::string& name, std::vector<std::string>& stack) {
+  const Function* f = nullptr;
+  for (auto& g : m.fns)
+    if (g.name == name) f = &g;
+  if (!f) throw Error(kStatusVerify, 0, 0, "unknown function @" + name);
+  if (f->has_body) return *f;
+  if (!f->grad) throw Error(kStatusVerify, f->line, f->col, "function @" + name + " has no body and no gradient attribute");
+  for (auto& s : stack)
+    if (s == name) throw Error(kStatusVerify, f->grad->line, f->grad->col, "cyclic gradient declaration @" + name);
+  stack.push_back(name);
+  Function src = canonical_rec(m, f->grad->source, stack);
+  stack.pop_back();
+  return differentiate(src, *f->grad, f->name);
+}
+}  // namespace
+
+Function canonical_function(const Module& m, const std::string& name) {
+  std::vector<std::string> stack;
+  return canonical_rec(m, name, stack);
+}
+
 // Remove instructions that do not (transitively) contribute to the result.
 void dead_code_elim(Function& f) {
   std::vector<char> live(f.types.size(), 0);

@@ -162,6 +162,9 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " NULL or not 16-byte aligned");
   }
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  // parameter i of the function: an input, or the seed (last parameter of a
+  // seedable gradient, passed separately; it may feed a dot and need a cast)
+  auto param = [&](int i) -> const dlvm_tensor& { return i < n_in ? in[i] : *seed; };
   Bound b;
   b.ptr.resize(P.bufs.size());
   b.st.resize(P.bufs.size());
@@ -181,8 +184,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         b.ptr[k] = seed->data;
         break;
       case BufferSlot::Work:
-        if (s.cast_of >= 0 && in[s.cast_of].dtype == DLVM_BF16 && s.cast_ld == 0)
-          b.ptr[k] = in[s.cast_of].data;
+        if (s.cast_of >= 0 && param(s.cast_of).dtype == DLVM_BF16 && s.cast_ld == 0)
+          b.ptr[k] = param(s.cast_of).data;
         else
           b.ptr[k] = static_cast<char*>(workspace) + s.offset;
         break;
@@ -254,13 +257,13 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         e = sf ? sf(gp, stream) : launch_gemm_simt(gp, stream);
       }
     } else if (st.kind == Step::CAST) {
-      const bool f32 = in[st.cast.input].dtype == DLVM_F32;
+      const dlvm_tensor& src = param(st.cast.input);
+      const bool f32 = src.dtype == DLVM_F32;
       if (st.cast.ld)
-        e = launch_pack_bf16(in[st.cast.input].data, f32, st.cast.numel / st.cast.cols, st.cast.cols,
-                             b.ptr[st.cast.dst_buf], st.cast.ld, stream);
+        e = launch_pack_bf16(src.data, f32, st.cast.numel / st.cast.cols, st.cast.cols, b.ptr[st.cast.dst_buf],
+                             st.cast.ld, stream);
       else if (f32)
-        e = launch_cast_bf16(static_cast<const float*>(in[st.cast.input].data), b.ptr[st.cast.dst_buf],
-                             st.cast.numel, stream);
+        e = launch_cast_bf16(static_cast<const float*>(src.data), b.ptr[st.cast.dst_buf], st.cast.numel, stream);
     } else if (st.kind == Step::EVENT) {
       if (events && events[st.event_index]) e = cudaEventRecord(static_cast<cudaEvent_t>(events[st.event_index]), stream);
     }
@@ -317,9 +320,11 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
   try {
     Module m = parse_module(std::string(module_text, len));
     verify_module(m);
-    Function* src = m.find(fn_name);
-    if (!src) return fail(DLVM_ERR_USAGE, std::string("no function @") + fn_name);
-    if (!src->has_body) return fail(DLVM_ERR_USAGE, std::string("@") + fn_name + " has no body");
+    if (!m.find(fn_name)) return fail(DLVM_ERR_USAGE, std::string("no function @") + fn_name);
+    // a gradient declaration as the primal is canonicalised first, so `grad`
+    // may differentiate a gradient function (higher order)
+    const Function primal = canonical_function(m, fn_name);
+    const Function* src = &primal;
     Function* decl = nullptr;
     if (grad_name) {
       decl = m.find(grad_name);

@@ -256,14 +256,19 @@ void verify_module(Module& m) {
     if (f.has_body) throw Error(kStatusVerify, f.line, f.col, "a gradient declaration has no body");
     Function* src = m.find(c.source);
     if (!src) throw Error(kStatusVerify, c.line, c.col, "unknown function @" + c.source);
-    if (!src->has_body)
-      throw Error(kStatusVerify, c.line, c.col, "gradient of a body-less function is not supported");
     std::vector<Type> p, r;
     expected_gradient_type(*src, c, &p, &r);
     if (p != f.params || r != f.results)
       throw Error(kStatusVerify, f.line, f.col,
                   "declared type of @" + f.name + " does not match the expected gradient type");
-    check_differentiable(*src, c);
+    if (src->has_body) {
+      check_differentiable(*src, c);
+    } else {
+      // higher order: the source is itself a gradient
+      // declaration; its canonical body (ad.cpp) must be differentiable too
+      const Function body = canonical_function(m, c.source);
+      check_differentiable(body, c);
+    }
   }
 }
 

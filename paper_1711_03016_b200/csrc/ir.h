@@ -155,6 +155,11 @@ void expected_gradient_type(const Function& src, const GradConfig& cfg, std::vec
                             std::vector<Type>* results);
 // ad.cpp
 Function differentiate(const Function& src, const GradConfig& cfg, const std::string& name);
+// The function `name` with a body: as written, or its gradient declaration
+// canonicalised by `differentiate` (recursively: a declaration of a
+// declaration is a higher-order gradient).  Throws a
+// verify error for cycles and unknown sources.
+Function canonical_function(const Module& m, const std::string& name);
 void dead_code_elim(Function& f);
 // printer.cpp
 std::string print_function(const Function& f);

@@ -227,3 +227,34 @@ def test_plan_launch_counts_configs():
     assert f.num_launches(1) <= 14
     f2 = _plan_only(W.c2(64, 128).text, "chain", "chain_grad")
     assert f2.num_launches(0) == 1 and f2.num_launches(1) == 3
+
+
+def test_higher_order_cpp_ad_equals_oracle():
+    """Gradient of a gradient function (Fig. 4 d2g_dw2 and an
+    MLP Hessian-vector product): the C++-generated second-order IR,
+    interpreted by the oracle in float64, equals the oracle's own second-order
+    result (its adjoint code generation + reverse sweep)."""
+    from test_oracle_higher_order import _mlp2, _scalar_sum_pow, fig4_second_order
+    rng = np.random.default_rng(17)
+    t = fig4_second_order(8, 12, 6)
+    m = oracle.parse(t)
+    ins = [rng.normal(size=p.shape) * 0.5 for p in m.functions["g"].param_types]
+    f = _plan_only(t, "dg", "d2g_dw2")
+    assert f.signature(1) == _oracle_sig(m, "d2g_dw2")
+    _ad_cross_check(t, "dg", "d2g_dw2", ins, rtol=1e-10)
+    text, P_ = _mlp2(5, 4, 6, 3, "sigmoid")
+    ins = [rng.normal(size=s) * 0.5 for _, s in P_]
+    _ad_cross_check(text, "df", "hvp", ins, rng.normal(size=(4, 6)), rtol=1e-10)
+    t3 = _scalar_sum_pow(3, 4, 3)
+    _ad_cross_check(t3, "d2", "d3", [np.array([0.5, -1.5, 2.0])], rtol=1e-12)
+    f3 = _plan_only(t3, "d2", "d3")
+    assert "unsupported" not in f3.print(3)
+
+
+def test_cyclic_gradient_declarations_error_class():
+    t = "<2 x f32>"
+    text = (f'module "c"\nstage raw\n[gradient @b]\nfunc @a: ({t}) -> {t}\n'
+            f"[gradient @a]\nfunc @b: ({t}) -> {t}\n")
+    with pytest.raises(oracle.VerifyError):
+        oracle.parse(text)
+    assert _status(text, "a") == 1

@@ -370,3 +370,57 @@ def test_simt_split_k_shapes():
         ins64 = [a.astype(np.float64), b.astype(np.float64)]
         ref = oracle.run(m, "f", ins64)
         assert_f32_parity(res["primal"][0], ref[0], term_bound(m, "f", ins64)[0], what=f"dot {M}x{K}x{N}")
+
+
+def test_higher_order_fig4_d2g_dw2_f32():
+    """Second-order gradient (Fig. 4 `d2g_dw2`) executed by the
+    same kernels: the handle's primal is the canonicalised `dg`, its
+    gradient differentiates `dg`'s output 0 w.r.t. w (A17 term bounds)."""
+    from test_oracle_higher_order import fig4_second_order
+    t = fig4_second_order(64, 96, 80)
+    m = oracle.parse(t)
+    rng = np.random.default_rng(23)
+    ins = [(rng.normal(size=p.shape) * s).astype(np.float32)
+           for p, s in zip(m.functions["g"].param_types, (1.0, 0.1, 0.1))]
+    res = gpu_run(t, "dg", "d2g_dw2", ins)
+    ins64 = [x.astype(np.float64) for x in ins]
+    bp = term_bound(oracle.parse('module "p"\nstage raw\n' + res["fn"].print(0)), "dg", ins64)
+    # out2 = tanh(x.w + b): the dot's accumulation error passes through the
+    # 1-Lipschitz tanh, so its bound is the pre-activation's sum|terms|
+    bp[2] = np.abs(ins64[0]) @ np.abs(ins64[1]) + np.abs(ins64[2])
+    for k, (g, r) in enumerate(zip(res["primal"], oracle.run(m, "dg", ins64))):
+        assert_f32_parity(g, r, bp[k], what=f"dg out{k}")
+    (ref,) = oracle.run(m, "d2g_dw2", ins64)
+    bound = term_bound(_grad_module(res), "d2g_dw2", ins64)[0]
+    assert_f32_parity(res["grad"][0], ref, bound, what="d2g_dw2")
+
+
+@pytest.mark.parametrize("prec,dims", [("f32", (48, 40, 56, 24)), ("bf16", (512, 256, 384, 128))])
+def test_higher_order_mlp_hessian_vector_product(prec, dims):
+    """MLP loss Hessian-vector product: [gradient @df from 0 wrt 1, 3
+    seedable] with the direction v as seed.  f32: A17 term bounds; bf16
+    (tcgen05 GEMMs for every dot of the second-order program): normwise 2e-2
+    against the oracle under the bf16 dot policy (A18')."""
+    from test_oracle_higher_order import _mlp2
+    B, I, H, O = dims
+    text, P_ = _mlp2(B, I, H, O, "tanh")
+    m = oracle.parse(text)
+    rng = np.random.default_rng(29)
+    ins = [(rng.normal(size=s) * (1.0 / np.sqrt(s[0]) if n.startswith("w") else 1.0)).astype(np.float32)
+           for n, s in P_]
+    v = rng.normal(size=(I, H)).astype(np.float32)
+    ins64 = [x.astype(np.float64) for x in ins] + [v.astype(np.float64)]
+    if prec == "f32":
+        res = gpu_run(text, "df", "hvp", ins, seed=v, which="grad")
+        ref = oracle.run(m, "hvp", ins64)
+        bounds = term_bound(_grad_module(res), "hvp", ins64)
+        for k, (g, r, b) in enumerate(zip(res["grad"], ref, bounds)):
+            assert_f32_parity(g, r, b, what=f"hvp out{k}")
+    else:
+        ins = [bf16_round(x) if n in ("x", "w1", "w2") else x for x, (n, _) in zip(ins, P_)]
+        ins64 = [x.astype(np.float64) for x in ins] + [v.astype(np.float64)]
+        res = gpu_run(text, "df", "hvp", ins, seed=v, dot_precision="bf16", which="grad")
+        assert "gemm tcgen05" in res["fn"].print(3)
+        ref = oracle.run(m, "hvp", ins64, dot_policy="bf16")
+        for k, (g, r) in enumerate(zip(res["grad"], ref)):
+            assert_normwise(g, r, 2e-2, what=f"hvp bf16 out{k}")
