@@ -218,20 +218,27 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       std::memset(&gp, 0, sizeof(gp));
       gp.M = g.M;
       gp.N = g.N;
-      gp.K = g.K;
-      const uint8_t sta = b.st[g.a.buf], stb = b.st[g.b.buf];
-      size_t ea = sta == (uint8_t)SType::BF16 ? 2 : 4, eb = stb == (uint8_t)SType::BF16 ? 2 : 4;
-      gp.a = static_cast<const char*>(b.ptr[g.a.buf]) + g.a.offset * ea;
-      gp.b = static_cast<const char*>(b.ptr[g.b.buf]) + g.b.offset * eb;
-      gp.a_s0 = g.a.strides[0];
-      gp.a_s1 = g.a.strides[1];
-      gp.b_s0 = g.b.strides[0];
-      gp.b_s1 = g.b.strides[1];
-      gp.a_kmajor = g.a_kmajor;
-      gp.b_kmajor = g.b_kmajor;
-      gp.bf16 = sta == (uint8_t)SType::BF16;
-      if ((sta == (uint8_t)SType::BF16) != (stb == (uint8_t)SType::BF16))
-        return fail(DLVM_ERR_RUNTIME, "dot operands with different storage types");
+      gp.n_seg = (int32_t)g.seg.size();
+      bool aligned = true;
+      for (size_t q = 0; q < g.seg.size(); ++q) {
+        const GemmSeg& sg = g.seg[q];
+        GemmSegParams& sp = gp.seg[q];
+        const uint8_t sta = b.st[sg.a.buf], stb = b.st[sg.b.buf];
+        if (sta != stb || (q > 0 && (sta == (uint8_t)SType::BF16) != (gp.bf16 != 0)))
+          return fail(DLVM_ERR_RUNTIME, "dot operands with different storage types");
+        gp.bf16 = sta == (uint8_t)SType::BF16;
+        const size_t ea = sta == (uint8_t)SType::BF16 ? 2 : 4;
+        sp.a = static_cast<const char*>(b.ptr[sg.a.buf]) + sg.a.offset * ea;
+        sp.b = static_cast<const char*>(b.ptr[sg.b.buf]) + sg.b.offset * ea;
+        sp.K = sg.K;
+        sp.a_s0 = sg.a.strides[0];
+        sp.a_s1 = sg.a.strides[1];
+        sp.b_s0 = sg.b.strides[0];
+        sp.b_s1 = sg.b.strides[1];
+        sp.a_kmajor = sg.a_kmajor;
+        sp.b_kmajor = sg.b_kmajor;
+        aligned = aligned && reinterpret_cast<uintptr_t>(sp.a) % 16 == 0 && reinterpret_cast<uintptr_t>(sp.b) % 16 == 0;
+      }
       gp.bm = g.bm;
       gp.bn = g.bn;
       to_dev(g.epi, b, &gp.epi);
@@ -246,7 +253,6 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         gp.pf_esize[gp.n_pf] = es;
         ++gp.n_pf;
       }
-      bool aligned = (reinterpret_cast<uintptr_t>(gp.a) % 16 == 0) && (reinterpret_cast<uintptr_t>(gp.b) % 16 == 0);
       if (g.tensor_core && aligned && gp.bf16) {
         GemmLaunchFn sf = fn->specialize ? find_gemm_spec(g.epi.sig.c_str(), g.bn) : nullptr;
         e = sf ? sf(gp, stream) : launch_gemm_tc(gp, stream);
@@ -298,8 +304,10 @@ double step_bytes(const Plan& P, const Step& st) {
   for (auto& r : g.reduces) (void)r;
   if (st.kind == Step::GEMM) {
     const GemmStep& m = st.gemm;
-    double e = m.tensor_core || P.bufs[m.a.buf].st == SType::BF16 ? 2.0 : 4.0;
-    b += (double)(m.M * m.K + m.K * m.N) * e;
+    for (auto& sg : m.seg) {
+      double e = m.tensor_core || P.bufs[sg.a.buf].st == SType::BF16 ? 2.0 : 4.0;
+      b += (double)(m.M * sg.K + sg.K * m.N) * e;
+    }
   }
   return b;
 }

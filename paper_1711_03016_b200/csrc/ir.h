@@ -53,6 +53,7 @@ enum class Op : uint8_t {
   DataTypeCast, // Table 1
   Slice,        // Table 1
   Sech2,        // planner-internal: subtract(1, multiply(tanh z, tanh z)) == sech^2(z) (reading A12)
+  DotSum,       // planner-internal: dot(A1,B1) + ... + dot(As,Bs), one GEMM with s K segments
 };
 const char* op_name(Op op);
 bool op_from_name(const std::string& s, Op* out);

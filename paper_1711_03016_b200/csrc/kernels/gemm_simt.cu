@@ -162,67 +162,73 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ 
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-  const int64_t kb = (int64_t)blockIdx.z * kchunk, ke = kb + kchunk < p.K ? kb + kchunk : p.K;
   float acc[TM][4];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  // element e of the A batch (BM x KB) / B batch (KB x BN), in the operand's
-  // contiguous order so consecutive threads read consecutive addresses
-  auto a_idx = [&](int e, int& kk, int& mm) {
-    if (p.a_kmajor) { kk = e % KB; mm = e / KB; } else { mm = e % BM; kk = e / BM; }
-  };
-  auto b_idx = [&](int e, int& kk, int& nn) {
-    if (p.b_kmajor) { kk = e % KB; nn = e / KB; } else { nn = e % BN; kk = e / BN; }
-  };
-  float ra[NA], rb[NB];
-  auto load = [&](int64_t k0) {
+  // K segments (sums of products, one accumulator); a split K (cluster)
+  // applies to single-segment GEMMs
+  for (int q = 0; q < p.n_seg; ++q) {
+    const GemmSegParams& G = p.seg[q];
+    const int64_t kb = gridDim.z > 1 ? (int64_t)blockIdx.z * kchunk : 0;
+    const int64_t ke = gridDim.z > 1 ? (kb + kchunk < G.K ? kb + kchunk : G.K) : G.K;
+    // element e of the A batch (BM x KB) / B batch (KB x BN), in the operand's
+    // contiguous order so consecutive threads read consecutive addresses
+    auto a_idx = [&](int e, int& kk, int& mm) {
+      if (G.a_kmajor) { kk = e % KB; mm = e / KB; } else { mm = e % BM; kk = e / BM; }
+    };
+    auto b_idx = [&](int e, int& kk, int& nn) {
+      if (G.b_kmajor) { kk = e % KB; nn = e / KB; } else { nn = e % BN; kk = e / BN; }
+    };
+    float ra[NA], rb[NB];
+    auto load = [&](int64_t k0) {
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-      int kk, mm;
-      a_idx(tid + i * 256, kk, mm);
-      const int64_t gm = m0 + mm, gk = k0 + kk;
-      ra[i] = (gm < p.M && gk < ke) ? ldop<BF16>(p.a, gm * p.a_s0 + gk * p.a_s1) : 0.f;
-    }
+      for (int i = 0; i < NA; ++i) {
+        int kk, mm;
+        a_idx(tid + i * 256, kk, mm);
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        ra[i] = (gm < p.M && gk < ke) ? ldop<BF16>(G.a, gm * G.a_s0 + gk * G.a_s1) : 0.f;
+      }
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      int kk, nn;
-      b_idx(tid + i * 256, kk, nn);
-      const int64_t gn = n0 + nn, gk = k0 + kk;
-      rb[i] = (gn < p.N && gk < ke) ? ldop<BF16>(p.b, gk * p.b_s0 + gn * p.b_s1) : 0.f;
-    }
-  };
-  if (kb < ke) load(kb);
-  for (int64_t k0 = kb; k0 < ke; k0 += KB) {
+      for (int i = 0; i < NB; ++i) {
+        int kk, nn;
+        b_idx(tid + i * 256, kk, nn);
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        rb[i] = (gn < p.N && gk < ke) ? ldop<BF16>(G.b, gk * G.b_s0 + gn * G.b_s1) : 0.f;
+      }
+    };
+    if (kb < ke) load(kb);
+    for (int64_t k0 = kb; k0 < ke; k0 += KB) {
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-      int kk, mm;
-      a_idx(tid + i * 256, kk, mm);
-      As[kk][mm] = ra[i];
-    }
+      for (int i = 0; i < NA; ++i) {
+        int kk, mm;
+        a_idx(tid + i * 256, kk, mm);
+        As[kk][mm] = ra[i];
+      }
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      int kk, nn;
-      b_idx(tid + i * 256, kk, nn);
-      Bs[kk][nn] = rb[i];
-    }
-    __syncthreads();
-    if (k0 + KB < ke) load(k0 + KB);  // in flight while this batch's FMAs run
-    const int kn = ke - k0 < KB ? (int)(ke - k0) : KB;
+      for (int i = 0; i < NB; ++i) {
+        int kk, nn;
+        b_idx(tid + i * 256, kk, nn);
+        Bs[kk][nn] = rb[i];
+      }
+      __syncthreads();
+      if (k0 + KB < ke) load(k0 + KB);  // in flight while this tile's FMAs run
+      const int kn = ke - k0 < KB ? (int)(ke - k0) : KB;
 #pragma unroll 4
-    for (int kk = 0; kk < kn; ++kk) {
-      float a[TM], b[4];
+      for (int kk = 0; kk < kn; ++kk) {
+        float a[TM], b[4];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+        for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (gridDim.z > 1) {
     // split K: partial tiles through distributed shared memory, summed by
@@ -334,17 +340,18 @@ cudaError_t launch_bm(const GemmParams& p, cudaStream_t stream) {
     const int64_t v = e ? std::atoll(e) : 8;
     return v < 1 ? 1 : (v > 8 ? 8 : v);
   }();
+  const int64_t K = p.seg[0].K;
   int64_t ks = 1;
-  if (tiles < 148) {
+  if (tiles < 148 && p.n_seg == 1) {
     ks = 296 / tiles;
-    const int64_t kmax = (p.K + 2 * BK - 1) / (2 * BK);
+    const int64_t kmax = (K + 2 * BK - 1) / (2 * BK);
     ks = ks < kmax ? ks : kmax;
     ks = ks < max_split ? ks : max_split;
     ks = ks > 1 ? ks : 1;
   }
-  int64_t kchunk = ((p.K + ks - 1) / ks + BK - 1) / BK * BK;
+  int64_t kchunk = ((K + ks - 1) / ks + BK - 1) / BK * BK;
   if (kchunk <= 0) kchunk = BK;
-  ks = p.K > 0 ? (p.K + kchunk - 1) / kchunk : 1;
+  ks = K > 0 ? (K + kchunk - 1) / kchunk : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)ks);
   cfg.blockDim = dim3(256, 1, 1);

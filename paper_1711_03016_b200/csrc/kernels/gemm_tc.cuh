@@ -36,8 +36,8 @@ constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 384;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
 struct TcParams {
-  CUtensorMap tma_a;
-  CUtensorMap tma_b;
+  CUtensorMap tma_a[kMaxSeg];  // per K segment (sums of products share one accumulator)
+  CUtensorMap tma_b[kMaxSeg];
   GemmParams g;
   int32_t tiles_m, tiles_n;
 };
@@ -491,7 +491,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles = P.tiles_m * P.tiles_n;
-  const int num_kb = (int)((g.K + BK - 1) / BK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -503,8 +502,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       mbar_init(tempty_bar + 8 * s, 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_b)) : "memory");
+    for (int q = 0; q < g.n_seg; ++q) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_a[q])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_b[q])) : "memory");
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
@@ -533,27 +534,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         }
       }
       if (lane == 0) {
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(empty_bar + 8 * s, ph ^ 1);
-          const uint32_t fb = full_bar + 8 * s;
-          mbar_expect_tx(fb, STAGE_TX);
-          const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
-          const int k0 = kb * BK;
-          if (g.a_kmajor) {
-            tma_load_2d(a_dst, &P.tma_a, fb, k0, m0);
-          } else {
-            tma_load_2d(a_dst, &P.tma_a, fb, m0, k0);
-            tma_load_2d(a_dst + 8192, &P.tma_a, fb, m0 + 64, k0);
-          }
-          if (g.b_kmajor) {
-            tma_load_2d(b_dst, &P.tma_b, fb, k0, n0);
-          } else {
+        for (int q = 0; q < g.n_seg; ++q) {
+          const GemmSegParams& G = g.seg[q];
+          const CUtensorMap* ma = &P.tma_a[q];
+          const CUtensorMap* mb = &P.tma_b[q];
+          const int num_kb = (int)((G.K + BK - 1) / BK);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(empty_bar + 8 * s, ph ^ 1);
+            const uint32_t fb = full_bar + 8 * s;
+            mbar_expect_tx(fb, STAGE_TX);
+            const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
+            const int k0 = kb * BK;
+            if (G.a_kmajor) {
+              tma_load_2d(a_dst, ma, fb, k0, m0);
+            } else {
+              tma_load_2d(a_dst, ma, fb, m0, k0);
+              tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0);
+            }
+            if (G.b_kmajor) {
+              tma_load_2d(b_dst, mb, fb, k0, n0);
+            } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, &P.tma_b, fb, n0 + 64 * c, k0);
-          }
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+              for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, n0 + 64 * c, k0);
+            }
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
       }
@@ -561,7 +568,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = umma_idesc(BN, !g.a_kmajor, !g.b_kmajor);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -571,20 +577,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         mbar_wait(tempty_bar + 8 * as, aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(full_bar + 8 * s, ph);
-          tc_fence_after();
-          const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
+        uint32_t accum = 0;  // the tile's first MMA overwrites the accumulator
+        for (int q = 0; q < g.n_seg; ++q) {
+          const GemmSegParams& G = g.seg[q];
+          const uint32_t idesc = umma_idesc(BN, !G.a_kmajor, !G.b_kmajor);
+          const int num_kb = (int)((G.K + BK - 1) / BK);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(full_bar + 8 * s, ph);
+            tc_fence_after();
+            const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = g.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
-            const uint64_t bd = g.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
-          }
-          umma_commit(empty_bar + 8 * s);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = G.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
+              const uint64_t bd = G.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
+              umma_bf16(d_tmem, ad, bd, idesc, accum);
+              accum = 1;
+            }
+            umma_commit(empty_bar + 8 * s);
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
         umma_commit(tfull_bar + 8 * as);
@@ -809,17 +822,21 @@ bool make_params(const GemmParams& p, TcParams* tp) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
   const int BN = p.bn;
-  bool ok;
-  if (p.a_kmajor)  // A [M,K], K contiguous: map {K, M}, box {64, 128}
-    ok = encode(&tp->tma_a, p.a, p.K, p.M, p.a_s0, BM);
-  else  // A stored [K][M]: map {M, K}, box {64, 64}
-    ok = encode(&tp->tma_a, p.a, p.M, p.K, p.a_s1, 64);
-  if (!ok) return false;
-  if (p.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN}
-    ok = encode(&tp->tma_b, p.b, p.K, p.N, p.b_s1, BN);
-  else  // B stored [K][N]: map {N, K}, box {64, 64}
-    ok = encode(&tp->tma_b, p.b, p.N, p.K, p.b_s0, 64);
-  if (!ok) return false;
+  if (p.n_seg < 1 || p.n_seg > kMaxSeg) return false;
+  for (int q = 0; q < p.n_seg; ++q) {
+    const GemmSegParams& G = p.seg[q];
+    bool ok;
+    if (G.a_kmajor)  // A [M,K], K contiguous: map {K, M}, box {64, 128}
+      ok = encode(&tp->tma_a[q], G.a, G.K, p.M, G.a_s0, BM);
+    else  // A stored [K][M]: map {M, K}, box {64, 64}
+      ok = encode(&tp->tma_a[q], G.a, p.M, G.K, G.a_s1, 64);
+    if (!ok) return false;
+    if (G.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN}
+      ok = encode(&tp->tma_b[q], G.b, G.K, p.N, G.b_s1, BN);
+    else  // B stored [K][N]: map {N, K}, box {64, 64}
+      ok = encode(&tp->tma_b[q], G.b, p.N, G.K, G.b_s0, 64);
+    if (!ok) return false;
+  }
   tp->tiles_m = (int)((p.M + BM - 1) / BM);
   tp->tiles_n = (int)((p.N + BN - 1) / BN);
   return true;

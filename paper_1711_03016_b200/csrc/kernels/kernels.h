@@ -41,13 +41,23 @@ struct EwParams {
 // element-wise program kernel over an [R, C] iteration space
 cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream);
 
-struct GemmParams {
-  int64_t M, N, K;
+constexpr int kMaxSeg = 8;
+
+// one K segment: sum_k A[m,k] B[k,n] over k < K
+struct GemmSegParams {
   const void* a;  // bf16 or f32
   const void* b;
+  int64_t K;
   int64_t a_s0, a_s1;  // A[m,k] at a + m*a_s0 + k*a_s1 (elements)
   int64_t b_s0, b_s1;  // B[k,n] at b + k*b_s0 + n*b_s1
   int32_t a_kmajor, b_kmajor;
+};
+
+// C[M,N] = sum over segments of A_s . B_s, then the epilogue program
+struct GemmParams {
+  int64_t M, N;
+  int32_t n_seg;
+  GemmSegParams seg[kMaxSeg];
   int32_t bf16;        // operand element type: 1 bf16, 0 f32
   int32_t bm, bn;      // tile; defines the epilogue partial layout
   EwParams epi;        // ndims 2, dims {M, N}; slot 0 = accumulator

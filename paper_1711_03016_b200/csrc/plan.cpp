@@ -181,13 +181,14 @@ struct Planner {
   static bool is_view(const Inst* in) {
     return in && (in->op == Op::Transpose || in->op == Op::ShapeCast || in->op == Op::Slice);
   }
+  static bool is_dotlike(Op op) { return op == Op::Dot || op == Op::DotSum; }
   static bool is_ew(const Inst* in) {
     return in && (is_elementwise(in->op) || in->op == Op::Sech2 || in->op == Op::DataTypeCast);
   }
   bool produced(int v) const {
     const Inst* in = def(v);
     if (!in || vi[v].dead) return false;
-    return in->op == Op::Dot || (in->op == Op::Reduce && red_root.count(v)) || vi[v].mat;
+    return is_dotlike(in->op) || (in->op == Op::Reduce && red_root.count(v)) || vi[v].mat;
   }
   SType natural(int v) const { return ty(v).dtype == DType::Bool ? SType::U8 : SType::F32; }
 
@@ -238,6 +239,41 @@ struct Planner {
     }
     std::vector<int> defidx(f.types.size(), -1);
     for (size_t k = 0; k < f.insts.size(); ++k) defidx[f.insts[k].result] = (int)k;
+    // linear algebra fusion: add(dot(A1,B1), dot(A2,B2))
+    // of single-use, same-shape products -> one DotSum (a GEMM whose K loop
+    // walks every product into one accumulator); chains of adds keep growing
+    // the sum, e.g. W x + U h + b -> DotSum(x, W, h, U) + b (the bias and the
+    // activation then fuse into the GEMM epilogue like any other)
+    {
+      std::vector<int> uses(f.types.size(), 0), is_ret(f.types.size(), 0);
+      for (auto& in : f.insts)
+        for (auto& o : in.ops)
+          if (!o.is_lit()) ++uses[o.value];
+      for (auto& o : f.ret)
+        if (!o.is_lit()) is_ret[o.value] = 1;
+      for (auto& in : f.insts) {
+        if (in.op != Op::Add || in.ops[0].is_lit() || in.ops[1].is_lit()) continue;
+        if (in.ops[0].value == in.ops[1].value) continue;
+        const auto& rs = f.types[in.result].shape;
+        auto fusable = [&](const Operand& o) {
+          const int d = defidx[o.value];
+          if (d < 0) return false;
+          const Op op = f.insts[d].op;
+          return (op == Op::Dot || op == Op::DotSum) && uses[o.value] == 1 && !is_ret[o.value] &&
+                 f.types[o.value].shape == rs;
+        };
+        if (!fusable(in.ops[0]) || !fusable(in.ops[1])) continue;
+        const Inst& x = f.insts[defidx[in.ops[0].value]];
+        const Inst& y = f.insts[defidx[in.ops[1].value]];
+        if ((int)(x.ops.size() + y.ops.size()) / 2 > kPlanMaxSeg) continue;
+        std::vector<Operand> ops = x.ops;
+        ops.insert(ops.end(), y.ops.begin(), y.ops.end());
+        --uses[in.ops[0].value];
+        --uses[in.ops[1].value];
+        in.op = Op::DotSum;
+        in.ops = ops;
+      }
+    }
     for (auto& in : f.insts) {  // subtract(1, multiply(t, t)), t = tanh(z) -> sech2(z)
       if (in.op != Op::Subtract || !in.ops[0].is_lit() || in.ops[0].lit != 1.0 || in.ops[1].is_lit()) continue;
       int m = defidx[in.ops[1].value];
@@ -268,7 +304,7 @@ struct Planner {
     for (size_t k = 0; k < f.ret.size(); ++k)
       if (!f.ret[k].is_lit()) vi[f.ret[k].value].outs.push_back((int)k);
     for (auto& in : f.insts) {
-      if (in.op != Op::Dot) continue;
+      if (!is_dotlike(in.op)) continue;
       for (auto& o : in.ops) {
         if (o.is_lit()) continue;
         int v = o.value;
@@ -443,7 +479,7 @@ struct Planner {
       Node n;
       n.pos = (int)k;
       n.writes.insert(v);
-      if (in.op == Op::Dot) {
+      if (is_dotlike(in.op)) {
         n.is_dot = true;
         n.dot_inst = (int)k;
       } else if (in.op == Op::Reduce && red_root.count(v)) {
@@ -852,7 +888,7 @@ struct Planner {
     for (size_t v = 0; v < f.types.size(); ++v) {
       VInfo& x = vi[v];
       if (!produced((int)v)) continue;
-      bool is_dot = def((int)v)->op == Op::Dot;
+      bool is_dot = is_dotlike(def((int)v)->op);
       bool others_read = false;
       if (is_dot && fused_dot_group.count((int)v)) {
         int g = fused_dot_group[(int)v];
@@ -1413,27 +1449,33 @@ struct Planner {
     GemmStep& gm = s.gemm;
     gm.M = ty(dv).shape[0];
     gm.N = ty(dv).shape[1];
-    gm.K = in.ops[0].type.shape[1];
     bool bf = opt.policy == Policy::BF16;
-    for (int k = 0; k < 2; ++k) {
-      const Operand& o = in.ops[k];
-      if (o.is_lit()) unsupported("dot of a literal operand");
-      TensorRef r;
-      if (!ref_of(o.value, bf, &r)) unsupported("dot operand not addressable");
-      if (bf && r.st != SType::BF16) unsupported("missing bf16 copy of a dot operand");
-      if (r.strides.size() != 2 || !(r.strides[1] == 1 || r.strides[0] == 1 || r.shape[0] == 1 || r.shape[1] == 1))
-        unsupported("dot operand needs a unit stride");
-      (k == 0 ? gm.a : gm.b) = r;
+    bool tc = bf && gm.M >= 128 && gm.N >= 64;
+    for (size_t p = 0; p + 1 < in.ops.size(); p += 2) {
+      GemmSeg sg;
+      sg.K = in.ops[p].type.shape[1];
+      for (int k = 0; k < 2; ++k) {
+        const Operand& o = in.ops[p + k];
+        if (o.is_lit()) unsupported("dot of a literal operand");
+        TensorRef r;
+        if (!ref_of(o.value, bf, &r)) unsupported("dot operand not addressable");
+        if (bf && r.st != SType::BF16) unsupported("missing bf16 copy of a dot operand");
+        if (r.strides.size() != 2 || !(r.strides[1] == 1 || r.strides[0] == 1 || r.shape[0] == 1 || r.shape[1] == 1))
+          unsupported("dot operand needs a unit stride");
+        (k == 0 ? sg.a : sg.b) = r;
+      }
+      // A [M,K]: K-major if K is the contiguous dim; B [K,N]: K-major if K is contiguous
+      sg.a_kmajor = sg.a.strides[1] == 1 && (sg.a.shape[0] == 1 || sg.a.strides[0] != 1 || sg.a.shape[1] == 1);
+      if (sg.a.strides[1] == 1 && sg.a.shape[1] != 1) sg.a_kmajor = true;
+      if (sg.a.strides[0] == 1 && sg.a.shape[0] != 1 && sg.a.strides[1] != 1) sg.a_kmajor = false;
+      sg.b_kmajor = sg.b.strides[0] == 1 && sg.b.shape[0] != 1 && sg.b.strides[1] != 1;
+      int64_t lda = sg.a_kmajor ? sg.a.strides[0] : sg.a.strides[1];
+      int64_t ldb = sg.b_kmajor ? sg.b.strides[1] : sg.b.strides[0];
+      tc = tc && lda % 8 == 0 && ldb % 8 == 0 && sg.a.offset % 8 == 0 && sg.b.offset % 8 == 0;
+      gm.K += sg.K;
+      gm.seg.push_back(sg);
     }
-    // A [M,K]: K-major if K is the contiguous dim; B [K,N]: K-major if K is contiguous
-    gm.a_kmajor = gm.a.strides[1] == 1 && (gm.a.shape[0] == 1 || gm.a.strides[0] != 1 || gm.a.shape[1] == 1);
-    if (gm.a.strides[1] == 1 && gm.a.shape[1] != 1) gm.a_kmajor = true;
-    if (gm.a.strides[0] == 1 && gm.a.shape[0] != 1 && gm.a.strides[1] != 1) gm.a_kmajor = false;
-    gm.b_kmajor = gm.b.strides[0] == 1 && gm.b.shape[0] != 1 && gm.b.strides[1] != 1;
-    int64_t lda = gm.a_kmajor ? gm.a.strides[0] : gm.a.strides[1];
-    int64_t ldb = gm.b_kmajor ? gm.b.strides[1] : gm.b.strides[0];
-    gm.tensor_core = bf && lda % 8 == 0 && ldb % 8 == 0 && gm.a.offset % 8 == 0 && gm.b.offset % 8 == 0 &&
-                     gm.M >= 128 && gm.N >= 64 && gm.K >= 64;
+    gm.tensor_core = tc && gm.K >= 64;
     // SIMT: 32-row tiles when 64-row tiles would not fill the SMs twice over
     // (the tile fixes the epilogue partial layout, so it is chosen here)
     const int64_t simt_tiles64 = ((gm.M + 63) / 64) * ((gm.N + 63) / 64);
@@ -1464,8 +1506,14 @@ struct Planner {
     gm.epi.sig = program_signature(gm.epi.prog);
     std::ostringstream d;
     d << (gm.tensor_core ? "gemm tcgen05 bf16" : (bf ? "gemm simt bf16" : "gemm simt f32")) << " %"
-      << f.names[dv] << " M=" << gm.M << " N=" << gm.N << " K=" << gm.K << " A:" << (gm.a_kmajor ? "K" : "M")
-      << "-major B:" << (gm.b_kmajor ? "K" : "N") << "-major; epilogue ops=" << (int)gm.epi.prog.n_ins
+      << f.names[dv] << " M=" << gm.M << " N=" << gm.N << " K=" << gm.K;
+    if (gm.seg.size() > 1) {
+      d << " (" << gm.seg.size() << " K segments:";
+      for (auto& sg : gm.seg) d << " " << sg.K;
+      d << ")";
+    }
+    d << " A:" << (gm.seg[0].a_kmajor ? "K" : "M") << "-major B:" << (gm.seg[0].b_kmajor ? "K" : "N")
+      << "-major; epilogue ops=" << (int)gm.epi.prog.n_ins
       << " in=" << (int)gm.epi.prog.n_in << " stores=" << (int)gm.epi.prog.n_stores
       << " reductions=" << (int)gm.epi.prog.n_reduces;
     if (n.fused_epilogue >= 0) {

@@ -84,10 +84,20 @@ struct EwGroup {
   int direct_buf = -1;           // finalize: skipped when this buffer is bound as f32 (producer wrote it)
 };
 
-struct GemmStep {
-  int64_t M = 0, N = 0, K = 0;
+constexpr int kPlanMaxSeg = 8;  // == kMaxSeg of kernels.h (checked in capi.cpp)
+
+// one K segment of a GEMM: the product a . b accumulated with the others
+struct GemmSeg {
   TensorRef a, b;                // a: [M,K], b: [K,N]; one unit stride each
+  int64_t K = 0;
   bool a_kmajor = true, b_kmajor = false;
+};
+
+struct GemmStep {
+  int64_t M = 0, N = 0, K = 0;   // K: total over the segments
+  // sum of products (linear algebra fusion: W x + U h + b
+  // is one GEMM whose K loop walks both products into one accumulator)
+  std::vector<GemmSeg> seg;
   bool tensor_core = false;      // tcgen05 (bf16) vs SIMT (f32/bf16 operands)
   int bm = 128, bn = 128;        // tile shape (partials layout of epilogue reductions)
   EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator

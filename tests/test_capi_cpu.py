@@ -258,3 +258,21 @@ def test_cyclic_gradient_declarations_error_class():
     with pytest.raises(oracle.VerifyError):
         oracle.parse(text)
     assert _status(text, "a") == 1
+
+
+def test_linear_algebra_fusion_rnn_plan():
+    """W x + U h + b is one matrix multiplication.  The
+    RNN's forward cells are single GEMMs with two K segments (bias and tanh
+    in the epilogue), and the weight gradients dW = sum_t x_t^T dZ_t,
+    dU = sum_t h_{t-1}^T dZ_t are single GEMMs with T K segments."""
+    T = 4
+    w = W.rnn(T, 256, 128, 192)
+    f = _plan_only(w.text, w.fn, w.grad, "bf16")
+    fwd, bwd = f.print(2), f.print(3)
+    assert fwd.count("gemm tcgen05") == T and fwd.count("(2 K segments: 128 192)") == T
+    assert bwd.count(f"({T} K segments: 256 256 256 256)") == 2
+    assert bwd.count("gemm tcgen05") == T + (T - 1) + 2
+    # the generated adjoint (C++ AD) is still the oracle's VJP
+    ws = W.rnn(3, 6, 4, 5, "f32")
+    ins = [x.astype(np.float64) for x in ws.inputs()]
+    _ad_cross_check(ws.text, ws.fn, ws.grad, ins, np.float64(ws.seed()))

@@ -424,3 +424,28 @@ def test_higher_order_mlp_hessian_vector_product(prec, dims):
         ref = oracle.run(m, "hvp", ins64, dot_policy="bf16")
         for k, (g, r) in enumerate(zip(res["grad"], ref)):
             assert_normwise(g, r, 2e-2, what=f"hvp bf16 out{k}")
+
+
+def test_rnn_two_segment_gemm_f32():
+    """Unrolled RNN (linear algebra fusion) under the fp32 dot
+    policy: multi-segment SIMT GEMMs, ragged shapes (A17 term bounds)."""
+    w = W.rnn(3, 70, 40, 52, "f32")
+    _check_f32(w, w.inputs(), w.seed())
+
+
+def test_rnn_multi_segment_gemm_bf16():
+    """Same program at tcgen05 shapes: forward cells with 2 K segments, dW and
+    dU with T K segments of mixed operand majors; normwise 2e-2 against the
+    oracle under the bf16 dot policy (A18')."""
+    w = W.rnn(4, 384, 192, 320)
+    m = oracle.parse(w.text)
+    ins = [bf16_round(x) if a.name.startswith(("x", "W", "U")) or a.name == "h0" else x
+           for x, a in zip(w.inputs(), w.args)]
+    res = gpu_run(w.text, w.fn, w.grad, ins, seed=w.seed(), dot_precision="bf16")
+    assert res["fn"].print(3).count("K segments") >= 2 + 4
+    ins64 = [x.astype(np.float64) for x in ins]
+    ref_p = oracle.run(m, w.fn, ins64, dot_policy="bf16")
+    assert_normwise(res["primal"][0], ref_p[0], 2e-2, what="rnn loss")
+    ref = oracle.run(m, w.grad, ins64 + [np.float64(w.seed())], dot_policy="bf16")
+    for k, (g, r) in enumerate(zip(res["grad"], ref)):
+        assert_normwise(g, r, 2e-2, what=f"rnn grad out{k}")

@@ -323,4 +323,44 @@ def sgd_ir(shapes: Sequence[Tuple[int, ...]], lr: float = 1e-3, copies: Sequence
                      ["    return (" + ", ".join(rets) + ")", "}", ""])
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+def rnn_ir(T: int, B: int, I: int, H: int, module: str = "rnn") -> str:
+    """Unrolled simple RNN (§3.1.2):
+    h_t = tanh(x_t W + h_{t-1} U + b), t = 1..T (row-vector convention, x_t
+    [B, I], h [B, H]), loss 0.5 * sum((h_T - y)^2), and
+    `[gradient @rnn wrt W, U, b keeping 0 seedable]`."""
+    xs = [(f"x{t}", (B, I)) for t in range(1, T + 1)]
+    params = xs + [("h0", (B, H)), ("W", (I, H)), ("U", (H, H)), ("b", (1, H)), ("y", (B, H))]
+    sig = ", ".join(_ty(s) for _, s in params)
+    X, Hs = _ty((B, I)), _ty((B, H))
+    lines = [f'module "{module}"', "stage raw", "", f"func @rnn: ({sig}) -> f32 {{",
+             "'entry(" + ", ".join(f"%{n}: {_ty(s)}" for n, s in params) + "):"]
+    for t in range(1, T + 1):
+        lines += [f"    %wx{t} = dot %x{t}: {X}, %W: {_ty((I, H))}",
+                  f"    %uh{t} = dot %h{t - 1}: {Hs}, %U: {_ty((H, H))}",
+                  f"    %s{t} = add %wx{t}: {Hs}, %uh{t}: {Hs}",
+                  f"    %z{t} = add %s{t}: {Hs}, %b: {_ty((1, H))}",
+                  f"    %h{t} = tanh %z{t}: {Hs}"]
+    lines += [f"    %r = subtract %h{T}: {Hs}, %y: {Hs}",
+              f"    %e = multiply %r: {Hs}, %r: {Hs}",
+              f"    %q = reduce %e: {Hs} by add along 1",
+              f"    %l = reduce %q: {_ty((B,))} by add along 0",
+              f"    %L = multiply %l: f32, 0.5: f32",
+              "    return %L: f32", "}", "",
+              f"[gradient @rnn wrt {T + 1}, {T + 2}, {T + 3} keeping 0 seedable]",
+              f"func @rnn_grad: ({sig}, f32) -> ({_ty((I, H))}, {_ty((H, H))}, {_ty((1, H))}, f32)"]
+    return "\n".join(lines) + "\n"
+
+
+def rnn(T: int = 8, B: int = 8192, I: int = 2048, H: int = 2048, dot_precision: str = "bf16") -> Workload:
+    """Config r (NEXT rank 2): the unrolled RNN above; x_t ~ N(0,1),
+    h0 ~ U(-0.5, 0.5), W, U Glorot, b ~ U(+-0.1), y ~ U(-0.5, 0.5), seed 1/B."""
+    args = [ArgSpec(f"x{t}", (B, I), ("normal",), batched=True) for t in range(1, T + 1)]
+    args += [ArgSpec("h0", (B, H), ("uniform", -0.5, 0.5), batched=True),
+             ArgSpec("W", (I, H), ("glorot", I, H)), ArgSpec("U", (H, H), ("glorot", H, H)),
+             ArgSpec("b", (1, H), ("uniform", -0.1, 0.1)),
+             ArgSpec("y", (B, H), ("uniform", -0.5, 0.5), batched=True)]
+    return Workload(6, "rnn", rnn_ir(T, B, I, H), "rnn", "rnn_grad", args, seed_value=1.0 / B,
+                    dot_precision=dot_precision, batch=B, global_batch=B)
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "rnn": rnn}
