@@ -278,6 +278,56 @@ def bench_chain(dev, K, W_):
             "launches_fwd_adj": f.num_launches(1), "kernels": [{"desc": r["desc"][:80], "ms": r["ms"]} for r in kb]}
 
 
+def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
+    """One gradient step of a NEXT-row workload (rnn: linear algebra fusion;
+    mlp_hvp: a second-order gradient) through dlvm_grad_run: samples/s,
+    algorithmic TFLOP/s of its GEMMs against the tensor roofline, and the
+    oracle on a bounded row sample of the same program (`small(rows)`)."""
+    import numpy as np
+    import torch
+    import oracle
+    import paper_1711_03016_b200 as P
+    f = P.Function(w.text, w.fn, w.grad, dot_precision=w.dot_precision)
+    ins = [to_dev(x, dev, a.name in bf16_args) for x, a in zip(w.inputs(), w.args)]
+    sd = w.seed()
+    seed = to_dev(np.asarray(sd, dtype=np.float32), dev) if sd is not None else None
+    outs = f._outputs(1, dev, None)
+    ws = f._workspace(1, dev)
+    step = lambda: f.grad_run(ins, seed=seed, outputs=outs, workspace=ws)
+    for _ in range(W_):
+        step()
+    ms = time_steps(step, K, dev, 1)
+    kb = kernel_breakdown(f, 1, step, min(K, 5), dev)
+    gemm = [r for r in kb if r["flops"] > 0]
+    flops = sum(r["flops"] for r in gemm)
+    gemm_ms = sum(r["ms"] for r in gemm)
+    pk = peaks()
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    ach = flops / (gemm_ms * 1e-3) / 1e12
+    out = {"workload": w.name, "value": w.global_batch / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms,
+           "step_tflops": flops / (ms * 1e-3) / 1e12, "launches": f.num_launches(1),
+           "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                        "kernel": "all GEMMs of the step", "algorithmic_flops_per_step": flops,
+                        "gemm_share_of_step": gemm_ms / sum(r["ms"] for r in kb)},
+           "kernels": [{"desc": r["desc"][:110], "ms": round(r["ms"], 4)} for r in sorted(kb, key=lambda r: -r["ms"])[:6]]}
+    try:
+        cores = oracle_threads()
+        ws_ = small(cpu_rows)
+        m = oracle.parse(ws_.text)
+        args = [x.astype(np.float64) for x in ws_.inputs()]
+        sd = ws_.seed()
+        if sd is not None:
+            args.append(np.asarray(sd, dtype=np.float64))
+        t0 = time.perf_counter()
+        oracle.run(m, ws_.grad, args)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": cpu_rows / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{cpu_rows} rows of {w.name} (full-size weights), float64 numpy ({dt:.2f} s)"}
+    except Exception as ex:  # noqa: BLE001
+        out["cpu_baseline"] = {"error": repr(ex)}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -287,6 +337,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-elementwise", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the rnn / mlp_hvp legs (SURVEY §8(f) rows)")
     ap.add_argument("--cpu-rows", type=int, default=None)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: on for the launch-bound c1)")
@@ -511,6 +562,16 @@ def main():
                 ew["cpu_baseline"] = cpu_baseline_chain(256)
             except Exception as ex:  # noqa: BLE001
                 ew["cpu_baseline"] = {"error": repr(ex)}
+        if not args.no_next:
+            legs = {}
+            rnn = WL.rnn()
+            legs["rnn"] = bench_grad_leg(rnn, lambda r: WL.rnn(8, r, 2048, 2048), dev, K, W_,
+                                         {"W", "U", "h0"} | {f"x{t}" for t in range(1, 9)}, 16)
+            hv = WL.mlp_hvp()
+            legs["mlp_hvp"] = bench_grad_leg(hv, lambda r: WL.mlp_hvp(r), dev, K, W_, {"x", "W1", "W2"}, 16)
+            for v in legs.values():
+                out["gpu_launches"] += v["launches"] * K
+            out["next_rows"] = legs
     if rank == 0:
         print(json.dumps(out))
     if world > 1:

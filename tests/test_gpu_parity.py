@@ -286,12 +286,19 @@ def test_random_programs(seed):
         assert_f32_parity(g, r, b, what=f"random grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
 
 
-@pytest.mark.parametrize("case", ["c2", "c3", "c5"])
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", "c5", "rnn", "hvp"])
 def test_specialized_programs_bit_identical_to_interpreter(case):
     """Compile-time specialised programs (spec_programs.inc) and the generic
-    interpreter evaluate the same ops in the same order: bit-identical."""
+    interpreter evaluate the same ops in the same order: bit-identical
+    (EW kernels, tcgen05 epilogues, SIMT epilogues)."""
     import paper_1711_03016_b200 as P
-    if case == "c2":
+    if case == "c1":
+        w, prec = W.c1(), "f32"
+    elif case == "rnn":
+        w, prec = W.rnn(8, 256, 128, 192), "bf16"
+    elif case == "hvp":
+        w, prec = W.mlp_hvp(256, 128, 192, 64), "bf16"
+    elif case == "c2":
         w, prec = W.c2(256, 4096), "f32"
     elif case == "c3":
         w, prec = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)]), "bf16"

@@ -363,4 +363,41 @@ def rnn(T: int = 8, B: int = 8192, I: int = 2048, H: int = 2048, dot_precision: 
                     dot_precision=dot_precision, batch=B, global_batch=B)
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "rnn": rnn}
+def mlp_hvp_ir(B: int, I: int, H: int, O: int, module: str = "hvp") -> str:
+    """Higher-order AD: a 2-layer
+    tanh MLP with MSE loss `@f`, its gradient `@df` w.r.t. W1, b1, W2, and the
+    gradient of `@df`'s first output (dL/dW1) w.r.t. W1 and W2, seeded with a
+    direction v: a Hessian-vector product `@hvp(x, W1, b1, W2, y, v)`."""
+    P = [("x", (B, I)), ("W1", (I, H)), ("b1", (1, H)), ("W2", (H, O)), ("y", (B, O))]
+    sig = ", ".join(_ty(s) for _, s in P)
+    Hs, Os = _ty((B, H)), _ty((B, O))
+    lines = [f'module "{module}"', "stage raw", "", f"func @f: ({sig}) -> f32 {{",
+             "'entry(" + ", ".join(f"%{n}: {_ty(s)}" for n, s in P) + "):",
+             f"    %z = dot %x: {_ty((B, I))}, %W1: {_ty((I, H))}",
+             f"    %a = add %z: {Hs}, %b1: {_ty((1, H))}",
+             f"    %h = tanh %a: {Hs}",
+             f"    %o = dot %h: {Hs}, %W2: {_ty((H, O))}",
+             f"    %r = subtract %o: {Os}, %y: {Os}",
+             f"    %e = multiply %r: {Os}, %r: {Os}",
+             f"    %q = reduce %e: {Os} by add along 1",
+             f"    %l = reduce %q: {_ty((B,))} by add along 0",
+             f"    %L = multiply %l: f32, 0.5: f32",
+             "    return %L: f32", "}", "",
+             "[gradient @f wrt 1, 2, 3]",
+             f"func @df: ({sig}) -> ({_ty((I, H))}, {_ty((1, H))}, {_ty((H, O))})", "",
+             "[gradient @df from 0 wrt 1, 3 seedable]",
+             f"func @hvp: ({sig}, {_ty((I, H))}) -> ({_ty((I, H))}, {_ty((H, O))})"]
+    return "\n".join(lines) + "\n"
+
+
+def mlp_hvp(B: int = 8192, I: int = 4096, H: int = 4096, O: int = 1000) -> Workload:
+    """Config h (NEXT rank 3): Hessian-vector product of the MLP above; x ~
+    N(0,1), Glorot weights, b ~ U(+-0.1), y one-hot, direction v ~ N(0,1)."""
+    args = [ArgSpec("x", (B, I), ("normal",), batched=True), ArgSpec("W1", (I, H), ("glorot", I, H)),
+            ArgSpec("b1", (1, H), ("uniform", -0.1, 0.1)), ArgSpec("W2", (H, O), ("glorot", H, O)),
+            ArgSpec("y", (B, O), ("onehot",), batched=True)]
+    return Workload(7, "mlp_hvp", mlp_hvp_ir(B, I, H, O), "df", "hvp", args,
+                    seed_spec=ArgSpec("v", (I, H), ("normal",)), dot_precision="bf16", batch=B, global_batch=B)
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "rnn": rnn, "mlp_hvp": mlp_hvp}
