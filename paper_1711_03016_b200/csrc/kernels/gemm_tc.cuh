@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include <type_traits>
@@ -65,6 +66,37 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// CTA-pair (cta_group::2) primitives: a shared::cluster address of the same
+// offset in CTA `rank` of the cluster, remote arrive, cluster barrier
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// relaxed: it only has to follow this warp's completed TMEM reads (wait::ld +
+// fence::before_thread_sync), not its global stores; a release arrive
+// compiles to MEMBAR.ALL.GPU and stalls the epilogue on its own stores
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// both CTAs of a pair load their half; the bytes complete on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
                                             int32_t c1) {
   asm volatile(
@@ -85,15 +117,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// instruction descriptor for kind::f16: bf16 x bf16 -> f32, M=128, N=n
-__host__ __device__ constexpr uint32_t umma_idesc(int n, bool a_mn, bool b_mn) {
+// instruction descriptor for kind::f16: bf16 x bf16 -> f32, M=m (128, or 256
+// for a CTA pair), N=n
+__host__ __device__ constexpr uint32_t umma_idesc(int n, bool a_mn, bool b_mn, int m = BM) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
          | (1u << 10)                    // B format bf16
          | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K)
          | ((b_mn ? 1u : 0u) << 16)      // B major (0 = K)
          | ((uint32_t)(n >> 3) << 17)    // N >> 3
-         | ((uint32_t)(BM >> 4) << 24);  // M >> 4
+         | ((uint32_t)(m >> 4) << 24);   // M >> 4
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -106,6 +139,21 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
+}
+// CTA pair: issued by the leader; one MMA spans both CTAs' smem and TMEM
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -462,7 +510,17 @@ struct vm_cw<VmEpi<CW>> {
 };
 __host__ __device__ constexpr int epi_chunk_width(int slots) { return slots <= 6 ? 16 : (slots <= 12 ? 8 : 4); }
 
-template <int BN, class PROG>
+// CTAS = 1: one CTA per 128 x BN tile.  CTAS = 2: a CTA pair (cluster of 2
+// on one TPC) per 256 x BN tile: each CTA stages its 128 rows of A and half
+// of B's columns, the leader issues cta_group::2 MMAs over both CTAs' smem
+// into both CTAs' TMEM (per-SM smem traffic per MMA drops by a third), and
+// each CTA runs the epilogue of its own 128 rows.
+template <int CTAS, int BN>
+__host__ __device__ constexpr int num_stages() {
+  return CTAS == 2 ? 6 : STAGES;
+}
+
+template <int BN, class PROG, int CTAS = 1>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
   constexpr int VMCW = vm_cw<PROG>::value;
   constexpr bool SPEC = VMCW == 0;
@@ -470,36 +528,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                                VmEpiTraits>;
   constexpr int NS = T::kSlots;
   constexpr int NRS = epi_num_reds<T, SPEC>();
-  constexpr int B_STAGE_BYTES = BN * BK * 2;
-  constexpr uint32_t STAGE_TX = A_STAGE_BYTES + B_STAGE_BYTES;
+  constexpr int NST = num_stages<CTAS, BN>();
+  constexpr int BNC = BN / CTAS;                     // B columns staged per CTA
+  constexpr int B_STAGE_BYTES = BNC * BK * 2;
+  constexpr uint32_t STAGE_TX = A_STAGE_BYTES + B_STAGE_BYTES;  // per CTA
   constexpr int TMEM_COLS = 2 * BN;  // 256 or 512
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sA = base;
-  const uint32_t sB = base + STAGES * A_STAGE_BYTES;
-  const uint32_t sBar = sB + STAGES * B_STAGE_BYTES;  // full[S], empty[S], tfull[2], tempty[2]
-  const uint32_t full_bar = sBar, empty_bar = sBar + 8 * STAGES, tfull_bar = sBar + 16 * STAGES,
+  const uint32_t sB = base + NST * A_STAGE_BYTES;
+  const uint32_t sBar = sB + NST * B_STAGE_BYTES;  // full[S], empty[S], tfull[2], tempty[2]
+  const uint32_t full_bar = sBar, empty_bar = sBar + 8 * NST, tfull_bar = sBar + 16 * NST,
                  tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * STAGES + 32);
-  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * STAGES + 64);  // [kEpiReds][4][BN]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * NST + 32);
+  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * NST + 64);  // [kEpiReds][4][BN]
   float* rowred = colred + kEpiReds * 4 * BN;                                          // [kEpiReds][2][BM]
   float* allred = rowred + kEpiReds * 2 * BM;                                          // [kEpiReds][8]
-  float* xpose = allred + kEpiReds * 8;                                                // [8][32][17]
 
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = P.tiles_m * P.tiles_n;
+  const int n_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
+  const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
+  const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(full_bar + 8 * s, 1);
       mbar_init(empty_bar + 8 * s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + 8 * s, 1);
-      mbar_init(tempty_bar + 8 * s, 256);
+      mbar_init(tempty_bar + 8 * s, 8 * CTAS);  // one arrival per epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < g.n_seg; ++q) {
@@ -508,22 +569,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CTAS == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
     int s = 0;
     uint32_t ph = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = tile0; t < n_tiles; t += tile_step) {
       int tm, tn;
       tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
-      const int m0 = tm * BM, n0 = tn * BN;
+      const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
       for (int i = 0; i < g.n_pf; ++i) {
         const int64_t cols = min((int64_t)BN, g.N - n0);
         const uint32_t bytes = (uint32_t)((cols * g.pf_esize[i] + 15) & ~15);
@@ -542,22 +610,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(empty_bar + 8 * s, ph ^ 1);
             const uint32_t fb = full_bar + 8 * s;
-            mbar_expect_tx(fb, STAGE_TX);
             const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
             const int k0 = kb * BK;
-            if (G.a_kmajor) {
-              tma_load_2d(a_dst, ma, fb, k0, m0);
-            } else {
-              tma_load_2d(a_dst, ma, fb, m0, k0);
-              tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0);
-            }
-            if (G.b_kmajor) {
-              tma_load_2d(b_dst, mb, fb, k0, n0);
-            } else {
+            const int nb = n0 + (int)rank * BNC;  // this CTA's half of B
+            if constexpr (CTAS == 2) {
+              // both halves complete on the leader's barrier, armed with both CTAs' bytes
+              const uint32_t lb = mapa_rank(fb, 0);
+              if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_TX);
+              if (G.a_kmajor) {
+                tma_load_2d_pair(a_dst, ma, lb, k0, m0);
+              } else {
+                tma_load_2d_pair(a_dst, ma, lb, m0, k0);
+                tma_load_2d_pair(a_dst + 8192, ma, lb, m0 + 64, k0);
+              }
+              if (G.b_kmajor) {
+                tma_load_2d_pair(b_dst, mb, lb, k0, nb);
+              } else {
 #pragma unroll
-              for (int c = 0; c < BN / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, n0 + 64 * c, k0);
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d_pair(b_dst + c * 8192, mb, lb, nb + 64 * c, k0);
+              }
+            } else {
+              mbar_expect_tx(fb, STAGE_TX);
+              if (G.a_kmajor) {
+                tma_load_2d(a_dst, ma, fb, k0, m0);
+              } else {
+                tma_load_2d(a_dst, ma, fb, m0, k0);
+                tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0);
+              }
+              if (G.b_kmajor) {
+                tma_load_2d(b_dst, mb, fb, k0, nb);
+              } else {
+#pragma unroll
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, nb + 64 * c, k0);
+              }
             }
-            if (++s == STAGES) {
+            if (++s == NST) {
               s = 0;
               ph ^= 1;
             }
@@ -567,11 +654,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(tempty_bar + 8 * as, aph ^ 1);
@@ -580,7 +667,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         uint32_t accum = 0;  // the tile's first MMA overwrites the accumulator
         for (int q = 0; q < g.n_seg; ++q) {
           const GemmSegParams& G = g.seg[q];
-          const uint32_t idesc = umma_idesc(BN, !G.a_kmajor, !G.b_kmajor);
+          const uint32_t idesc = umma_idesc(BN, !G.a_kmajor, !G.b_kmajor, BM * CTAS);
           const int num_kb = (int)((G.K + BK - 1) / BK);
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(full_bar + 8 * s, ph);
@@ -590,17 +677,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = G.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
               const uint64_t bd = G.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
-              umma_bf16(d_tmem, ad, bd, idesc, accum);
+              if constexpr (CTAS == 2)
+                umma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+              else
+                umma_bf16(d_tmem, ad, bd, idesc, accum);
               accum = 1;
             }
-            umma_commit(empty_bar + 8 * s);
-            if (++s == STAGES) {
+            if constexpr (CTAS == 2)
+              umma_commit_pair(empty_bar + 8 * s);  // both CTAs' slots are free
+            else
+              umma_commit(empty_bar + 8 * s);
+            if (++s == NST) {
               s = 0;
               ph ^= 1;
             }
           }
         }
-        umma_commit(tfull_bar + 8 * as);
+        if constexpr (CTAS == 2)
+          umma_commit_pair(tfull_bar + 8 * as);
+        else
+          umma_commit(tfull_bar + 8 * as);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
@@ -643,9 +739,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       }
     const bool vec_ok = E.vec == 4;
     int it = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
       int tm, tn;
       tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      tm = tm * CTAS + (int)rank;  // this CTA's 128-row block (partials layout)
+      const bool block_live = (int64_t)tm * BM < g.M;
       const int64_t m = (int64_t)tm * BM + 32 * q + lane;
       const bool mval = m < g.M;
       const int as = it & 1;
@@ -721,9 +819,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           }
         }
       }
-      // accumulator buffer free for the next tile's MMAs
+      // accumulator buffer free for the next tile's MMAs (one arrival per warp,
+      // on the leader's barrier for a pair)
       tc_fence_before();
-      mbar_arrive(tempty_bar + 8 * as);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CTAS == 2)
+          mbar_arrive_cluster(mapa_rank(tempty_bar + 8 * as, 0));
+        else
+          mbar_arrive(tempty_bar + 8 * as);
+      }
       if (has_row || has_all) {
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
@@ -735,7 +840,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           }
         }
       }
-      if (has_col || has_row || has_all) {
+      if ((has_col || has_row || has_all) && block_live) {
         epi_bar();
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
@@ -767,9 +872,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // the pair's MMAs and epilogues are done
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+    if constexpr (CTAS == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
 }
 
@@ -801,11 +910,13 @@ bool encode(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int CTAS = 1>
 constexpr int smem_bytes() {
-  return 1024 + STAGES * (A_STAGE_BYTES + BN * BK * 2) + 16 * STAGES + 64 +
+  constexpr int NST = num_stages<CTAS, BN>();
+  return 1024 + NST * (A_STAGE_BYTES + (BN / CTAS) * BK * 2) + 16 * NST + 64 +
          (kEpiReds * 4 * BN + kEpiReds * 2 * BM + kEpiReds * 8 + 8 * 32 * 17) * 4;
 }
+static_assert(smem_bytes<256, 2>() <= 227 * 1024, "CTA-pair stages exceed shared memory");
 
 int num_sms() {
   static int n = 0;
@@ -818,7 +929,7 @@ int num_sms() {
   return n;
 }
 
-bool make_params(const GemmParams& p, TcParams* tp) {
+bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
   const int BN = p.bn;
@@ -831,32 +942,62 @@ bool make_params(const GemmParams& p, TcParams* tp) {
     else  // A stored [K][M]: map {M, K}, box {64, 64}
       ok = encode(&tp->tma_a[q], G.a, p.M, G.K, G.a_s1, 64);
     if (!ok) return false;
-    if (G.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN}
-      ok = encode(&tp->tma_b[q], G.b, G.K, p.N, G.b_s1, BN);
+    if (G.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN / ctas} (a CTA's share)
+      ok = encode(&tp->tma_b[q], G.b, G.K, p.N, G.b_s1, BN / ctas);
     else  // B stored [K][N]: map {N, K}, box {64, 64}
       ok = encode(&tp->tma_b[q], G.b, p.N, G.K, G.b_s0, 64);
     if (!ok) return false;
   }
-  tp->tiles_m = (int)((p.M + BM - 1) / BM);
+  tp->tiles_m = (int)((p.M + BM * ctas - 1) / (BM * ctas));
   tp->tiles_n = (int)((p.N + BN - 1) / BN);
   return true;
 }
 
-template <int BN, class PROG>
-cudaError_t launch_prog(const GemmParams& p, cudaStream_t stream) {
+// CTA pairs for large 256-wide tiles (DLVM_GEMM_CTA2=0 forces single CTAs)
+bool use_cta_pair(const GemmParams& p) {
+  static const int mode = [] {
+    const char* e = std::getenv("DLVM_GEMM_CTA2");
+    return e ? std::atoi(e) : 1;
+  }();
+  return mode != 0 && p.bn == 256 && p.M >= 512;
+}
+
+template <int BN, class PROG, int CTAS>
+cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
-  constexpr int SMEM = smem_bytes<BN>();
+  constexpr int SMEM = smem_bytes<BN, CTAS>();
+  auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, PROG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   TcParams tp;
-  if (!make_params(p, &tp)) return cudaErrorInvalidValue;
+  if (!make_params(p, &tp, CTAS)) return cudaErrorInvalidValue;
   const int tiles = tp.tiles_m * tp.tiles_n;
-  const int grid = std::min(tiles, num_sms());
-  gemm_tc_kernel<BN, PROG><<<grid, NUM_THREADS, SMEM, stream>>>(tp);
-  return cudaGetLastError();
+  const int grid = CTAS * std::min(tiles, num_sms() / CTAS);  // persistent: one CTA (pair) per SM (pair)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CTAS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CTAS > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tp);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int BN, class PROG>
+cudaError_t launch_prog(const GemmParams& p, cudaStream_t stream) {
+  if constexpr (BN == 256) {
+    if (use_cta_pair(p)) return launch_ctas<BN, PROG, 2>(p, stream);
+  }
+  return launch_ctas<BN, PROG, 1>(p, stream);
 }
 
 }  // namespace
