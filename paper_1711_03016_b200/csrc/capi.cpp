@@ -25,6 +25,8 @@ using namespace dlvm;
 struct dlvm_fn_s {
   Function primal;
   std::optional<Function> grad;
+  Function opt_primal;           // what the plans execute (optimize_function unless DLVM_NO_OPT)
+  std::optional<Function> opt_grad;
   Plan plan[2];
   bool planned[2] = {false, false};
   std::string plan_error[2];
@@ -357,6 +359,12 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
       int nw = decl->grad->has_wrt ? (int)decl->grad->wrt.size() : src->num_args();
       h->n_grads = nw;
     }
+    h->opt_primal = h->primal;
+    if (h->grad) h->opt_grad = *h->grad;
+    if (!(o.flags & DLVM_NO_OPT)) {
+      optimize_function(h->opt_primal);
+      if (h->opt_grad) optimize_function(*h->opt_grad);
+    }
     for (int which = 0; which < 2; ++which) {
       if (which == 1 && !h->grad) continue;
       PlanOptions po;
@@ -365,7 +373,7 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
       po.specialize = (o.flags & DLVM_NO_SPECIALIZE) == 0;
       po.n_grads = which ? h->n_grads : 0;
       try {
-        h->plan[which] = make_plan(which ? *h->grad : h->primal, po);
+        h->plan[which] = make_plan(which ? *h->opt_grad : h->opt_primal, po);
         h->planned[which] = true;
       } catch (const Error& e) {
         h->plan_error[which] = e.what();
@@ -433,8 +441,15 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
         }
         break;
       }
+      case 6:
+        s = print_function(fn->opt_primal);
+        break;
+      case 7:
+        if (!fn->opt_grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        s = print_function(*fn->opt_grad);
+        break;
       default:
-        return fail(DLVM_ERR_USAGE, "which must be 0..5");
+        return fail(DLVM_ERR_USAGE, "which must be 0..7");
     }
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());

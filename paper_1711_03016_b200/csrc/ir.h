@@ -162,6 +162,9 @@ Function differentiate(const Function& src, const GradConfig& cfg, const std::st
 // verify error for cycles and unknown sources.
 Function canonical_function(const Module& m, const std::string& name);
 void dead_code_elim(Function& f);
+// create-time optimiser (opt.cpp): algebra simplification, CSE, matrix-chain
+// reordering, DCE -- value-preserving in exact arithmetic
+void optimize_function(Function& f);
 // printer.cpp
 std::string print_function(const Function& f);
 

@@ -41,6 +41,7 @@ struct TcParams {
   CUtensorMap tma_b[kMaxSeg];
   GemmParams g;
   int32_t tiles_m, tiles_n;
+  int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -87,22 +88,35 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// both CTAs of a pair load their half; the bytes complete on the leader's barrier
+// both CTAs of a pair load their half; the bytes complete on the leader's
+// barrier.  `pol`: L2 eviction policy (createpolicy) for the tile's lines.
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int32_t c0,
-                                                 int32_t c1) {
+                                                 int32_t c1, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-      "[%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
+}
+// L2 policies: keep (evict_last) the small operand every tile re-reads,
+// stream (evict_first) the large one read once, or normal
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+  uint64_t p;
+  if (hint == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (hint == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
-                                            int32_t c1) {
+                                            int32_t c1, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], "
+      "[%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
 }
 
@@ -602,6 +616,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         }
       }
       if (lane == 0) {
+        const uint64_t pol_a = l2_policy(P.hint_a), pol_b = l2_policy(P.hint_b);
         for (int q = 0; q < g.n_seg; ++q) {
           const GemmSegParams& G = g.seg[q];
           const CUtensorMap* ma = &P.tma_a[q];
@@ -618,30 +633,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
               const uint32_t lb = mapa_rank(fb, 0);
               if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_TX);
               if (G.a_kmajor) {
-                tma_load_2d_pair(a_dst, ma, lb, k0, m0);
+                tma_load_2d_pair(a_dst, ma, lb, k0, m0, pol_a);
               } else {
-                tma_load_2d_pair(a_dst, ma, lb, m0, k0);
-                tma_load_2d_pair(a_dst + 8192, ma, lb, m0 + 64, k0);
+                tma_load_2d_pair(a_dst, ma, lb, m0, k0, pol_a);
+                tma_load_2d_pair(a_dst + 8192, ma, lb, m0 + 64, k0, pol_a);
               }
               if (G.b_kmajor) {
-                tma_load_2d_pair(b_dst, mb, lb, k0, nb);
+                tma_load_2d_pair(b_dst, mb, lb, k0, nb, pol_b);
               } else {
 #pragma unroll
-                for (int c = 0; c < BNC / 64; ++c) tma_load_2d_pair(b_dst + c * 8192, mb, lb, nb + 64 * c, k0);
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d_pair(b_dst + c * 8192, mb, lb, nb + 64 * c, k0, pol_b);
               }
             } else {
               mbar_expect_tx(fb, STAGE_TX);
               if (G.a_kmajor) {
-                tma_load_2d(a_dst, ma, fb, k0, m0);
+                tma_load_2d(a_dst, ma, fb, k0, m0, pol_a);
               } else {
-                tma_load_2d(a_dst, ma, fb, m0, k0);
-                tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0);
+                tma_load_2d(a_dst, ma, fb, m0, k0, pol_a);
+                tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0, pol_a);
               }
               if (G.b_kmajor) {
-                tma_load_2d(b_dst, mb, fb, k0, nb);
+                tma_load_2d(b_dst, mb, fb, k0, nb, pol_b);
               } else {
 #pragma unroll
-                for (int c = 0; c < BNC / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, nb + 64 * c, k0);
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, nb + 64 * c, k0, pol_b);
               }
             }
             if (++s == NST) {
@@ -950,6 +965,31 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1) {
   }
   tp->tiles_m = (int)((p.M + BM * ctas - 1) / (BM * ctas));
   tp->tiles_n = (int)((p.N + BN - 1) / BN);
+  // L2 policy: when one operand is small enough to stay resident (every tile
+  // row re-reads all of it) and the other is streamed once, keep the small
+  // one and stream the big one, so the epilogue's store stream does not evict
+  // it (DLVM_GEMM_L2HINT=0 disables)
+  static const int hints_on = [] {
+    const char* e = std::getenv("DLVM_GEMM_L2HINT");
+    return e ? std::atoi(e) : 0;  // off: measured no gain (A is re-read by every N tile too)
+  }();
+  double bytes_a = 0, bytes_b = 0;
+  for (int q = 0; q < p.n_seg; ++q) {
+    bytes_a += 2.0 * p.M * p.seg[q].K;
+    bytes_b += 2.0 * p.N * p.seg[q].K;
+  }
+  const double keep_max = 48.0 * (1 << 20);
+  tp->hint_a = tp->hint_b = 0;
+  if (hints_on) {
+    const int stream = hints_on == 2 ? 2 : 0;
+    if (bytes_b <= keep_max && bytes_a >= 4 * bytes_b) {
+      tp->hint_b = 1;
+      tp->hint_a = stream;
+    } else if (bytes_a <= keep_max && bytes_b >= 4 * bytes_a) {
+      tp->hint_a = 1;
+      tp->hint_b = stream;
+    }
+  }
   return true;
 }
 

@@ -276,3 +276,77 @@ def test_linear_algebra_fusion_rnn_plan():
     ws = W.rnn(3, 6, 4, 5, "f32")
     ins = [x.astype(np.float64) for x in ws.inputs()]
     _ad_cross_check(ws.text, ws.fn, ws.grad, ins, np.float64(ws.seed()))
+
+
+def _opt_equiv(text, fn, grad, ins, seed=None, rtol=1e-11):
+    """The optimised IR the plans execute (print modes 6/7), interpreted by
+    the oracle in float64, computes what the written program computes."""
+    m = oracle.parse(text)
+    f = _plan_only(text, fn, grad)
+    om = oracle.parse('module "o"\nstage optimizable\n' + f.print(6) + ("\n" + f.print(7) if grad else ""))
+    for name, args in [(fn, list(ins))] + ([(grad, list(ins) + ([seed] if seed is not None else []))] if grad else []):
+        for a, b in zip(oracle.run(om, name, args), oracle.run(m, name, args)):
+            np.testing.assert_allclose(a, b, rtol=rtol, atol=rtol * (np.max(np.abs(b)) + 1e-300))
+    return f
+
+
+OPT_PROGRAM = """module "o"
+stage raw
+func @f: (<16 x 4 x f32>, <4 x 512 x f32>, <512 x 8 x f32>, <16 x 8 x f32>) -> f32 {
+'entry(%x: <16 x 4 x f32>, %w1: <4 x 512 x f32>, %w2: <512 x 8 x f32>, %t: <16 x 8 x f32>):
+    %u = dot %x: <16 x 4 x f32>, %w1: <4 x 512 x f32>
+    %v = dot %u: <16 x 512 x f32>, %w2: <512 x 8 x f32>
+    %p = power %v: <16 x 8 x f32>, 2: f32
+    %q = power %t: <16 x 8 x f32>, 1: f32
+    %o = power %v: <16 x 8 x f32>, 0: f32
+    %a = multiply %p: <16 x 8 x f32>, 1: f32
+    %b = add %a: <16 x 8 x f32>, 0: f32
+    %c = subtract %b: <16 x 8 x f32>, %q: <16 x 8 x f32>
+    %d = multiply %c: <16 x 8 x f32>, %o: <16 x 8 x f32>
+    %e = negate %d: <16 x 8 x f32>
+    %g = negate %e: <16 x 8 x f32>
+    %h = transpose %g: <16 x 8 x f32>
+    %k = transpose %h: <8 x 16 x f32>
+    %r0 = reduce %k: <16 x 8 x f32> by add along 1
+    %r1 = reduce %r0: <16 x f32> by add along 0
+    return %r1: f32
+}
+[gradient @f wrt 1, 2]
+func @df: (<16 x 4 x f32>, <4 x 512 x f32>, <512 x 8 x f32>, <16 x 8 x f32>) -> (<4 x 512 x f32>, <512 x 8 x f32>)
+"""
+
+
+def test_optimiser_algebra_cse_and_matrix_chain():
+    """Create-time optimiser: x^2 -> x*x, x^1 -> x, x^0 -> 1,
+    x*1, x+0, -(-x), transpose(transpose x) removed; (x.W1).W2 with a
+    512-wide middle is reassociated to x.(W1.W2) (16*4*8 + 4*512*8
+    multiply-adds instead of 16*4*512 + 16*512*8); values unchanged (f64)."""
+    rng = np.random.default_rng(5)
+    ins = [rng.normal(size=s) for s in [(16, 4), (4, 512), (512, 8), (16, 8)]]
+    f = _opt_equiv(OPT_PROGRAM, "f", "df", ins)
+    o = f.print(6)
+    assert " power " not in o and " negate " not in o and " transpose " not in o, o
+    assert "dot %w1: <4 x 512 x f32>, %w2: <512 x 8 x f32>" in o, o
+    assert o.count(" = dot ") == 2
+    assert "unsupported" not in f.print(3)
+    # the written program is planned unchanged with DLVM_NO_OPT
+    g = P.Function(OPT_PROGRAM, "f", "df", flags=P.DLVM_PLAN_ONLY | P.DLVM_NO_OPT)
+    assert " power " in g.print(6) and g.print(6) == g.print(0)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_optimiser_preserves_random_programs(seed):
+    rng = np.random.default_rng(1000 + seed)
+    text, args = _rand_program(rng)
+    ins = [rng.uniform(-1, 1, s) for _, s in args]
+    _opt_equiv(text, "f", "g", ins)
+
+
+def test_optimiser_configs_and_higher_order():
+    for w, prec in CONFIGS[:3]:
+        ins = [x.astype(np.float64) for x in w.inputs()]
+        seed = None if w.seed() is None else np.asarray(w.seed(), dtype=np.float64)
+        _opt_equiv(w.text, w.fn, w.grad, ins, seed)
+    hv = W.mlp_hvp(8, 4, 6, 3)
+    ins = [x.astype(np.float64) for x in hv.inputs()]
+    _opt_equiv(hv.text, hv.fn, hv.grad, ins, hv.seed().astype(np.float64))

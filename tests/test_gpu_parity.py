@@ -456,3 +456,20 @@ def test_rnn_multi_segment_gemm_bf16():
     ref = oracle.run(m, w.grad, ins64 + [np.float64(w.seed())], dot_policy="bf16")
     for k, (g, r) in enumerate(zip(res["grad"], ref)):
         assert_normwise(g, r, 2e-2, what=f"rnn grad out{k}")
+
+
+def test_optimised_program_parity_f32():
+    """The create-time optimiser's output (algebra simplification, CSE,
+    matrix-chain reordering) on the GPU against the oracle run on the
+    program as written; bounds from the optimised IR's own terms (the
+    reassociated chain sums different products)."""
+    from test_capi_cpu import OPT_PROGRAM
+    rng = np.random.default_rng(41)
+    ins = [(rng.normal(size=s) * 0.5).astype(np.float32) for s in [(16, 4), (4, 512), (512, 8), (16, 8)]]
+    res = gpu_run(OPT_PROGRAM, "f", "df", ins)
+    ins64 = [x.astype(np.float64) for x in ins]
+    m = oracle.parse(OPT_PROGRAM)
+    om = oracle.parse('module "o"\nstage optimizable\n' + res["fn"].print(6) + "\n" + res["fn"].print(7))
+    assert_f32_parity(res["primal"][0], oracle.run(m, "f", ins64)[0], term_bound(om, "f", ins64)[0], what="opt f")
+    for k, (g, r, b) in enumerate(zip(res["grad"], oracle.run(m, "df", ins64), term_bound(om, "df", ins64))):
+        assert_f32_parity(g, r, b, what=f"opt df out{k}")
