@@ -21,6 +21,7 @@
 #include <type_traits>
 
 #include "ew_spec.cuh"
+#include "launch.cuh"
 #include "spec_registry.h"
 
 namespace dlvm {
@@ -44,6 +45,8 @@ __host__ __device__ constexpr int num_red_slots() {
 
 template <int VEC, class P>
 __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr bool SPEC = !std::is_void_v<P>;
   using T = std::conditional_t<SPEC, spec::Traits<std::conditional_t<SPEC, P, spec::Prog<0, 0, spec::St<>, spec::Rd<>>>>, VmTraits>;
   constexpr int NS = T::kSlots;
@@ -252,6 +255,8 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
 // in a fixed order (threadIdx.y strides the chunks, then a fixed-order sum
 // over threadIdx.y), written to every home of the reduced value.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EwParams p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float part[256];
   const int ex = blockDim.x, cy = blockDim.y;
   const int64_t e = (int64_t)blockIdx.x * ex + threadIdx.x;
@@ -290,6 +295,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
 // RPI rows loaded before they are computed.  Same arithmetic as ew_kernel.
 template <int VEC, class P>
 __global__ void __launch_bounds__(256, 3) ew2d_kernel(const __grid_constant__ EwParams p) {
+  pdl_trigger();
+  pdl_wait();
   using T = spec::Traits<P>;
   constexpr int NS = T::kSlots, NI = T::kIn > 0 ? T::kIn : 1;
   constexpr int NR = T::Reds::n > 0 ? T::Reds::n : 1;
@@ -402,6 +409,8 @@ constexpr bool has_row_red() {
 }
 
 __global__ void cast_bf16_kernel(const float* __restrict__ src, unsigned short* __restrict__ dst, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
   for (; i + 3 < n; i += stride) {
@@ -419,12 +428,14 @@ cudaError_t launch_spec_ew(const EwParams& p, int bx, int by, cudaStream_t strea
   dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
   if constexpr (!has_row_red<P>()) {
     if (p.ndims == 2 && p.ncols == 1) {
-      ew2d_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
-      return cudaGetLastError();
+      LaunchCfg L(grid, block, 0, stream);
+      cudaError_t e = cudaLaunchKernelEx(&L.cfg, ew2d_kernel<VEC, P>, p);
+      return e != cudaSuccess ? e : cudaGetLastError();
     }
   }
-  ew_kernel<VEC, P><<<grid, block, 0, stream>>>(p);
-  return cudaGetLastError();
+  LaunchCfg L(grid, block, 0, stream);
+  cudaError_t e = cudaLaunchKernelEx(&L.cfg, ew_kernel<VEC, P>, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
@@ -457,23 +468,25 @@ int num_ew_specs() {
 
 cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream) {
   dim3 grid((unsigned)p.gx, (unsigned)p.gy), block(bx, by);
-  if (p.vec == 4)
-    ew_kernel<4, void><<<grid, block, 0, stream>>>(p);
-  else
-    ew_kernel<1, void><<<grid, block, 0, stream>>>(p);
-  return cudaGetLastError();
+  LaunchCfg L(grid, block, 0, stream);
+  cudaError_t e = p.vec == 4 ? cudaLaunchKernelEx(&L.cfg, ew_kernel<4, void>, p)
+                             : cudaLaunchKernelEx(&L.cfg, ew_kernel<1, void>, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream) {
   const int64_t n = p.dims[0];
   dim3 block = n >= 32 ? dim3(32, 8) : dim3(1, 256);
   dim3 grid((unsigned)((n + block.x - 1) / block.x));
-  finalize_kernel<<<grid, block, 0, stream>>>(p);
-  return cudaGetLastError();
+  LaunchCfg L(grid, block, 0, stream);
+  cudaError_t e = cudaLaunchKernelEx(&L.cfg, finalize_kernel, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 __global__ void pack_bf16_kernel(const void* __restrict__ src, int src_f32, int64_t rows, int64_t cols,
                                  unsigned short* __restrict__ dst, int64_t ld) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
   if (r >= rows) return;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ld; c += (int64_t)gridDim.x * blockDim.x) {
@@ -488,15 +501,17 @@ __global__ void pack_bf16_kernel(const void* __restrict__ src, int src_f32, int6
 cudaError_t launch_pack_bf16(const void* src, bool src_f32, int64_t rows, int64_t cols, void* dst, int64_t ld,
                              cudaStream_t stream) {
   dim3 block(128, 4), grid((unsigned)std::min<int64_t>((ld + 127) / 128, 8), (unsigned)((rows + 3) / 4));
-  pack_bf16_kernel<<<grid, block, 0, stream>>>(src, src_f32 ? 1 : 0, rows, cols,
-                                               reinterpret_cast<unsigned short*>(dst), ld);
-  return cudaGetLastError();
+  LaunchCfg L(grid, block, 0, stream);
+  cudaError_t e = cudaLaunchKernelEx(&L.cfg, pack_bf16_kernel, src, src_f32 ? 1 : 0, rows, cols,
+                                     reinterpret_cast<unsigned short*>(dst), ld);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream) {
   int64_t blocks = std::min<int64_t>((n / 4 + 255) / 256 + 1, 148 * 16);
-  cast_bf16_kernel<<<(unsigned)blocks, 256, 0, stream>>>(src, reinterpret_cast<unsigned short*>(dst), n);
-  return cudaGetLastError();
+  LaunchCfg L(dim3((unsigned)blocks), dim3(256), 0, stream);
+  cudaError_t e = cudaLaunchKernelEx(&L.cfg, cast_bf16_kernel, src, reinterpret_cast<unsigned short*>(dst), n);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace dlvm

@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "ew_spec.cuh"
+#include "launch.cuh"
 #include "spec_registry.h"
 
 namespace dlvm {
@@ -152,6 +153,8 @@ constexpr int KB = BK;
 
 template <bool BF16, int BM, class PROG>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const __grid_constant__ GemmParams p, int64_t kchunk) {
+  pdl_trigger();
+  pdl_wait();
   using S = EpiShape<PROG>;
   constexpr int TM = BM / 16;
   constexpr int NA = BM * KB / 256, NB = KB * BN / 256;
@@ -352,19 +355,8 @@ cudaError_t launch_bm(const GemmParams& p, cudaStream_t stream) {
   int64_t kchunk = ((K + ks - 1) / ks + BK - 1) / BK * BK;
   if (kchunk <= 0) kchunk = BK;
   ks = K > 0 ? (K + kchunk - 1) / kchunk : 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)ks);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = (unsigned)ks;
-  cfg.attrs = attr;
-  cfg.numAttrs = ks > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_simt_kernel<BF16, BM, PROG>, p, kchunk);
+  LaunchCfg L(dim3((unsigned)gx, (unsigned)gy, (unsigned)ks), dim3(256, 1, 1), 0, stream, 1, (unsigned)ks);
+  return cudaLaunchKernelEx(&L.cfg, gemm_simt_kernel<BF16, BM, PROG>, p, kchunk);
 }
 
 template <int BM, class PROG>

@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "ew_spec.cuh"
+#include "launch.cuh"
 #include "spec_registry.h"
 
 namespace dlvm {
@@ -598,6 +599,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   if constexpr (CTAS == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // prologue done: let the next kernel start its own, then wait for the
+  // previous kernel's results (PDL, launch.cuh)
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
     int s = 0;
@@ -1016,19 +1021,8 @@ cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
   if (!make_params(p, &tp, CTAS)) return cudaErrorInvalidValue;
   const int tiles = tp.tiles_m * tp.tiles_n;
   const int grid = CTAS * std::min(tiles, num_sms() / CTAS);  // persistent: one CTA (pair) per SM (pair)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid, 1, 1);
-  cfg.blockDim = dim3(NUM_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CTAS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = CTAS > 1 ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tp);
+  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), SMEM, stream, CTAS, 1);
+  cudaError_t e = cudaLaunchKernelEx(&L.cfg, kern, tp);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
