@@ -34,7 +34,7 @@ def gpu_run(text: str, fn: str, grad: Optional[str], inputs: Sequence[np.ndarray
     dev = torch.device("cuda:0")
     ins = []
     for i, x in enumerate(inputs):
-        t = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        t = torch.from_numpy(np.array(x, copy=True)).to(dev)  # keeps 0-d arrays 0-d (ascontiguousarray does not)
         if i in bf16_inputs:
             t = t.to(torch.bfloat16)
         ins.append(t)

@@ -350,3 +350,22 @@ def test_optimiser_configs_and_higher_order():
     hv = W.mlp_hvp(8, 4, 6, 3)
     ins = [x.astype(np.float64) for x in hv.inputs()]
     _opt_equiv(hv.text, hv.fn, hv.grad, ins, hv.seed().astype(np.float64))
+
+
+def test_adjoint_ir_structure_filecheck():
+    """FileCheck-style checks (SURVEY §4 T6, P:L92/L340 lit+FileCheck) of the
+    generated adjoint IR, written from the adjoint rules: Fig. 4's dg uses
+    dot(transpose(x), dZ) for dW, a column reduce for db, the tanh adjoint
+    1 - y*y, keeps g's result last; DCE removed the unused dX."""
+    f = _plan_only(W.fig4_ir(), "g", "dg")
+    g = f.print(1)
+    lines = [l.strip() for l in g.splitlines()]
+    order = ["= tanh %1", "multiply %2: <4 x 5 x f32>, %2", "subtract 1: f32", "reduce", "by add along 0",
+             "shapeCast", "to 1 x 5", "transpose %x", "dot %d", "return (%d"]
+    pos = 0
+    for pat in order:  # CHECK: in order
+        while pos < len(lines) and pat not in lines[pos]:
+            pos += 1
+        assert pos < len(lines), f"CHECK not found in order: {pat}\n{g}"
+    assert "transpose %w" not in g  # CHECK-NOT: dX (x is not in wrt)
+    assert lines[-2].endswith("%2: <4 x 5 x f32>)")  # kept g result last (A7)

@@ -473,3 +473,38 @@ def test_optimised_program_parity_f32():
     assert_f32_parity(res["primal"][0], oracle.run(m, "f", ins64)[0], term_bound(om, "f", ins64)[0], what="opt f")
     for k, (g, r, b) in enumerate(zip(res["grad"], oracle.run(m, "df", ins64), term_bound(om, "df", ins64))):
         assert_f32_parity(g, r, b, what=f"opt df out{k}")
+
+
+@pytest.mark.parametrize("case", ["c1", "c3s", "fig4", "rnn"])
+def test_cross_ad_oracle_adjoint_ir_on_gpu(case):
+    """SURVEY §4 T6 cross-AD check: the ORACLE's adjoint IR (oracle/adjoint.py,
+    generated independently of the C++ AD, no DCE) executed as a plain
+    function by the GPU library equals the oracle's value-level gradient."""
+    import paper_1711_03016_b200 as P
+    if case == "c1":
+        w, prec = W.c1(), "f32"
+        ins = w.inputs() + [np.float32(w.seed())]
+        name, text = w.grad, w.text
+    elif case == "c3s":
+        w, prec = W.c3(64, layers=[(96, 80, "relu"), (80, 40, None)]), "f32"
+        ins = w.inputs() + [np.float32(w.seed())]
+        name, text = w.grad, w.text
+    elif case == "rnn":
+        w, prec = W.rnn(3, 24, 16, 20, "f32"), "f32"
+        ins = w.inputs() + [np.float32(w.seed())]
+        name, text = w.grad, w.text
+    else:
+        text, name, prec = W.fig4_ir(8, 12, 6), "dg", "f32"
+        m0 = oracle.parse(text)
+        rng = np.random.default_rng(2)
+        ins = [rng.uniform(-1, 1, t.shape).astype(np.float32) for t in m0.functions["g"].param_types]
+    m = oracle.parse(text)
+    gtext = 'module "x"\nstage optimizable\n' + oracle.adjoint_text(
+        m.functions[m.functions[name].gradient.source], m.functions[name].gradient, name)
+    ins = [np.asarray(x, dtype=np.float32) for x in ins]
+    res = gpu_run(gtext, name, None, ins, dot_precision=prec, which="primal")
+    ins64 = [x.astype(np.float64) for x in ins]
+    ref = oracle.run(m, name, ins64)
+    bounds = term_bound(oracle.parse(gtext), name, ins64)
+    for k, (g, r, b) in enumerate(zip(res["primal"], ref, bounds)):
+        assert_f32_parity(g, r, b, what=f"{case} oracle-IR out{k}")
