@@ -71,11 +71,13 @@ typedef struct {
 #define DLVM_NO_SPECIALIZE 0x4u  /* always use the generic element-wise program interpreter */
 #define DLVM_NO_OPT 0x8u         /* skip the create-time IR optimiser (algebra simplification, CSE,
                                     matrix-chain reordering; §3.1.2) */
+#define DLVM_NO_JIT 0x10u        /* no create-time NVRTC specialisation of element-wise programs that
+                                    are not in the ahead-of-time registry (they are interpreted) */
 
 typedef struct {
   int32_t dot_precision; /* DLVM_DOT_F32 | DLVM_DOT_BF16 */
   int32_t device;        /* CUDA device ordinal the handle launches on */
-  uint32_t flags;        /* DLVM_PLAN_ONLY | DLVM_NO_FUSION | DLVM_NO_SPECIALIZE | DLVM_NO_OPT */
+  uint32_t flags;        /* DLVM_PLAN_ONLY | DLVM_NO_FUSION | DLVM_NO_SPECIALIZE | DLVM_NO_OPT | DLVM_NO_JIT */
 } dlvm_options;
 
 typedef struct dlvm_fn_s* dlvm_fn;
@@ -109,8 +111,10 @@ dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_
  * dead-code elimination (which=1) in the .dl syntax of Fig. 3, the launch
  * plan of the primal (2) / gradient (3), the element-wise program
  * signatures of the primal (4) / gradient (5) launches (one per line, the
- * keys of the compile-time specialisations), or the optimised primal (6) /
- * gradient (7) that the plans execute (identical to 0/1 with DLVM_NO_OPT).  Writes at most `cap` bytes
+ * keys of the compile-time specialisations), the optimised primal (6) /
+ * gradient (7) that the plans execute (identical to 0/1 with DLVM_NO_OPT),
+ * or (8) the kernels specialised at create time by NVRTC (one line each:
+ * plan, step, status, instantiation).  Writes at most `cap` bytes
  * including the NUL; *needed receives the full size including the NUL. */
 dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);
 

@@ -4,8 +4,8 @@ by fused element-wise kernels and tcgen05 GEMMs through a C ABI
 (include/dlvm.h).  `Function` is the Python binding; `dp` holds the
 data-parallel driver (one NCCL all-reduce of parameter gradients)."""
 
-from .dlvm import (DLVM_BF16, DLVM_BOOL, DLVM_F32, DLVM_GRADIENT, DLVM_NO_FUSION, DLVM_NO_OPT, DLVM_NO_SPECIALIZE,
+from .dlvm import (DLVM_BF16, DLVM_BOOL, DLVM_F32, DLVM_GRADIENT, DLVM_NO_FUSION, DLVM_NO_JIT, DLVM_NO_OPT, DLVM_NO_SPECIALIZE,
                    DLVM_PLAN_ONLY, DLVM_PRIMAL, DlvmError, Function, dlvm_version, lib)
 
 __all__ = ["Function", "DlvmError", "lib", "dlvm_version", "DLVM_PLAN_ONLY", "DLVM_NO_FUSION",
-           "DLVM_NO_SPECIALIZE", "DLVM_NO_OPT", "DLVM_PRIMAL", "DLVM_GRADIENT", "DLVM_F32", "DLVM_BF16", "DLVM_BOOL"]
+           "DLVM_NO_SPECIALIZE", "DLVM_NO_OPT", "DLVM_NO_JIT", "DLVM_PRIMAL", "DLVM_GRADIENT", "DLVM_F32", "DLVM_BF16", "DLVM_BOOL"]

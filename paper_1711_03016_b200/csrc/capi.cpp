@@ -12,10 +12,12 @@
 #include <cstring>
 #include <new>
 #include <optional>
+#include <sstream>
 #include <string>
 
 #include "../../include/dlvm.h"
 #include "ir.h"
+#include "jit.h"
 #include "kernels/kernels.h"
 #include "kernels/spec_registry.h"
 #include "plan.h"
@@ -34,6 +36,8 @@ struct dlvm_fn_s {
   int n_grads = 0;
   std::vector<void*> launch_events[2];
   bool specialize = true;
+  std::vector<void*> jit_fn[2];  // per plan step: create-time specialised kernel (CUfunction) or null
+  std::string jit_report;        // print mode 8
 };
 
 namespace {
@@ -199,7 +203,10 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     if (lev.empty() || !lev[i]) return cudaSuccess;
     return cudaEventRecord(static_cast<cudaEvent_t>(lev[i]), stream);
   };
-  for (const Step& st : P.steps) {
+  const std::vector<void*>& jit = fn->jit_fn[which];
+  for (size_t si = 0; si < P.steps.size(); ++si) {
+    const Step& st = P.steps[si];
+    void* const jf = si < jit.size() ? jit[si] : nullptr;
     cudaError_t e = cudaSuccess;
     if (st.kind == Step::EW && st.ew.finalize && st.ew.direct_buf >= 0 && b.st[st.ew.direct_buf] == (uint8_t)SType::F32)
       continue;  // the producer wrote the single partial into the f32 home
@@ -212,7 +219,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         e = launch_finalize(p, stream);
       } else {
         EwLaunchFn sf = fn->specialize ? find_ew_spec(st.ew.sig.c_str(), st.ew.vec) : nullptr;
-        e = sf ? sf(p, st.ew.bx, st.ew.by, stream) : launch_ew(p, st.ew.bx, st.ew.by, stream);
+        e = jf ? launch_ew_fn(jf, p, st.ew.bx, st.ew.by, stream)
+               : sf ? sf(p, st.ew.bx, st.ew.by, stream) : launch_ew(p, st.ew.bx, st.ew.by, stream);
       }
     } else if (st.kind == Step::GEMM) {
       const GemmStep& g = st.gemm;
@@ -257,12 +265,13 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       }
       if (g.tensor_core && aligned && gp.bf16) {
         GemmLaunchFn sf = fn->specialize ? find_gemm_spec(g.epi.sig.c_str(), g.bn) : nullptr;
-        e = sf ? sf(gp, stream) : launch_gemm_tc(gp, stream);
+        e = jf ? launch_gemm_tc_fn(jf, gemm_tc_ctas(gp.M, gp.bn), gp, stream) : sf ? sf(gp, stream) : launch_gemm_tc(gp, stream);
       }
       else {
         if (g.tensor_core) return fail(DLVM_ERR_RUNTIME, "tensor-core dot operand misaligned");
         GemmLaunchFn sf = fn->specialize ? find_simt_spec(g.epi.sig.c_str(), g.bm) : nullptr;
-        e = sf ? sf(gp, stream) : launch_gemm_simt(gp, stream);
+        e = jf && gp.bf16 == (g.seg[0].a.st == SType::BF16) ? launch_gemm_simt_fn(jf, gp, stream)
+            : sf ? sf(gp, stream) : launch_gemm_simt(gp, stream);
       }
     } else if (st.kind == Step::CAST) {
       const dlvm_tensor& src = param(st.cast.input);
@@ -312,6 +321,58 @@ double step_bytes(const Plan& P, const Step& st) {
     }
   }
   return b;
+}
+
+// Create-time specialisation (jit.h): every EW / GEMM step whose program is
+// not in the ahead-of-time registry is compiled by NVRTC with the program as
+// C++ types -- the same template the registry instantiates.  A failure
+// leaves the step on the interpreter and is listed by print mode 8.
+bool force_jit() {  // DLVM_FORCE_JIT=1: ignore the ahead-of-time registry (testing the JIT path)
+  static const bool on = [] {
+    const char* e = std::getenv("DLVM_FORCE_JIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+void jit_specialise(dlvm_fn h) {
+  std::vector<JitRequest> reqs;
+  std::vector<std::pair<int, size_t>> where;
+  for (int w = 0; w < 2; ++w) {
+    if (!h->planned[w]) continue;
+    const Plan& P = h->plan[w];
+    h->jit_fn[w].assign(P.steps.size(), nullptr);
+    const bool bf = h->opts.dot_precision == DLVM_DOT_BF16;
+    for (size_t si = 0; si < P.steps.size(); ++si) {
+      const Step& st = P.steps[si];
+      std::string expr;
+      if (st.kind == Step::EW && !st.ew.finalize && (force_jit() || !find_ew_spec(st.ew.sig.c_str(), st.ew.vec))) {
+        bool row_red = false;
+        for (int q = 0; q < st.ew.prog.n_reduces; ++q) row_red |= st.ew.prog.reduce_kind[q] == RED_ROW;
+        const bool two_d = st.ew.ndims == 2 && st.ew.ncols == 1 && !row_red;
+        expr = std::string("&dlvm::kern::") + (two_d ? "ew2d_kernel<" : "ew_kernel<") + std::to_string(st.ew.vec) +
+               ", " + jit_prog_type(st.ew.sig) + ">";
+      } else if (st.kind == Step::GEMM && st.gemm.tensor_core && (force_jit() || !find_gemm_spec(st.gemm.epi.sig.c_str(), st.gemm.bn))) {
+        expr = "&dlvm::kern::gemm_tc_kernel<" + std::to_string(st.gemm.bn) + ", " + jit_prog_type(st.gemm.epi.sig) +
+               ", " + std::to_string(gemm_tc_ctas(st.gemm.M, st.gemm.bn)) + ">";
+      } else if (st.kind == Step::GEMM && !st.gemm.tensor_core && (force_jit() || !find_simt_spec(st.gemm.epi.sig.c_str(), st.gemm.bm))) {
+        expr = std::string("&dlvm::kern::simt::gemm_simt_kernel<") + (bf ? "true" : "false") + ", " +
+               std::to_string(st.gemm.bm) + ", " + jit_prog_type(st.gemm.epi.sig) + ">";
+      }
+      if (expr.empty()) continue;
+      reqs.push_back(JitRequest{expr});
+      where.emplace_back(w, si);
+    }
+  }
+  jit_build(reqs);
+  std::ostringstream rep;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    h->jit_fn[where[i].first][where[i].second] = reqs[i].function;
+    rep << (where[i].first ? "grad" : "primal") << " step " << where[i].second << ": "
+        << (reqs[i].function ? "specialised " : "interpreted (" + reqs[i].error.substr(0, 200) + ") ") << reqs[i].expr
+        << "\n";
+  }
+  h->jit_report = rep.str();
 }
 
 }  // namespace
@@ -384,6 +445,7 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
         }
       }
     }
+    if (!(o.flags & (DLVM_PLAN_ONLY | DLVM_NO_SPECIALIZE | DLVM_NO_JIT)) && jit_available()) jit_specialise(h);
     *out = h;
     return DLVM_OK;
   } catch (const Error& e) {
@@ -448,8 +510,11 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
         if (!fn->opt_grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
         s = print_function(*fn->opt_grad);
         break;
+      case 8:
+        s = fn->jit_report;
+        break;
       default:
-        return fail(DLVM_ERR_USAGE, "which must be 0..7");
+        return fail(DLVM_ERR_USAGE, "which must be 0..8");
     }
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());

@@ -14,7 +14,7 @@
 // run is bit-reproducible; reading A14).
 #pragma once
 
-#include <cstdint>
+#include "rtc_compat.h"
 
 namespace dlvm {
 

@@ -1,6 +1,8 @@
 // tcgen05 GEMM entry points (kernel template in gemm_tc.cuh): the generic
 // instantiation whose epilogue interprets the planner's program, and the
 // lookup of compile-time epilogue specialisations (gemm_tc_spec*.cu).
+#include <cstring>
+
 #include "gemm_tc.cuh"
 
 namespace dlvm {
@@ -23,6 +25,25 @@ cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream) {
   if (cw == 16) return launch_prog<128, VmEpi<16>>(p, stream);
   if (cw == 8) return launch_prog<128, VmEpi<8>>(p, stream);
   return launch_prog<128, VmEpi<4>>(p, stream);
+}
+
+int gemm_tc_ctas(int64_t M, int bn) {
+  GemmParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.M = M;
+  p.bn = bn;
+  return use_cta_pair(p) ? 2 : 1;
+}
+
+cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStream_t stream) {
+  TcParams tp;
+  if (!make_params(p, &tp, ctas)) return cudaErrorInvalidValue;
+  const int smem = ctas == 2 ? smem_bytes<256, 2>() : (p.bn == 256 ? smem_bytes<256, 1>() : smem_bytes<128, 1>());
+  const int tiles = tp.tiles_m * tp.tiles_n;
+  const int grid = ctas * std::min(tiles, num_sms() / ctas);
+  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), smem, stream, (unsigned)ctas, 1);
+  void* args[] = {&tp};
+  return launch_jit(fn, L, args);
 }
 
 GemmLaunchFn find_gemm_spec(const char* sig, int bn) {

@@ -1,0 +1,879 @@
+#pragma once
+// tcgen05 tensor-core GEMM for `dot` under the bf16 policy (K5 of SURVEY.md
+// §2.5; Table 1 "dot"; reading A15: bf16 operands, fp32 accumulation).
+//
+// C[M,N] = A[M,K] . B[K,N], bf16 operands read by TMA (cp.async.bulk.tensor,
+// 128-byte swizzle) into a 4-stage shared-memory ring guarded by mbarriers;
+// one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
+// N=BN, K=16) accumulating in TMEM (two BN-column accumulators so the
+// epilogue of tile i overlaps the main loop of tile i+1); four epilogue warps
+// read TMEM with tcgen05.ld.32x32b and run the fused element-wise epilogue
+// program (bias, activation, activation derivative, column/row/full partial
+// sums) before storing -- "linear algebra fusion" of P:L231-236 done on the
+// accumulator tile.  `transpose` of an operand is absorbed into the UMMA
+// descriptor major bit (A K- or M-major, B K- or N-major), so the adjoint
+// dots dY.W^T and X^T.dY read W and X in place.
+//
+// Warp roles (256 threads, persistent over tiles, 1 CTA/SM):
+//   warp 0: TMA producer   warp 1: MMA issuer   warp 2: TMEM allocator
+//   warps 4-11: epilogue (TMEM lanes 32*(warp%4) .. +31 = tile rows; two
+//               warps per lane quarter split the tile's column chunks)
+// Device code only: compiled ahead of time (gemm_tc*.cu) and, for epilogue
+// programs outside the registry, at create time by NVRTC (csrc/jit.cpp).
+#ifdef __CUDACC_RTC__
+// the kernel only passes the descriptor's address to TMA
+struct alignas(64) CUtensorMap_st {
+  unsigned long long opaque[16];
+};
+typedef CUtensorMap_st CUtensorMap;
+#else
+#include <cuda.h>
+#endif
+
+#include "ew_kernels.cuh"
+
+namespace dlvm {
+namespace kern {
+
+constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 384;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+
+struct TcParams {
+  CUtensorMap tma_a[kMaxSeg];  // per K segment (sums of products share one accumulator)
+  CUtensorMap tma_b[kMaxSeg];
+  GemmParams g;
+  int32_t tiles_m, tiles_n;
+  int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
+};
+
+// CTA-pair (cta_group::2) primitives: a shared::cluster address of the same
+// offset in CTA `rank` of the cluster, remote arrive, cluster barrier
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// relaxed: it only has to follow this warp's completed TMEM reads (wait::ld +
+// fence::before_thread_sync), not its global stores; a release arrive
+// compiles to MEMBAR.ALL.GPU and stalls the epilogue on its own stores
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// both CTAs of a pair load their half; the bytes complete on the leader's
+// barrier.  `pol`: L2 eviction policy (createpolicy) for the tile's lines.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int32_t c0,
+                                                 int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+// L2 policies: keep (evict_last) the small operand every tile re-reads,
+// stream (evict_first) the large one read once, or normal
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+  uint64_t p;
+  if (hint == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (hint == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
+                                            int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], "
+      "[%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor for kind::f16: bf16 x bf16 -> f32, M=m (128, or 256
+// for a CTA pair), N=n
+__host__ __device__ constexpr uint32_t umma_idesc(int n, bool a_mn, bool b_mn, int m = BM) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A format bf16
+         | (1u << 10)                    // B format bf16
+         | ((a_mn ? 1u : 0u) << 15)      // A major (0 = K)
+         | ((b_mn ? 1u : 0u) << 16)      // B major (0 = K)
+         | ((uint32_t)(n >> 3) << 17)    // N >> 3
+         | ((uint32_t)(m >> 4) << 24);   // M >> 4
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+// CTA pair: issued by the leader; one MMA spans both CTAs' smem and TMEM
+__device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// RV consecutive rows m0.. of column n of an epilogue operand: one storage-
+// type branch and one 64-bit offset per batch; rows >= nrow are skipped.
+template <int RV>
+__device__ __forceinline__ void epi_load(const EwDevIn& in, int64_t m0, int64_t n, int nrow, float* v) {
+  const int64_t base = m0 * in.s[0] + n * in.s[1];
+  const int64_t rs = in.s[0];
+  if (in.st == (uint8_t)SType::F32) {
+    const float* p = reinterpret_cast<const float*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = j < nrow ? __ldg(p + j * rs) : 0.f;
+  } else if (in.st == (uint8_t)SType::BF16) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = j < nrow ? __uint_as_float(((unsigned)__ldg(p + j * rs)) << 16) : 0.f;
+  } else {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) v[j] = (j < nrow && __ldg(p + j * rs)) ? 1.f : 0.f;
+  }
+}
+
+template <int RV>
+__device__ __forceinline__ void epi_store(const EwDevOut& o, int64_t m0, int64_t n, int nrow, const float* v) {
+  const int64_t base = m0 * o.s[0] + n * o.s[1];
+  const int64_t rs = o.s[0];
+  if (o.st == (uint8_t)SType::F32) {
+    float* p = reinterpret_cast<float*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = v[j];
+  } else if (o.st == (uint8_t)SType::BF16) {
+    unsigned short* p = reinterpret_cast<unsigned short*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = f2bf(v[j]);
+  } else {
+    unsigned char* p = reinterpret_cast<unsigned char*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) p[j * rs] = v[j] != 0.f ? 1 : 0;
+  }
+}
+
+
+template <int CW>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+  if constexpr (CW == 16) {
+    tmem_ld16(taddr, v);
+  } else if constexpr (CW == 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+  }
+}
+
+// CW consecutive columns n0.. of row m of an epilogue operand.  `full`: the
+// whole segment is in bounds and 16-byte vector accesses are legal.
+template <int CW>
+__device__ __forceinline__ void epi_row_load(const EwDevIn& in, int64_t m, int64_t n0, int ncol, bool full,
+                                             float* v) {
+  const int64_t off = m * in.s[0] + n0 * in.s[1];
+  if (in.s[1] == 0) {  // constant along the row (column vector / scalar)
+    const float x = ncol > 0 ? ld1(in.ptr, off, in.st) : 0.f;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) v[j] = x;
+    return;
+  }
+  if (full && in.s[1] == 1) {
+    if (in.st == (uint8_t)SType::F32) {
+      const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(in.ptr) + off);
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k) {
+        const float4 x = __ldg(p + k);
+        v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+      }
+      return;
+    }
+    if (in.st == (uint8_t)SType::BF16) {
+      unsigned w[CW / 2];
+      const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + off;
+      if constexpr (CW >= 8) {
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k) {
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+          w[4 * k] = x.x; w[4 * k + 1] = x.y; w[4 * k + 2] = x.z; w[4 * k + 3] = x.w;
+        }
+      } else {
+        const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = x.x; w[1] = x.y;
+      }
+#pragma unroll
+      for (int k = 0; k < CW / 2; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+      }
+      return;
+    }
+    unsigned w[CW / 4];
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + off;
+    if constexpr (CW == 16) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    } else if constexpr (CW == 8) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = x.x; w[1] = x.y;
+    } else {
+      w[0] = __ldg(reinterpret_cast<const unsigned*>(p));
+    }
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) {
+      v[4 * k] = (w[k] & 0xffu) ? 1.f : 0.f;
+      v[4 * k + 1] = (w[k] & 0xff00u) ? 1.f : 0.f;
+      v[4 * k + 2] = (w[k] & 0xff0000u) ? 1.f : 0.f;
+      v[4 * k + 3] = (w[k] & 0xff000000u) ? 1.f : 0.f;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < CW; ++j) v[j] = j < ncol ? ld1(in.ptr, off + j * in.s[1], in.st) : 0.f;
+}
+
+template <int CW>
+__device__ __forceinline__ void epi_row_store(const EwDevOut& o, int64_t m, int64_t n0, int ncol, bool full,
+                                              const float* v) {
+  const int64_t off = m * o.s[0] + n0 * o.s[1];
+  if (full && o.s[1] == 1) {  // widest aligned stores of the row segment
+    if (o.st == (uint8_t)SType::F32) {
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k) st4(o.ptr, off + 4 * k, o.st, v + 4 * k);
+    } else if (o.st == (uint8_t)SType::BF16) {
+      unsigned w[CW / 2];
+#pragma unroll
+      for (int k = 0; k < CW / 2; ++k) w[k] = (unsigned)f2bf(v[2 * k]) | ((unsigned)f2bf(v[2 * k + 1]) << 16);
+      unsigned short* p = reinterpret_cast<unsigned short*>(o.ptr) + off;
+      if constexpr (CW >= 8) {
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k)
+          *reinterpret_cast<uint4*>(p + 8 * k) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+      } else {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+      }
+    } else {
+      unsigned w[CW / 4];
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k)
+        w[k] = (v[4 * k] != 0.f ? 1u : 0u) | (v[4 * k + 1] != 0.f ? 0x100u : 0u) |
+               (v[4 * k + 2] != 0.f ? 0x10000u : 0u) | (v[4 * k + 3] != 0.f ? 0x1000000u : 0u);
+      unsigned char* p = reinterpret_cast<unsigned char*>(o.ptr) + off;
+      if constexpr (CW == 16) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else if constexpr (CW == 8) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+      } else {
+        *reinterpret_cast<unsigned*>(p) = w[0];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < CW; ++j)
+    if (j < ncol) st1(o.ptr, off + j * o.s[1], o.st, v[j]);
+}
+
+
+// Raw 16-byte words of a row segment (prefetched one chunk ahead, decoded
+// when the chunk is computed).  Sized for f32 (CW/4 uint4).
+template <int CW>
+struct RawSeg {
+  uint4 w[CW / 4];
+};
+
+// an operand whose CW-column row segment is one contiguous vector access
+__device__ __forceinline__ bool seg_vector(const EwDevIn& in) { return in.s[1] == 1 && in.s[0] != 0; }
+
+template <int CW>
+__device__ __forceinline__ void epi_row_fetch(const EwDevIn& in, int64_t m, int64_t n0, RawSeg<CW>& r) {
+  const int64_t off = m * in.s[0] + n0;
+  if (in.st == (uint8_t)SType::F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(in.ptr) + off);
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) r.w[k] = __ldg(p + k);
+  } else if (in.st == (uint8_t)SType::BF16) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(in.ptr) + off;
+    if constexpr (CW >= 8) {
+#pragma unroll
+      for (int k = 0; k < CW / 8; ++k) r.w[k] = __ldg(reinterpret_cast<const uint4*>(p + 8 * k));
+    } else {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      r.w[0] = make_uint4(x.x, x.y, 0, 0);
+    }
+  } else {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(in.ptr) + off;
+    if constexpr (CW == 16) {
+      r.w[0] = __ldg(reinterpret_cast<const uint4*>(p));
+    } else if constexpr (CW == 8) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      r.w[0] = make_uint4(x.x, x.y, 0, 0);
+    } else {
+      r.w[0] = make_uint4(__ldg(reinterpret_cast<const unsigned*>(p)), 0, 0, 0);
+    }
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void epi_row_decode(const EwDevIn& in, const RawSeg<CW>& r, float* v) {
+  const unsigned* w = reinterpret_cast<const unsigned*>(r.w);
+  if (in.st == (uint8_t)SType::F32) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(w[j]);
+  } else if (in.st == (uint8_t)SType::BF16) {
+#pragma unroll
+    for (int k = 0; k < CW / 2; ++k) {
+      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) {
+      v[4 * k] = (w[k] & 0xffu) ? 1.f : 0.f;
+      v[4 * k + 1] = (w[k] & 0xff00u) ? 1.f : 0.f;
+      v[4 * k + 2] = (w[k] & 0xff0000u) ? 1.f : 0.f;
+      v[4 * k + 3] = (w[k] & 0xff000000u) ? 1.f : 0.f;
+    }
+  }
+}
+
+// Column sums over the 32 lanes of CW values per lane (fixed butterfly
+// order): returns the sum for column *col; lanes < CW hold distinct columns.
+template <int CW>
+__device__ __forceinline__ float col_butterfly(float (&x)[CW], int lane, int* col) {
+  int base = 0;
+#pragma unroll
+  for (int k = 0, w = CW / 2; w >= 1; ++k, w /= 2) {
+    const bool up = (lane >> k) & 1;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? x[i] : x[i + w];
+      const float keep = up ? x[i + w] : x[i];
+      x[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 1 << k));
+    }
+    if (up) base += w;
+  }
+#pragma unroll
+  for (int s = CW; s < 32; s *= 2) x[0] = __fadd_rn(x[0], __shfl_xor_sync(0xffffffffu, x[0], s));
+  *col = base;
+  return x[0];
+}
+
+// Tile raster: groups of GROUP_M tile-rows, N fastest inside a group, so the
+// ~148 tiles in flight share a few A row-panels and all of B through L2
+// (a plain M-fastest order re-reads A once per N tile).
+constexpr int GROUP_M = 8;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int* tm, int* tn) {
+  const int per_group = GROUP_M * tiles_n;
+  const int grp = t / per_group;
+  const int first = grp * GROUP_M;
+  const int gsz = min(GROUP_M, tiles_m - first);
+  const int r = t - grp * per_group;
+  *tm = first + r % gsz;
+  *tn = r / gsz;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+
+// 32 lanes x 32 columns -> lane l holds the sum over lanes of column l
+__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const bool upper = (lane & w) != 0;
+      float send = upper ? v[i] : v[i + w];
+      float keep = upper ? v[i + w] : v[i];
+      float recv = __shfl_xor_sync(0xffffffffu, send, w);
+      v[i] = __fadd_rn(keep, recv);
+    }
+  }
+  return v[0];
+}
+
+constexpr int kEpiReds = 2;  // reductions per GEMM epilogue (smem budget); more -> not fused
+
+template <class T, bool S>
+__host__ __device__ constexpr int epi_num_reds() {
+  if constexpr (S) return T::Reds::n; else return kEpiReds;
+}
+
+// Interpreted epilogue programs, instantiated per column-chunk width CW (the
+// same width a specialised program of the same size uses, so both sum their
+// reductions in the same order and stay bit-identical).
+template <int CW>
+struct VmEpi {};
+struct VmEpiTraits {
+  static constexpr int kSlots = kMaxSlots;
+  static constexpr int kIn = 0, kLit = 0;
+};
+template <class P>
+struct vm_cw {
+  static constexpr int value = 0;
+};
+template <int CW>
+struct vm_cw<VmEpi<CW>> {
+  static constexpr int value = CW;
+};
+__host__ __device__ constexpr int epi_chunk_width(int slots) { return slots <= 6 ? 16 : (slots <= 12 ? 8 : 4); }
+
+// CTAS = 1: one CTA per 128 x BN tile.  CTAS = 2: a CTA pair (cluster of 2
+// on one TPC) per 256 x BN tile: each CTA stages its 128 rows of A and half
+// of B's columns, the leader issues cta_group::2 MMAs over both CTAs' smem
+// into both CTAs' TMEM (per-SM smem traffic per MMA drops by a third), and
+// each CTA runs the epilogue of its own 128 rows.
+template <int CTAS, int BN>
+__host__ __device__ constexpr int num_stages() {
+  return CTAS == 2 ? 6 : STAGES;
+}
+
+template <int BN, class PROG, int CTAS = 1>
+__global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
+  constexpr int VMCW = vm_cw<PROG>::value;
+  constexpr bool SPEC = VMCW == 0;
+  using T = cond_t<SPEC, spec::Traits<cond_t<SPEC, PROG, spec::Prog<0, 0, spec::St<>, spec::Rd<>>>>,
+                               VmEpiTraits>;
+  constexpr int NS = T::kSlots;
+  constexpr int NRS = epi_num_reds<T, SPEC>();
+  constexpr int NST = num_stages<CTAS, BN>();
+  constexpr int BNC = BN / CTAS;                     // B columns staged per CTA
+  constexpr int B_STAGE_BYTES = BNC * BK * 2;
+  constexpr uint32_t STAGE_TX = A_STAGE_BYTES + B_STAGE_BYTES;  // per CTA
+  constexpr int TMEM_COLS = 2 * BN;  // 256 or 512
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sA = base;
+  const uint32_t sB = base + NST * A_STAGE_BYTES;
+  const uint32_t sBar = sB + NST * B_STAGE_BYTES;  // full[S], empty[S], tfull[2], tempty[2]
+  const uint32_t full_bar = sBar, empty_bar = sBar + 8 * NST, tfull_bar = sBar + 16 * NST,
+                 tempty_bar = tfull_bar + 16;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * NST + 32);
+  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * NST + 64);  // [kEpiReds][4][BN]
+  float* rowred = colred + kEpiReds * 4 * BN;                                          // [kEpiReds][2][BM]
+  float* allred = rowred + kEpiReds * 2 * BM;                                          // [kEpiReds][8]
+
+  const GemmParams& g = P.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
+  const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
+  const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tfull_bar + 8 * s, 1);
+      mbar_init(tempty_bar + 8 * s, 8 * CTAS);  // one arrival per epilogue warp of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < g.n_seg; ++q) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_a[q])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tma_b[q])) : "memory");
+    }
+  }
+  if (warp == 2) {
+    if constexpr (CTAS == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  // prologue done: let the next kernel start its own, then wait for the
+  // previous kernel's results (PDL, launch.cuh)
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = tile0; t < n_tiles; t += tile_step) {
+      int tm, tn;
+      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
+      for (int i = 0; i < g.n_pf; ++i) {
+        const int64_t cols = min((int64_t)BN, g.N - n0);
+        const uint32_t bytes = (uint32_t)((cols * g.pf_esize[i] + 15) & ~15);
+        for (int r = lane; r < BM && m0 + r < g.M; r += 32) {
+          const char* a = reinterpret_cast<const char*>(g.pf_ptr[i]) + (int64_t)(m0 + r) * g.pf_row_bytes[i] +
+                          (int64_t)n0 * g.pf_esize[i];
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+        }
+      }
+      if (lane == 0) {
+        const uint64_t pol_a = l2_policy(P.hint_a), pol_b = l2_policy(P.hint_b);
+        for (int q = 0; q < g.n_seg; ++q) {
+          const GemmSegParams& G = g.seg[q];
+          const CUtensorMap* ma = &P.tma_a[q];
+          const CUtensorMap* mb = &P.tma_b[q];
+          const int num_kb = (int)((G.K + BK - 1) / BK);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(empty_bar + 8 * s, ph ^ 1);
+            const uint32_t fb = full_bar + 8 * s;
+            const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
+            const int k0 = kb * BK;
+            const int nb = n0 + (int)rank * BNC;  // this CTA's half of B
+            if constexpr (CTAS == 2) {
+              // both halves complete on the leader's barrier, armed with both CTAs' bytes
+              const uint32_t lb = mapa_rank(fb, 0);
+              if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_TX);
+              if (G.a_kmajor) {
+                tma_load_2d_pair(a_dst, ma, lb, k0, m0, pol_a);
+              } else {
+                tma_load_2d_pair(a_dst, ma, lb, m0, k0, pol_a);
+                tma_load_2d_pair(a_dst + 8192, ma, lb, m0 + 64, k0, pol_a);
+              }
+              if (G.b_kmajor) {
+                tma_load_2d_pair(b_dst, mb, lb, k0, nb, pol_b);
+              } else {
+#pragma unroll
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d_pair(b_dst + c * 8192, mb, lb, nb + 64 * c, k0, pol_b);
+              }
+            } else {
+              mbar_expect_tx(fb, STAGE_TX);
+              if (G.a_kmajor) {
+                tma_load_2d(a_dst, ma, fb, k0, m0, pol_a);
+              } else {
+                tma_load_2d(a_dst, ma, fb, m0, k0, pol_a);
+                tma_load_2d(a_dst + 8192, ma, fb, m0 + 64, k0, pol_a);
+              }
+              if (G.b_kmajor) {
+                tma_load_2d(b_dst, mb, fb, k0, nb, pol_b);
+              } else {
+#pragma unroll
+                for (int c = 0; c < BNC / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, nb + 64 * c, k0, pol_b);
+              }
+            }
+            if (++s == NST) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+        const int as = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(tempty_bar + 8 * as, aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        uint32_t accum = 0;  // the tile's first MMA overwrites the accumulator
+        for (int q = 0; q < g.n_seg; ++q) {
+          const GemmSegParams& G = g.seg[q];
+          const uint32_t idesc = umma_idesc(BN, !G.a_kmajor, !G.b_kmajor, BM * CTAS);
+          const int num_kb = (int)((G.K + BK - 1) / BK);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(full_bar + 8 * s, ph);
+            tc_fence_after();
+            const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = G.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
+              const uint64_t bd = G.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
+              if constexpr (CTAS == 2)
+                umma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+              else
+                umma_bf16(d_tmem, ad, bd, idesc, accum);
+              accum = 1;
+            }
+            if constexpr (CTAS == 2)
+              umma_commit_pair(empty_bar + 8 * s);  // both CTAs' slots are free
+            else
+              umma_commit(empty_bar + 8 * s);
+            if (++s == NST) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+        }
+        if constexpr (CTAS == 2)
+          umma_commit_pair(tfull_bar + 8 * as);
+        else
+          umma_commit(tfull_bar + 8 * as);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue
+    // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (lane = tile row, the
+    // native tcgen05.ld 32x32b layout) and the CW-column chunks ch = h, h+2, ...
+    // Each lane loads / stores its row segment of CW consecutive elements
+    // with vector accesses; column sums use a shuffle butterfly.
+    const int ew = warp - 4;
+    const int q = ew & 3, h = ew >> 2;
+    const int et = threadIdx.x - 128;  // 0..255
+    const EwParams& E = g.epi;
+    const EwProgram& Pg = E.prog;
+    constexpr int CW = SPEC ? epi_chunk_width(NS) : VMCW;
+    constexpr int NSV = SPEC ? NS : (CW == 16 ? 6 : (CW == 8 ? 12 : kMaxSlots));  // interpreter slots
+    float v[NSV][CW];
+    if constexpr (SPEC) {
+#pragma unroll
+      for (int i = 0; i < T::kLit; ++i)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) v[T::kIn + i][j] = Pg.lits[i];
+    } else {
+      for (int i = 0; i < Pg.n_lits; ++i)
+#pragma unroll
+        for (int j = 0; j < CW; ++j) v[Pg.n_in + i][j] = Pg.lits[i];
+    }
+    auto red_slot = [&](int r) -> int {
+      if constexpr (SPEC) return T::Reds::at(2 * r); else return Pg.reduce_slot[r];
+    };
+    auto red_kind = [&](int r) -> int {
+      if constexpr (SPEC) return T::Reds::at(2 * r + 1); else return Pg.reduce_kind[r];
+    };
+    const int nred = SPEC ? NRS : Pg.n_reduces;
+    bool has_col = false, has_row = false, has_all = false;
+#pragma unroll
+    for (int r = 0; r < NRS; ++r)
+      if (r < nred) {
+        has_col |= red_kind(r) == RED_COL;
+        has_row |= red_kind(r) == RED_ROW;
+        has_all |= red_kind(r) == RED_ALL;
+      }
+    const bool vec_ok = E.vec == 4;
+    int it = 0;
+    for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+      int tm, tn;
+      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      tm = tm * CTAS + (int)rank;  // this CTA's 128-row block (partials layout)
+      const bool block_live = (int64_t)tm * BM < g.M;
+      const int64_t m = (int64_t)tm * BM + 32 * q + lane;
+      const bool mval = m < g.M;
+      const int as = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(tfull_bar + 8 * as, aph);
+      tc_fence_after();
+      float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
+#pragma unroll
+      for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
+      constexpr int NPF = SPEC && T::kIn > 1 ? T::kIn - 1 : 1;
+      RawSeg<CW> pf[NPF];  // next chunk's row segments of the vector operands
+      auto seg_full = [&](int ch) {
+        const int64_t n0 = (int64_t)tn * BN + ch * CW;
+        return mval && vec_ok && n0 + CW <= g.N;
+      };
+      if constexpr (SPEC) {
+        if (seg_full(h))
+#pragma unroll
+          for (int s2 = 1; s2 < T::kIn; ++s2)
+            if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + h * CW, pf[s2 - 1]);
+      }
+      for (int ch = h; ch < BN / CW; ch += 2) {
+        const int64_t n0 = (int64_t)tn * BN + ch * CW;
+        const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
+        const bool full = mval && ncol == CW && vec_ok;
+        RawSeg<CW> cur[NPF];
+        if constexpr (SPEC) {
+#pragma unroll
+          for (int s2 = 0; s2 < NPF; ++s2) cur[s2] = pf[s2];
+          if (ch + 2 < BN / CW && seg_full(ch + 2))
+#pragma unroll
+            for (int s2 = 1; s2 < T::kIn; ++s2)
+              if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, n0 + 2 * CW, pf[s2 - 1]);
+        }
+        tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
+        if constexpr (SPEC) {
+#pragma unroll
+          for (int s2 = 1; s2 < T::kIn; ++s2) {
+            if (full && seg_vector(E.in[s2]))
+              epi_row_decode<CW>(E.in[s2], cur[s2 - 1], v[s2]);
+            else
+              epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          }
+          T::template exec<CW>(v);
+#pragma unroll
+          for (int s2 = 0; s2 < T::Stores::n; ++s2)
+            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
+        } else {
+          for (int s2 = 1; s2 < Pg.n_in; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+          vm_exec<CW>(Pg, v);
+          for (int s2 = 0; s2 < Pg.n_stores; ++s2)
+            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[Pg.store_slot[s2]]);
+        }
+#pragma unroll
+        for (int r = 0; r < NRS; ++r) {
+          if (r >= nred) break;
+          const int kind = red_kind(r);
+          float x[CW];
+#pragma unroll
+          for (int j = 0; j < CW; ++j) x[j] = (mval && j < ncol) ? v[red_slot(r)][j] : 0.f;
+          if (kind == RED_COL) {
+            int col;
+            const float cs = col_butterfly<CW>(x, lane, &col);
+            if (lane < CW) colred[(r * 4 + q) * BN + ch * CW + col] = cs;
+          } else {
+            float s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < CW; ++j) s3 = __fadd_rn(s3, x[j]);
+            if (kind == RED_ROW)
+              rowacc[r] = __fadd_rn(rowacc[r], s3);
+            else
+              allacc[r] = __fadd_rn(allacc[r], s3);
+          }
+        }
+      }
+      // accumulator buffer free for the next tile's MMAs (one arrival per warp,
+      // on the leader's barrier for a pair)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CTAS == 2)
+          mbar_arrive_cluster(mapa_rank(tempty_bar + 8 * as, 0));
+        else
+          mbar_arrive(tempty_bar + 8 * as);
+      }
+      if (has_row || has_all) {
+#pragma unroll
+        for (int r = 0; r < NRS; ++r) {
+          if (r >= nred) break;
+          if (red_kind(r) == RED_ROW) rowred[(r * 2 + h) * BM + 32 * q + lane] = rowacc[r];
+          if (red_kind(r) == RED_ALL) {
+            const float s3 = warp_sum(allacc[r]);
+            if (lane == 0) allred[r * 8 + ew] = s3;
+          }
+        }
+      }
+      if ((has_col || has_row || has_all) && block_live) {
+        epi_bar();
+#pragma unroll
+        for (int r = 0; r < NRS; ++r) {
+          if (r >= nred) break;
+          const int kind = red_kind(r);
+          if (kind == RED_COL) {
+            for (int c = et; c < BN; c += 256) {
+              const int64_t n = (int64_t)tn * BN + c;
+              if (n >= g.N) continue;
+              float s3 = 0.f;
+              for (int w2 = 0; w2 < 4; ++w2) s3 = __fadd_rn(s3, colred[(r * 4 + w2) * BN + c]);
+              E.red[r][(int64_t)tm * g.N + n] = s3;
+            }
+          } else if (kind == RED_ROW) {
+            if (et < BM) {
+              const int64_t mm = (int64_t)tm * BM + et;
+              if (mm < g.M)
+                E.red[r][mm * E.gx + tn] = __fadd_rn(rowred[(r * 2) * BM + et], rowred[(r * 2 + 1) * BM + et]);
+            }
+          } else if (et == 0) {
+            float s3 = 0.f;
+            for (int w2 = 0; w2 < 8; ++w2) s3 = __fadd_rn(s3, allred[r * 8 + w2]);
+            E.red[r][(int64_t)tm * E.gx + tn] = s3;
+          }
+        }
+        epi_bar();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // the pair's MMAs and epilogues are done
+  if (warp == 2) {
+    tc_fence_after();
+    if constexpr (CTAS == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+}
+
+}  // namespace kern
+}  // namespace dlvm

@@ -1,9 +1,9 @@
 // Host-visible kernel parameter blocks and launchers (sm_100a).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
-
-#include <cstdint>
+#endif
 
 #include "ew_program.h"
 
@@ -38,8 +38,10 @@ struct EwParams {
   float* red[kMaxReduces];  // partial buffers
 };
 
+#ifndef __CUDACC_RTC__
 // element-wise program kernel over an [R, C] iteration space
 cudaError_t launch_ew(const EwParams& p, int bx, int by, cudaStream_t stream);
+#endif
 
 constexpr int kMaxSeg = 8;
 
@@ -69,7 +71,15 @@ struct GemmParams {
   int32_t pf_esize[4];      // element size in bytes
 };
 
+#ifndef __CUDACC_RTC__
 cudaError_t launch_gemm_simt(const GemmParams& p, cudaStream_t stream);
+
+// kernels compiled at create time (csrc/jit.cpp): same launch geometry as the
+// ahead-of-time launchers, the CUfunction passed as `fn`
+cudaError_t launch_ew_fn(void* fn, const EwParams& p, int bx, int by, cudaStream_t stream);
+cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStream_t stream);
+cudaError_t launch_gemm_simt_fn(void* fn, const GemmParams& p, cudaStream_t stream);
+int gemm_tc_ctas(int64_t M, int bn);  // 2: the launcher runs CTA pairs for this shape
 cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream);
 bool gemm_tc_available();
 
@@ -81,5 +91,7 @@ cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_
 // [rows, cols] f32 or bf16 (src_f32) -> bf16 rows of `ld` elements (ld >= cols)
 cudaError_t launch_pack_bf16(const void* src, bool src_f32, int64_t rows, int64_t cols, void* dst, int64_t ld,
                              cudaStream_t stream);
+
+#endif
 
 }  // namespace dlvm

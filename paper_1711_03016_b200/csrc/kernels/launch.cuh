@@ -14,9 +14,13 @@
 // then returns at once.  DLVM_PDL=0 launches without the attribute.
 #pragma once
 
+#ifndef __CUDACC_RTC__
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#endif
 
 namespace dlvm {
 
@@ -27,6 +31,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_trigger() {}  // implicit trigger at CTA exit
 #endif
 
+#ifndef __CUDACC_RTC__
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("DLVM_PDL");
@@ -60,5 +65,62 @@ struct LaunchCfg {
     cfg.numAttrs = n;
   }
 };
+
+// Launch a kernel loaded from a create-time JIT cubin (csrc/jit.cpp) with the
+// configuration of `L` (same grid, cluster and PDL attributes as the
+// ahead-of-time path); `smem` > 48 KB is opted in on the function first.
+inline cudaError_t launch_jit(void* fn, const LaunchCfg& L, void** args) {
+  static PFN_cuLaunchKernelEx_v11060 launch = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint("cuLaunchKernelEx", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<PFN_cuLaunchKernelEx_v11060>(p)
+               : nullptr;
+  }();
+  static PFN_cuFuncSetAttribute_v9000 set_attr = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<PFN_cuFuncSetAttribute_v9000>(p)
+               : nullptr;
+  }();
+  if (!launch || !set_attr) return cudaErrorNotSupported;
+  CUfunction f = static_cast<CUfunction>(fn);
+  if (L.cfg.dynamicSmemBytes > 48 * 1024 &&
+      set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)L.cfg.dynamicSmemBytes) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  CUlaunchAttribute at[2];
+  unsigned na = 0;
+  for (unsigned i = 0; i < L.cfg.numAttrs; ++i) {
+    const cudaLaunchAttribute& a = L.cfg.attrs[i];
+    if (a.id == cudaLaunchAttributeClusterDimension) {
+      at[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      at[na].value.clusterDim.x = a.val.clusterDim.x;
+      at[na].value.clusterDim.y = a.val.clusterDim.y;
+      at[na].value.clusterDim.z = a.val.clusterDim.z;
+      ++na;
+    } else if (a.id == cudaLaunchAttributeProgrammaticStreamSerialization) {
+      at[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      at[na].value.programmaticStreamSerializationAllowed = a.val.programmaticStreamSerializationAllowed;
+      ++na;
+    }
+  }
+  CUlaunchConfig c = {};
+  c.gridDimX = L.cfg.gridDim.x;
+  c.gridDimY = L.cfg.gridDim.y;
+  c.gridDimZ = L.cfg.gridDim.z;
+  c.blockDimX = L.cfg.blockDim.x;
+  c.blockDimY = L.cfg.blockDim.y;
+  c.blockDimZ = L.cfg.blockDim.z;
+  c.sharedMemBytes = (unsigned)L.cfg.dynamicSmemBytes;
+  c.hStream = static_cast<CUstream>(L.cfg.stream);
+  c.attrs = at;
+  c.numAttrs = na;
+  return launch(&c, f, args, nullptr) == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+#endif
 
 }  // namespace dlvm

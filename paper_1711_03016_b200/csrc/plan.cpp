@@ -1253,6 +1253,36 @@ struct Planner {
       for (int d = 0; d < kPlanDims; ++d) g.stores[i].strides[d] = d < g.ndims ? st_s[i][d] : 0;
   }
 
+  // A long 1-D iteration space (every operand contiguous or a scalar; only
+  // full reductions) is viewed as [n/W, W] rows so the 2-D kernel streams
+  // several rows per thread (the 1-D form gives each thread one vector)
+  static void rows_of_long_1d(EwGroup& g) {
+    if (g.ndims != 1 || g.ncols != 1 || g.dims[0] < (1 << 20)) return;
+    for (int q = 0; q < g.prog.n_reduces; ++q)
+      if (g.prog.reduce_kind[q] != RED_ALL) return;
+    const int64_t n = g.dims[0];
+    int64_t W = 0;
+    for (int64_t w : {4096, 2048, 1024})
+      if (n % w == 0) {
+        W = w;
+        break;
+      }
+    if (!W) return;
+    auto ok = [](const IterRef& r) { return r.buf == -2 || r.strides[0] == 0 || r.strides[0] == 1; };
+    for (auto& r : g.inputs) if (!ok(r)) return;
+    for (auto& r : g.stores) if (!ok(r)) return;
+    auto split = [&](IterRef& r) {
+      const int64_t st = r.strides[0];
+      r.strides[0] = st * W;
+      r.strides[1] = st;
+    };
+    for (auto& r : g.inputs) split(r);
+    for (auto& r : g.stores) split(r);
+    g.ndims = 2;
+    g.dims[0] = n / W;
+    g.dims[1] = W;
+  }
+
   static void ew_launch(EwGroup& g) {
     int64_t C = 1, R = 1;
     for (int d = 0; d < g.ndims; ++d) (d < g.ndims - g.ncols ? R : C) *= g.dims[d];
@@ -1415,6 +1445,7 @@ struct Planner {
         if (s.ew.ndims == 1 && ri.kind == RED_COL) ri.kind = RED_ALL;
         s.ew.prog.reduce_kind[ri.slot_index] = ri.kind;
       }
+      rows_of_long_1d(s.ew);
       ew_launch(s.ew);
       s.ew.sig = program_signature(s.ew.prog);
       int64_t C = 1, R = 1;

@@ -17,7 +17,7 @@ DLVM_OK, DLVM_ERR_VERIFY, DLVM_ERR_PARSE, DLVM_ERR_USAGE, DLVM_ERR_RUNTIME, DLVM
     DLVM_ERR_UNSUPPORTED = range(7)
 DLVM_BOOL, DLVM_F32, DLVM_F64, DLVM_BF16 = range(4)
 DLVM_DOT_F32, DLVM_DOT_BF16 = 0, 1
-DLVM_PLAN_ONLY, DLVM_NO_FUSION, DLVM_NO_SPECIALIZE, DLVM_NO_OPT = 1, 2, 4, 8
+DLVM_PLAN_ONLY, DLVM_NO_FUSION, DLVM_NO_SPECIALIZE, DLVM_NO_OPT, DLVM_NO_JIT = 1, 2, 4, 8, 16
 DLVM_PRIMAL, DLVM_GRADIENT = 0, 1
 MAX_RANK = 8
 
