@@ -369,3 +369,32 @@ def test_adjoint_ir_structure_filecheck():
         assert pos < len(lines), f"CHECK not found in order: {pat}\n{g}"
     assert "transpose %w" not in g  # CHECK-NOT: dX (x is not in wrt)
     assert lines[-2].endswith("%2: <4 x 5 x f32>)")  # kept g result last (A7)
+
+
+def test_kernel_templates_compile_under_nvrtc():
+    """The create-time JIT (csrc/jit.cpp) compiles the kernel templates with
+    NVRTC; a header change that breaks runtime compilation must fail here, on
+    the CPU (NVRTC needs no GPU).  One EW, one tcgen05 (CTA pair) and one SIMT
+    instantiation with registry programs."""
+    nvrtc = pytest.importorskip("cuda.bindings.nvrtc")
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from gen_specializations import prog_type
+    kdir = os.path.join(ROOT, "paper_1711_03016_b200", "csrc", "kernels")
+    prog = lambda sig: prog_type(sig).replace("spec::", "dlvm::spec::")
+    exprs = [f"&dlvm::kern::ew2d_kernel<4, {prog('i4l0|22,0,1,2;1,4,0,0;9,5,3,0|s6|r')}>",
+             f"&dlvm::kern::gemm_tc_kernel<256, {prog('i2l0|21,1,0,0;9,0,2,0|s3|r3:0')}, 2>",
+             f"&dlvm::kern::simt::gemm_simt_kernel<false, 32, {prog('i2l1|7,0,1,0|s3|r')}>"]
+    opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device", ("-I" + kdir).encode(),
+            b"-I/usr/local/cuda/include"]
+    src = b'#include "gemm_tc_kernel.cuh"\n#include "gemm_simt_kernel.cuh"\n'
+    err, p = nvrtc.nvrtcCreateProgram(src, b"t.cu", 0, [], [])
+    for e in exprs:
+        nvrtc.nvrtcAddNameExpression(p, e.encode())
+    (r,) = nvrtc.nvrtcCompileProgram(p, len(opts), opts)
+    _, n = nvrtc.nvrtcGetProgramLogSize(p)
+    log = b" " * n
+    nvrtc.nvrtcGetProgramLog(p, log)
+    assert r == nvrtc.nvrtcResult.NVRTC_SUCCESS, log.decode()[:3000]
+    for e in exprs:
+        _, low = nvrtc.nvrtcGetLoweredName(p, e.encode())
+        assert low and low.startswith(b"_ZN4dlvm4kern")
