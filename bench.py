@@ -244,6 +244,17 @@ def cpu_baseline_chain(rows: int, C: int = 16384):
 
 
 # ----------------------------------------------------------------- main
+def ncu_traffic(name):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the workload's dominant kernel from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(prof)).get(name)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def bench_chain(dev, K, W_):
     """config 2: y = tanh(x*w + b)*m and its adjoint on [16384, 16384] f32."""
     import torch
@@ -273,7 +284,8 @@ def bench_chain(dev, K, W_):
     return {"workload": "c2_chain [16384,16384] f32", "fwd_ms": ms_f, "fwd_gbs": bf / (ms_f * 1e-3) / 1e9,
             "fwd_adj_ms": ms_a, "fwd_adj_gbs": ba / (ms_a * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": gbs_a, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": gbs_a / pk["hbm_gbs"], "traffic": None,
+                         "frac": gbs_a / pk["hbm_gbs"],
+                         "traffic": (ncu_traffic("c2_chain") or {}).get("traffic_bytes"),
                          "kernel": main["desc"][:90], "algorithmic_bytes": ba},
             "launches_fwd_adj": f.num_launches(1), "kernels": [{"desc": r["desc"][:80], "ms": r["ms"]} for r in kb]}
 
@@ -470,12 +482,12 @@ def main():
             "peak_kind": "sustained bf16 " + pk["source"], "frac_of_burst": achieved / pk["bf16_tflops"],
             "gemm_share_of_step": gemm_ms / sum(r["ms"] for r in kb) if kb else None,
             "algorithmic_flops_per_step": step_flops, "tcgen05_launches": len(tc)}
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            roof["traffic"] = json.load(open(prof)).get(w.name)
-        except Exception:
-            pass
+    tr = ncu_traffic(w.name)
+    if tr:
+        roof["traffic"] = tr["traffic_bytes"]
+        roof["traffic_kernel"] = tr["kernel"]
+        roof["traffic_algorithmic_bytes"] = tr["algorithmic_bytes"]
+        roof["traffic_source"] = tr["source"]
     launches = (f.num_launches(1) + (sgd_info["launches"] if sgd_info else 0)) * K
     # end to end: H2D of this step's batch (pinned host) + step + D2H of the loss
     e2e = None
