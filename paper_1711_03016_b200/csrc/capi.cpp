@@ -253,7 +253,15 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       gp.bn = g.bn;
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);
-      for (int i = 1; i < gp.epi.prog.n_in && gp.n_pf < 4; ++i) {  // row-contiguous [M, N] epilogue inputs
+      // L2 prefetch of row-contiguous epilogue inputs by the TMA producer warp:
+      // off by default -- measured to slow the mainloop (the producer issues
+      // them between its operand loads): c4 10.53 -> 10.31 ms without.
+      // DLVM_GEMM_PF=1 enables it.
+      static const bool epi_pf = [] {
+        const char* e = std::getenv("DLVM_GEMM_PF");
+        return e && e[0] == '1';
+      }();
+      for (int i = 1; epi_pf && i < gp.epi.prog.n_in && gp.n_pf < 4; ++i) {  // row-contiguous [M, N] epilogue inputs
         const EwDevIn& r = gp.epi.in[i];
         if (r.nchunks != 1 || r.s[1] != 1 || r.s[0] == 0) continue;
         const int es = r.st == (uint8_t)SType::F32 ? 4 : r.st == (uint8_t)SType::BF16 ? 2 : 1;

@@ -365,6 +365,17 @@ struct RawSeg {
 // an operand whose CW-column row segment is one contiguous vector access
 __device__ __forceinline__ bool seg_vector(const EwDevIn& in) { return in.s[1] == 1 && in.s[0] != 0; }
 
+#ifndef DLVM_EPI_L1_PREFETCH
+#define DLVM_EPI_L1_PREFETCH 0  // measured no gain on the mask + bf16 epilogue (tools/gemm_store_probe.py)
+#endif
+constexpr bool kEpiL1Prefetch = DLVM_EPI_L1_PREFETCH != 0;
+
+__device__ __forceinline__ void epi_row_prefetch_l1(const EwDevIn& in, int64_t m, int64_t n0) {
+  const int es = in.st == (uint8_t)SType::F32 ? 4 : in.st == (uint8_t)SType::BF16 ? 2 : 1;
+  const char* a = reinterpret_cast<const char*>(in.ptr) + (m * in.s[0] + n0) * es;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+}
+
 template <int CW>
 __device__ __forceinline__ void epi_row_fetch(const EwDevIn& in, int64_t m, int64_t n0, RawSeg<CW>& r) {
   const int64_t off = m * in.s[0] + n0;
@@ -770,6 +781,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #pragma unroll
             for (int s2 = 1; s2 < T::kIn; ++s2)
               if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, n0 + 2 * CW, pf[s2 - 1]);
+          // the row segments two chunks further on into L1 (no registers):
+          // their latency overlaps this chunk and the next
+          if (kEpiL1Prefetch && ch + 6 < BN / CW && seg_full(ch + 6))
+#pragma unroll
+            for (int s2 = 1; s2 < T::kIn; ++s2)
+              if (seg_vector(E.in[s2])) epi_row_prefetch_l1(E.in[s2], m, n0 + 6 * CW);
         }
         tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
         if constexpr (SPEC) {
