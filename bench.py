@@ -129,9 +129,10 @@ def to_dev(x, dev, bf16=False):
 
 
 def mlp_setup(w, dev, rank):
-    """Inputs of the MLP gradient on this rank: x and W as bf16 (they feed
-    only dots, dlvm.h), b and t as f32.  Returns (handle, dev inputs, seed,
-    host inputs, n_grads)."""
+    """Inputs of the MLP gradient on this rank: x and W as bf16 (the bf16 dot
+    policy rounds them anyway), one-hot t as bf16 (exact), the rest f32
+    (dlvm.h storage rule).  Returns (handle, dev inputs, seed, host inputs,
+    n_grads)."""
     import numpy as np
     import torch
     import paper_1711_03016_b200 as P
@@ -139,7 +140,9 @@ def mlp_setup(w, dev, rank):
     host = w.inputs(row_offset=rank * w.batch)
     dev_in = []
     for a, x in zip(w.args, host):
-        bf = w.dot_precision == "bf16" and (a.name == "x" or a.name.startswith("w"))
+        # bf16 storage (dlvm.h): the dot operands the bf16 policy rounds anyway,
+        # and one-hot targets (exact in bf16) -- halves their upload in e2e
+        bf = (w.dot_precision == "bf16" and (a.name == "x" or a.name.startswith("w"))) or a.dist[0] == "onehot"
         dev_in.append(to_dev(x, dev, bf))
     seed = torch.tensor(np.float32(w.seed()), device=dev)
     return f, dev_in, seed, host, 2 * len(w.layers)

@@ -47,9 +47,11 @@ typedef enum {
 } dlvm_status;
 
 /* Element types of caller tensors.  IR `bool` is stored one byte per element
- * (0/1).  DLVM_BF16 is an execution-precision policy, not an IR type (reading
- * A15 of SURVEY.md §8(c)): an f32 argument that feeds only `dot` may be
- * passed as bf16 under DLVM_DOT_BF16, and an f32 output may be requested as
+ * (0/1).  DLVM_BF16 is a storage type, not an IR type (reading A15 of
+ * SURVEY.md §8(c)): an f32 argument may be passed as bf16 -- its values are
+ * then exactly the f32 widening of the bf16 elements (e.g. one-hot targets,
+ * or operands the bf16 dot policy rounds anyway) -- under DLVM_DOT_BF16, or
+ * under DLVM_DOT_F32 if it feeds no `dot`; an f32 output may be requested as
  * bf16 (stored with round-to-nearest-even). */
 typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3 } dlvm_dtype;
 

@@ -919,7 +919,12 @@ struct Planner {
       }
     }
     cast_buf.assign(f.num_args(), -1);
-    plan.input_feeds_only_dot.assign(f.num_args(), 0);
+    // an f32 argument may be passed as bf16 (its values are then exactly the
+    // f32 widening of the bf16 elements): every consumer reads the storage
+    // type at run time, except an fp32-policy SIMT dot (both operands f32)
+    plan.input_bf16_ok.assign(f.num_args(), 0);
+    for (int i = 0; i < f.num_args(); ++i)
+      plan.input_bf16_ok[i] = ty(i).dtype == DType::F32 && (opt.policy == Policy::BF16 || !vi[i].dot_use);
     if (opt.policy == Policy::BF16) {
       for (int i = 0; i < f.num_args(); ++i) {
         if (!vi[i].dot_use || ty(i).dtype != DType::F32) continue;
@@ -928,7 +933,6 @@ struct Planner {
         plan.bufs[b].cast_ld = padded_ld(ty(i));
         cast_buf[i] = b;
         vi[i].homes.push_back(make_home(b, i, SType::BF16, padded_ld(ty(i))));
-        plan.input_feeds_only_dot[i] = (vi[i].group_use || !vi[i].outs.empty()) ? 0 : 1;
       }
     }
   }

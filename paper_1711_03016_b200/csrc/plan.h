@@ -132,7 +132,7 @@ struct Plan {
   size_t workspace_bytes = 0;
   int n_inputs = 0, n_outputs = 0;
   bool seed_is_input = false;    // gradient plans: last parameter is the seed
-  std::vector<int> input_feeds_only_dot;  // per input: 1 if it may be passed as bf16
+  std::vector<int> input_bf16_ok;  // per input: 1 if it may be passed as bf16 (see make_plan)
   int launches() const;
   std::string str() const;
 };

@@ -508,3 +508,30 @@ def test_cross_ad_oracle_adjoint_ir_on_gpu(case):
     bounds = term_bound(oracle.parse(gtext), name, ins64)
     for k, (g, r, b) in enumerate(zip(res["primal"], ref, bounds)):
         assert_f32_parity(g, r, b, what=f"{case} oracle-IR out{k}")
+
+
+@pytest.mark.parametrize("case", ["c3", "c2"])
+def test_bf16_storage_inputs_bit_identical(case):
+    """dlvm.h: an f32 argument may be passed as bf16 (bf16 dot policy: any;
+    fp32 policy: not feeding a dot).  With bf16-representable values the
+    results are bit-identical to passing the same values as f32 (the kernels
+    widen on load: EW loads, GEMM epilogue inputs, dot operands)."""
+    import torch
+    import paper_1711_03016_b200 as P
+    dev = torch.device("cuda:0")
+    if case == "c3":
+        w, prec = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)]), "bf16"
+        as_bf = {"t", "b1", "b2", "x", "w1"}
+    else:
+        w, prec = W.c2(96, 4096), "f32"
+        as_bf = {"x", "w", "b", "m"}
+    f = P.Function(w.text, w.fn, w.grad, dot_precision=prec)
+    host = [bf16_round(x) for x in w.inputs()]
+    ins32 = [torch.from_numpy(x).to(dev) for x in host]
+    ins16 = [t.to(torch.bfloat16) if a.name in as_bf else t for t, a in zip(ins32, w.args)]
+    sd = w.seed()
+    seed = torch.from_numpy(np.array(bf16_round(np.asarray(sd, np.float32)) if np.ndim(sd) else np.float32(sd))).to(dev)
+    a = [o.cpu().numpy() for o in f.run(ins32) + f.grad_run(ins32, seed=seed)]
+    b = [o.cpu().numpy() for o in f.run(ins16) + f.grad_run(ins16, seed=seed)]
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
