@@ -763,13 +763,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         return mval && vec_ok && n0 + CW <= g.N;
       };
+      // warp h takes every other 16-column block (chunks of CW < 16 walk a
+      // block in order), so which warp sums which columns -- and with
+      // element-by-element row/full sums the whole summation order -- does
+      // not depend on the chunk width: a kept loss computed by the gradient's
+      // epilogue equals the primal's bit for bit (reading A20) even when the
+      // two programs get different chunk widths
+      constexpr int SUB = 16 / CW;                 // chunks per 16-column block
+      constexpr int NIT = BN / CW / 2;             // chunks per warp per tile
+      auto chunk_of = [&](int i) { return (h + 2 * (i / SUB)) * SUB + i % SUB; };
       if constexpr (SPEC) {
-        if (seg_full(h))
+        if (seg_full(chunk_of(0)))
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2)
-            if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + h * CW, pf[s2 - 1]);
+            if (seg_vector(E.in[s2]))
+              epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + chunk_of(0) * CW, pf[s2 - 1]);
       }
-      for (int ch = h; ch < BN / CW; ch += 2) {
+      for (int it = 0; it < NIT; ++it) {
+        const int ch = chunk_of(it);
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
         const bool full = mval && ncol == CW && vec_ok;
@@ -777,16 +788,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         if constexpr (SPEC) {
 #pragma unroll
           for (int s2 = 0; s2 < NPF; ++s2) cur[s2] = pf[s2];
-          if (ch + 2 < BN / CW && seg_full(ch + 2))
+          const int nx = it + 1 < NIT ? chunk_of(it + 1) : 0;
+          if (it + 1 < NIT && seg_full(nx))
 #pragma unroll
             for (int s2 = 1; s2 < T::kIn; ++s2)
-              if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, n0 + 2 * CW, pf[s2 - 1]);
-          // the row segments two chunks further on into L1 (no registers):
-          // their latency overlaps this chunk and the next
-          if (kEpiL1Prefetch && ch + 6 < BN / CW && seg_full(ch + 6))
+              if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + nx * CW, pf[s2 - 1]);
+          // row segments three chunks further on into L1 (no registers)
+          const int nx3 = it + 3 < NIT ? chunk_of(it + 3) : 0;
+          if (kEpiL1Prefetch && it + 3 < NIT && seg_full(nx3))
 #pragma unroll
             for (int s2 = 1; s2 < T::kIn; ++s2)
-              if (seg_vector(E.in[s2])) epi_row_prefetch_l1(E.in[s2], m, n0 + 6 * CW);
+              if (seg_vector(E.in[s2])) epi_row_prefetch_l1(E.in[s2], m, (int64_t)tn * BN + nx3 * CW);
         }
         tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
         if constexpr (SPEC) {
@@ -818,14 +830,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             int col;
             const float cs = col_butterfly<CW>(x, lane, &col);
             if (lane < CW) colred[(r * 4 + q) * BN + ch * CW + col] = cs;
-          } else {
-            float s3 = 0.f;
+          } else if (kind == RED_ROW) {  // element by element (chunk-width independent)
 #pragma unroll
-            for (int j = 0; j < CW; ++j) s3 = __fadd_rn(s3, x[j]);
-            if (kind == RED_ROW)
-              rowacc[r] = __fadd_rn(rowacc[r], s3);
-            else
-              allacc[r] = __fadd_rn(allacc[r], s3);
+            for (int j = 0; j < CW; ++j) rowacc[r] = __fadd_rn(rowacc[r], x[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) allacc[r] = __fadd_rn(allacc[r], x[j]);
           }
         }
       }

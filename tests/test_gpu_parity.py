@@ -535,3 +535,18 @@ def test_bf16_storage_inputs_bit_identical(case):
     b = [o.cpu().numpy() for o in f.run(ins16) + f.grad_run(ins16, seed=seed)]
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("case", ["c3", "c5"])
+def test_A20_kept_loss_bit_equal_bf16(case):
+    """Reading A20: the kept loss of the gradient run equals
+    dlvm_fn_run's bit for bit, also when the loss is a full sum fused into a
+    tcgen05 epilogue whose program (and chunk width) differs between the
+    primal and the gradient plans."""
+    if case == "c3":
+        w = W.c3(256, layers=[(256, 256, "relu"), (256, 100, None)])
+    else:
+        w = W._mlp_workload(5, "c5s", 256, [(256, 256, "tanh")] * 2, ("normal",), ("uniform", -0.5, 0.5),
+                            1.0 / 256, "bf16", 256)
+    res = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
+    assert res["grad"][-1] == res["primal"][0]
