@@ -251,6 +251,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       }
       gp.bm = g.bm;
       gp.bn = g.bn;
+      gp.ksplit = g.ksplit;
+      gp.split_bytes = g.split_bytes;
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);
       // L2 prefetch of row-contiguous epilogue inputs by the TMA producer warp:

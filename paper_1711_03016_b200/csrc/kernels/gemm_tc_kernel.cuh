@@ -548,7 +548,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
+  const int base_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
+  const int nsplit = g.ksplit > 1 ? g.ksplit : 1;
+  const int n_tiles = base_tiles * nsplit;       // work items (tile, K split)
   const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
   const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
 
@@ -593,7 +595,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     uint32_t ph = 0;
     for (int t = tile0; t < n_tiles; t += tile_step) {
       int tm, tn;
-      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      const int split = t / base_tiles;
+      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
       const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
       for (int i = 0; i < g.n_pf; ++i) {
         const int64_t cols = min((int64_t)BN, g.N - n0);
@@ -611,7 +614,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           const CUtensorMap* ma = &P.tma_a[q];
           const CUtensorMap* mb = &P.tma_b[q];
           const int num_kb = (int)((G.K + BK - 1) / BK);
-          for (int kb = 0; kb < num_kb; ++kb) {
+          const int kbs = (num_kb + nsplit - 1) / nsplit;
+          const int kb_lo = split * kbs, kb_hi = kb_lo + kbs < num_kb ? kb_lo + kbs : num_kb;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(empty_bar + 8 * s, ph ^ 1);
             const uint32_t fb = full_bar + 8 * s;
             const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
@@ -663,6 +668,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       uint32_t ph = 0;
       int it = 0;
       for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+        const int split = t / base_tiles;
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(tempty_bar + 8 * as, aph ^ 1);
@@ -673,7 +679,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           const GemmSegParams& G = g.seg[q];
           const uint32_t idesc = umma_idesc(BN, !G.a_kmajor, !G.b_kmajor, BM * CTAS);
           const int num_kb = (int)((G.K + BK - 1) / BK);
-          for (int kb = 0; kb < num_kb; ++kb) {
+          const int kbs = (num_kb + nsplit - 1) / nsplit;
+          const int kb_lo = split * kbs, kb_hi = kb_lo + kbs < num_kb ? kb_lo + kbs : num_kb;
+          for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(full_bar + 8 * s, ph);
             tc_fence_after();
             const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
@@ -745,8 +753,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     int it = 0;
     for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
       int tm, tn;
-      tile_coords(t, P.tiles_m, P.tiles_n, &tm, &tn);
+      const int split = t / base_tiles;
+      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
       tm = tm * CTAS + (int)rank;  // this CTA's 128-row block (partials layout)
+      // split K: this work item's raw accumulator goes to its split's slice
+      EwDevOut out0 = E.out[0];
+      out0.ptr = static_cast<char*>(out0.ptr) + (int64_t)split * g.split_bytes;
       const bool block_live = (int64_t)tm * BM < g.M;
       const int64_t m = (int64_t)tm * BM + 32 * q + lane;
       const bool mval = m < g.M;
@@ -812,12 +824,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           T::template exec<CW>(v);
 #pragma unroll
           for (int s2 = 0; s2 < T::Stores::n; ++s2)
-            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
+            epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
         } else {
           for (int s2 = 1; s2 < Pg.n_in; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
           vm_exec<CW>(Pg, v);
           for (int s2 = 0; s2 < Pg.n_stores; ++s2)
-            epi_row_store<CW>(E.out[s2], m, n0, mval ? ncol : 0, full, v[Pg.store_slot[s2]]);
+            epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[Pg.store_slot[s2]]);
         }
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {

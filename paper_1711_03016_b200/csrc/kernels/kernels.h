@@ -65,6 +65,11 @@ struct GemmParams {
   EwParams epi;        // ndims 2, dims {M, N}; slot 0 = accumulator
   // epilogue inputs with contiguous rows (e.g. the saved ReLU mask): the TMA
   // producer prefetches each tile's rows into L2 while the tile's MMAs run
+  // split K (single segment): work item t covers tile t % tiles, K range
+  // split t / tiles of ksplit, and stores its raw accumulator to the single
+  // output at + split * split_bytes (a following EW step sums the splits)
+  int32_t ksplit;
+  int64_t split_bytes;
   int32_t n_pf;
   const void* pf_ptr[4];
   int64_t pf_row_bytes[4];  // row stride in bytes

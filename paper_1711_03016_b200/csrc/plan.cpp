@@ -24,6 +24,7 @@
 #include "plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <set>
@@ -1294,7 +1295,7 @@ struct Planner {
     auto ok4 = [&](const IterRef& r) {
       if (r.buf == -2) return true;
       int64_t cs = r.strides[g.ndims - 1];
-      if (r.nchunks != 1) return false;
+      if (r.nchunks != 1 && (cs != 1 || r.chunk_stride % 4)) return false;
       if (cs == 0) return true;
       if (cs != 1 || r.offset % 4) return false;
       for (int d = 0; d < g.ndims - 1; ++d)
@@ -1539,6 +1540,49 @@ struct Planner {
     gm.epi.gx = gx;
     gm.epi.gy = gy;
     gm.epi.sig = program_signature(gm.epi.prog);
+    // split K when the tile grid fills the SMs badly (wave quantization):
+    // the GEMM stores S raw partial tiles and the epilogue program moves to
+    // an EW step that sums them in split order (deterministic)
+    const int S = split_k(gm);
+    EwGroup split_ew;
+    if (S > 1) {
+      split_ew = gm.epi;
+      const int pbuf = add_buf(BufferSlot::Work, -1, (size_t)S * gm.M * gm.N * 4, SType::F32);
+      IterRef part;
+      part.buf = pbuf;
+      part.strides[0] = gm.N;
+      part.strides[1] = 1;
+      part.nchunks = S;
+      part.chunk_stride = gm.M * gm.N;
+      split_ew.inputs[0] = part;
+      split_ew.ndims = 2;
+      split_ew.ncols = 1;
+      split_ew.dims[0] = gm.M;
+      split_ew.dims[1] = gm.N;
+      ew_launch(split_ew);
+      split_ew.sig = program_signature(split_ew.prog);
+      EwGroup st;
+      st.ndims = 2;
+      st.dims[0] = gm.M;
+      st.dims[1] = gm.N;
+      IterRef acc;
+      acc.buf = -2;
+      st.inputs.push_back(acc);
+      IterRef o;
+      o.buf = pbuf;
+      o.strides[0] = gm.N;
+      o.strides[1] = 1;
+      st.stores.push_back(o);
+      st.prog.n_in = 1;
+      st.prog.n_stores = 1;
+      st.prog.store_slot[0] = 0;
+      st.gx = gx;
+      st.gy = gy;
+      st.sig = program_signature(st.prog);
+      gm.epi = st;
+      gm.ksplit = S;
+      gm.split_bytes = gm.M * gm.N * 4;
+    }
     std::ostringstream d;
     d << (gm.tensor_core ? "gemm tcgen05 bf16" : (bf ? "gemm simt bf16" : "gemm simt f32")) << " %"
       << f.names[dv] << " M=" << gm.M << " N=" << gm.N << " K=" << gm.K;
@@ -1559,10 +1603,53 @@ struct Planner {
         else if (r.kind == Root::Copy) d << " copy(%" << f.names[r.v] << ")";
       }
     }
+    if (S > 1) d << " (K split " << S << ", raw partials; epilogue in the next step)";
     s.desc = d.str();
     gm.epi.desc = s.desc;
     plan.steps.push_back(s);
+    if (S > 1) {
+      Step e;
+      e.kind = Step::EW;
+      e.ew = split_ew;
+      std::ostringstream de;
+      de << "ew [" << gm.M << "," << gm.N << "] vec" << split_ew.vec << " sum of " << S << " K-split partials of %"
+         << f.names[dv] << " + epilogue ops=" << (int)split_ew.prog.n_ins << " stores=" << (int)split_ew.prog.n_stores
+         << " reductions=" << (int)split_ew.prog.n_reduces;
+      e.desc = de.str();
+      e.ew.desc = e.desc;
+      plan.steps.push_back(e);
+      finalize_reds(reds, (int)plan.steps.size() - 1, split_ew.gx, split_ew.gy, gm.M, gm.N, "%" + f.names[dv]);
+      return;
+    }
     finalize_reds(reds, (int)plan.steps.size() - 1, gx, gy, gm.M, gm.N, "%" + f.names[dv]);
+  }
+
+  // K split factor for a tcgen05 GEMM: the tile grid over the persistent
+  // CTAs (148 SMs; CTA pairs for 256-wide tiles with M >= 512, as the
+  // launcher chooses) leaves the last wave partly idle; splitting K into S
+  // work items per tile is worth it when it raises the busy fraction by > 5
+  // points and every split keeps K/S >= 4096 (DLVM_GEMM_SPLITK=0 disables)
+  static int split_k(const GemmStep& gm) {
+    static const bool on = [] {
+      const char* e = std::getenv("DLVM_GEMM_SPLITK");
+      return !(e && e[0] == '0');
+    }();
+    if (!on || !gm.tensor_core || gm.seg.size() != 1) return 1;
+    const int ctas = (gm.bn == 256 && gm.M >= 512) ? 2 : 1;
+    const int64_t clusters = 148 / ctas;
+    const int64_t tiles = ((gm.M + 128 * ctas - 1) / (128 * ctas)) * ((gm.N + gm.bn - 1) / gm.bn);
+    auto busy = [&](int64_t w) {
+      const int64_t waves = (w + clusters - 1) / clusters;
+      return (double)w / (double)(waves * clusters);
+    };
+    double best = busy(tiles);
+    int bs = 1;
+    for (int S = 2; S <= 4; ++S)
+      if (gm.K / S >= 4096 && busy(tiles * S) > best + 0.05) {
+        best = busy(tiles * S);
+        bs = S;
+      }
+    return bs;
   }
 
   void add_events() {

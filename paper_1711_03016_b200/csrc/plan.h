@@ -99,6 +99,8 @@ struct GemmStep {
   // is one GEMM whose K loop walks both products into one accumulator)
   std::vector<GemmSeg> seg;
   bool tensor_core = false;      // tcgen05 (bf16) vs SIMT (f32/bf16 operands)
+  int ksplit = 1;                // > 1: K split into raw partial tiles, summed by the next EW step
+  int64_t split_bytes = 0;       // byte stride between the partial tiles
   int bm = 128, bn = 128;        // tile shape (partials layout of epilogue reductions)
   EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator
 };
