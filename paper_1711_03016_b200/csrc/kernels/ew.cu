@@ -145,25 +145,54 @@ cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// [rows, cols] f32 / bf16 -> bf16 rows of ld (multiple of 8) elements, zero
+// padded: each thread writes 8 outputs (16 bytes) per step; sources whose
+// rows are 16-byte aligned (bf16: cols % 8 == 0; f32: cols % 4 == 0) move
+// as vectors, the rest element by element
 __global__ void pack_bf16_kernel(const void* __restrict__ src, int src_f32, int64_t rows, int64_t cols,
                                  unsigned short* __restrict__ dst, int64_t ld) {
   pdl_trigger();
   pdl_wait();
-  const int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
-  if (r >= rows) return;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ld; c += (int64_t)gridDim.x * blockDim.x) {
-    unsigned short v = 0;
-    if (c < cols)
-      v = src_f32 ? f2bf(__ldg(reinterpret_cast<const float*>(src) + r * cols + c))
-                  : __ldg(reinterpret_cast<const unsigned short*>(src) + r * cols + c);
-    dst[r * ld + c] = v;
+  const int64_t per_row = ld / 8, total = rows * per_row;
+  const bool vec = src_f32 ? (cols % 4 == 0) : (cols % 8 == 0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per_row, c = (i - r * per_row) * 8;
+    unsigned short v[8];
+    if (vec && c + 8 <= cols) {
+      if (src_f32) {
+        const float4* q = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(src) + r * cols + c);
+        const float4 x0 = __ldg(q), x1 = __ldg(q + 1);
+        v[0] = f2bf(x0.x); v[1] = f2bf(x0.y); v[2] = f2bf(x0.z); v[3] = f2bf(x0.w);
+        v[4] = f2bf(x1.x); v[5] = f2bf(x1.y); v[6] = f2bf(x1.z); v[7] = f2bf(x1.w);
+      } else {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned short*>(src) + r * cols + c));
+        *reinterpret_cast<uint4*>(dst + r * ld + c) = x;
+        continue;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[j] = 0;
+        if (c + j < cols)
+          v[j] = src_f32 ? f2bf(__ldg(reinterpret_cast<const float*>(src) + r * cols + c + j))
+                         : __ldg(reinterpret_cast<const unsigned short*>(src) + r * cols + c + j);
+      }
+    }
+    uint4 o;
+    o.x = (unsigned)v[0] | ((unsigned)v[1] << 16);
+    o.y = (unsigned)v[2] | ((unsigned)v[3] << 16);
+    o.z = (unsigned)v[4] | ((unsigned)v[5] << 16);
+    o.w = (unsigned)v[6] | ((unsigned)v[7] << 16);
+    *reinterpret_cast<uint4*>(dst + r * ld + c) = o;
   }
 }
 
 cudaError_t launch_pack_bf16(const void* src, bool src_f32, int64_t rows, int64_t cols, void* dst, int64_t ld,
                              cudaStream_t stream) {
-  dim3 block(128, 4), grid((unsigned)std::min<int64_t>((ld + 127) / 128, 8), (unsigned)((rows + 3) / 4));
-  LaunchCfg L(grid, block, 0, stream);
+  if (ld % 8) return cudaErrorInvalidValue;
+  const int64_t total = rows * (ld / 8);
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
+  LaunchCfg L(dim3((unsigned)blocks), dim3(256), 0, stream);
   cudaError_t e = cudaLaunchKernelEx(&L.cfg, pack_bf16_kernel, src, src_f32 ? 1 : 0, rows, cols,
                                      reinterpret_cast<unsigned short*>(dst), ld);
   return e != cudaSuccess ? e : cudaGetLastError();
