@@ -550,3 +550,39 @@ def test_A20_kept_loss_bit_equal_bf16(case):
                             1.0 / 256, "bf16", 256)
     res = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
     assert res["grad"][-1] == res["primal"][0]
+
+
+_JIT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import paper_1711_03016_b200 as P, workloads as W
+from helpers import gpu_run
+w = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)])
+r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
+w2 = W.c2(96, 4096)
+r2 = gpu_run(w2.text, w2.fn, w2.grad, w2.inputs(), seed=w2.seed())
+np.savez({out!r}, *(r["primal"] + r["grad"] + r2["primal"] + r2["grad"]))
+print(r["fn"].print(8).count("specialised"))
+"""
+
+
+def test_jit_kernels_bit_identical_to_ahead_of_time(tmp_path):
+    """DLVM_FORCE_JIT=1 compiles every EW / tcgen05 program with NVRTC at
+    create time instead of using the ahead-of-time registry: same templates,
+    same arithmetic -> bit-identical results (c3 bf16 GEMM epilogues, c2 EW)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for force in ("0", "1"):
+        out = str(tmp_path / f"r{force}.npz")
+        script = _JIT_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        env = dict(os.environ, DLVM_FORCE_JIT=force)
+        p = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        if force == "1":
+            assert int(p.stdout.strip().splitlines()[-1]) >= 5  # GEMM epilogues really were JIT-compiled
+        outs[force] = np.load(out)
+    for k in outs["0"].files:
+        np.testing.assert_array_equal(outs["0"][k], outs["1"][k])
