@@ -1315,6 +1315,10 @@ struct Planner {
     int64_t rpt = (R + (int64_t)g.by * want_gy - 1) / ((int64_t)g.by * want_gy);
     g.rpt = (int)std::min<int64_t>(64, std::max<int64_t>(1, rpt));
     g.gy = (R + (int64_t)g.by * g.rpt - 1) / ((int64_t)g.by * g.rpt);
+    if (g.gy > 65535) {  // tall, thin spaces: more rows per thread keep the grid's y extent legal
+      g.rpt = (int)((R + (int64_t)g.by * 65535 - 1) / ((int64_t)g.by * 65535));
+      g.gy = (R + (int64_t)g.by * g.rpt - 1) / ((int64_t)g.by * g.rpt);
+    }
   }
 
   // ------------------------------------------------------------ schedule
@@ -1517,6 +1521,8 @@ struct Planner {
     const int64_t simt_tiles64 = ((gm.M + 63) / 64) * ((gm.N + 63) / 64);
     gm.bm = gm.tensor_core ? 128 : (simt_tiles64 < 2 * 148 ? 32 : 64);
     gm.bn = gm.tensor_core ? (gm.N >= 256 ? 256 : 128) : 64;
+    if (!gm.tensor_core && (gm.M + gm.bm - 1) / gm.bm > 65535)
+      unsupported("SIMT dot with more than 65535 row tiles (over 4M rows under the fp32 dot policy)");
     Node epi;
     if (n.fused_epilogue >= 0) epi = nodes[n.fused_epilogue];
     epi.shape = ty(dv).shape;

@@ -398,3 +398,17 @@ def test_kernel_templates_compile_under_nvrtc():
     for e in exprs:
         _, low = nvrtc.nvrtcGetLoweredName(p, e.encode())
         assert low and low.startswith(b"_ZN4dlvm4kern")
+
+
+def test_tall_thin_launch_grids_stay_legal():
+    """Element-wise groups over very tall, thin spaces ([2^28, 1]) raise rows
+    per thread so the grid's y extent stays <= 65535 (CUDA limit)."""
+    import re as _re
+    for R in (1 << 22, 1 << 26, 1 << 28):
+        w = W.c2(R, 1)
+        f = _plan_only(w.text, w.fn, w.grad)
+        assert "unsupported" not in f.print(3)
+    w = W.c2(1 << 28, 1)
+    f = _plan_only(w.text, w.fn, w.grad)
+    counts = [int(x) for x in _re.findall(r"\((\d+) partials", f.print(3))]
+    assert counts and max(counts) <= 65535, counts  # one partial per grid row block
