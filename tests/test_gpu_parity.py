@@ -621,3 +621,35 @@ def test_c2_tall_thin_column():
     assert_f32_parity(db.cpu().numpy(), a1.sum(keepdims=True).reshape(1, 1), np.abs(a1).sum().reshape(1, 1), what="db")
     t = a1 * x64
     assert_f32_parity(dw.cpu().numpy(), t.sum().reshape(1, 1), np.abs(t).sum().reshape(1, 1), what="dw")
+
+
+_TMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+w = W.c2(300, 4096)
+r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed())
+np.savez({out!r}, *(r["primal"] + r["grad"]))
+"""
+
+
+def test_tma_staged_ew_kernel_bit_identical(tmp_path):
+    """The opt-in TMA-staged element-wise kernel (DLVM_EW_TMA=1: cp.async.bulk
+    ring, producer/consumer warps) computes the same program in the same row
+    order per column as ew2d_kernel: bit-identical c2 forward and adjoint,
+    including the column-sum partials."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tma in ("0", "1"):
+        out = str(tmp_path / f"t{tma}.npz")
+        script = _TMA_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_EW_TMA=tma),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        outs[tma] = np.load(out)
+    for k in outs["0"].files:
+        np.testing.assert_array_equal(outs["0"][k], outs["1"][k])
