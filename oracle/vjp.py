@@ -100,15 +100,28 @@ def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray], do
 
 
 def reverse_sweep(src: Function, env: Dict[str, np.ndarray], out_index: int,
-                  seed: np.ndarray, dot_policy=None) -> Dict[str, np.ndarray]:
-    """Adjoints of every value that the selected output depends on."""
+                  seed: np.ndarray, dot_policy=None, wrt: Optional[Sequence[int]] = None) -> Dict[str, np.ndarray]:
+    """Adjoints of every value that the selected output depends on.  With
+    `wrt`, only values that depend on those arguments (forward activity, as
+    adjoint.py does) get adjoints: the others never reach a `wrt` gradient,
+    and may be computed by ops without a derivative rule (`reduce ... by
+    multiply`; reading A24)."""
     adj: Dict[str, np.ndarray] = {}
 
     def is_float(name: str) -> bool:
         t = src.types[name]
         return t.dtype in FLOAT_DTYPES
 
+    active = None
+    if wrt is not None:
+        active = {src.param_names[i] for i in wrt}
+        for ins in src.insts:
+            if is_float(ins.result) and any(o.kind == "value" and o.name in active for o in ins.operands):
+                active.add(ins.result)
+
     def acc(name: str, c: np.ndarray):
+        if active is not None and name not in active:
+            return
         c = unbroadcast(c, src.types[name].shape)
         adj[name] = adj[name] + c if name in adj else c
 
@@ -137,8 +150,8 @@ def grad(src: Function, inputs: Sequence, wrt: Optional[Sequence[int]] = None,
     if seed is None:
         seed = np.ones(src.result_types[from_].shape, dtype=np.float64)
     seed = np.asarray(seed, dtype=np.float64).reshape(src.result_types[from_].shape)
-    adj = reverse_sweep(src, env, from_, seed, dot_policy)
     wrt = list(range(len(src.param_types))) if wrt is None else list(wrt)
+    adj = reverse_sweep(src, env, from_, seed, dot_policy, wrt)
     res = []
     for i in wrt:
         n = src.param_names[i]

@@ -117,8 +117,14 @@ __device__ __forceinline__ void vm_load(const EwDevIn& in, int64_t off, int64_t 
   if (in.nchunks > 1) {
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      float s = 0.f;
-      for (int k = 0; k < in.nchunks; ++k) s = __fadd_rn(s, ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st));
+      float s;
+      if (in.chunk_mul) {  // product over the reduced axis, in index order
+        s = 1.f;
+        for (int k = 0; k < in.nchunks; ++k) s = __fmul_rn(s, ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st));
+      } else {
+        s = 0.f;
+        for (int k = 0; k < in.nchunks; ++k) s = __fadd_rn(s, ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st));
+      }
       v[j] = s;
     }
     return;

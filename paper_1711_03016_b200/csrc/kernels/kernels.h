@@ -10,13 +10,15 @@
 namespace dlvm {
 
 // one program input: element (i_0..i_{n-1}) at ptr + sum_d i_d * s[d]
-// (+ k * chunk_stride summed over k < nchunks for reduction partials)
+// (+ k * chunk_stride summed over k < nchunks for reduction partials;
+// multiplied in k order instead when chunk_mul: `reduce ... by multiply`)
 struct EwDevIn {
   const void* ptr;
   int64_t s[kMaxIterDims];
   int64_t chunk_stride;
   int32_t nchunks;
   uint8_t st;  // SType
+  uint8_t chunk_mul;
 };
 
 struct EwDevOut {

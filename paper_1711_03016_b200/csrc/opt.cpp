@@ -158,8 +158,12 @@ struct Optimizer {
           }
           break;
         case Op::Reduce:
-          if (in.ops[0].is_lit() && !in.reduce_mul) {  // sum of n copies
-            rauw(r, L(in.ops[0].lit * (double)in.ops[0].type.shape[in.axis], rt));
+          if (in.ops[0].is_lit()) {  // sum / product of n copies
+            const int64_t n = in.ops[0].type.shape[in.axis];
+            double x = in.reduce_mul ? 1.0 : in.ops[0].lit * (double)n;
+            if (in.reduce_mul)
+              for (int64_t k = 0; k < n; ++k) x *= in.ops[0].lit;
+            rauw(r, L(x, rt));
             changed = true;
           }
           break;

@@ -125,6 +125,7 @@ struct VInfo {
   bool inl = false;        // element-wise/view value recomputed in registers
   bool dead = false;       // fused away (inner reduce of a chain)
   bool dot_use = false;    // operand of a dot (through views)
+  bool prod_use = false;   // operand of a `reduce ... by multiply` (through views)
   bool group_use = false;  // read by an element-wise kernel
   std::vector<Home> homes; // materialised copies
   int out_home = -1;       // output index this value is produced into directly
@@ -142,7 +143,8 @@ struct Root {
 };
 
 struct Node {
-  bool is_dot = false;
+  bool is_dot = false;         // an opaque node reading materialised operands: a dot,
+  bool is_prod = false;        // or (is_prod) a `reduce ... by multiply`
   int dot_inst = -1;
   std::vector<int64_t> shape;  // iteration shape
   std::vector<int> perm;       // iteration dim i <- reduced-operand dim perm[i] (reduce nodes)
@@ -183,13 +185,14 @@ struct Planner {
     return in && (in->op == Op::Transpose || in->op == Op::ShapeCast || in->op == Op::Slice);
   }
   static bool is_dotlike(Op op) { return op == Op::Dot || op == Op::DotSum; }
+  static bool is_prod(const Inst* in) { return in && in->op == Op::Reduce && in->reduce_mul; }
   static bool is_ew(const Inst* in) {
     return in && (is_elementwise(in->op) || in->op == Op::Sech2 || in->op == Op::DataTypeCast);
   }
   bool produced(int v) const {
     const Inst* in = def(v);
     if (!in || vi[v].dead) return false;
-    return is_dotlike(in->op) || (in->op == Op::Reduce && red_root.count(v)) || vi[v].mat;
+    return is_dotlike(in->op) || is_prod(in) || (in->op == Op::Reduce && red_root.count(v)) || vi[v].mat;
   }
   SType natural(int v) const { return ty(v).dtype == DType::Bool ? SType::U8 : SType::F32; }
 
@@ -203,7 +206,6 @@ struct Planner {
       if (f.types[i].rank() > kPlanDims) unsupported("rank > 8 tensors are not supported");
     }
     for (auto& in : f.insts) {
-      if (in.op == Op::Reduce && in.reduce_mul) unsupported("'reduce by multiply' is not supported on the GPU path");
       if (in.op == Op::DataTypeCast && !((in.cast_to == DType::F32 || in.cast_to == DType::Bool)))
         unsupported("dataTypeCast target");
       for (auto& o : in.ops)
@@ -305,14 +307,15 @@ struct Planner {
     for (size_t k = 0; k < f.ret.size(); ++k)
       if (!f.ret[k].is_lit()) vi[f.ret[k].value].outs.push_back((int)k);
     for (auto& in : f.insts) {
-      if (!is_dotlike(in.op)) continue;
+      const bool prod = is_prod(&in);
+      if (!is_dotlike(in.op) && !prod) continue;
       for (auto& o : in.ops) {
         if (o.is_lit()) continue;
         int v = o.value;
-        vi[v].dot_use = true;
+        (prod ? vi[v].prod_use : vi[v].dot_use) = true;
         while (is_view(def(v))) {
           v = def(v)->ops[0].value;
-          vi[v].dot_use = true;
+          (prod ? vi[v].prod_use : vi[v].dot_use) = true;
         }
       }
     }
@@ -322,6 +325,7 @@ struct Planner {
     for (auto& in : f.insts) {
       if (in.op != Op::Reduce) continue;
       if (in.ops[0].is_lit()) unsupported("reduce of a literal");
+      if (in.reduce_mul) continue;  // its own step (emit_prod), never chained into a sum
       int x = in.ops[0].value;
       auto it = red_root.find(x);
       if (it != red_root.end() && vi[x].users.size() == 1 && vi[x].outs.empty()) {
@@ -425,7 +429,7 @@ struct Planner {
       const Inst* in = def((int)v);
       if (!in || x.dead) continue;
       if (is_ew(in)) {
-        x.mat = !x.outs.empty() || x.dot_use || force_mat.count((int)v) || opt.no_fusion;
+        x.mat = !x.outs.empty() || x.dot_use || x.prod_use || force_mat.count((int)v) || opt.no_fusion;
         x.inl = !x.mat;
       } else if (is_view(in)) {
         x.mat = force_mat.count((int)v) > 0;
@@ -480,8 +484,9 @@ struct Planner {
       Node n;
       n.pos = (int)k;
       n.writes.insert(v);
-      if (is_dotlike(in.op)) {
+      if (is_dotlike(in.op) || is_prod(&in)) {
         n.is_dot = true;
+        n.is_prod = is_prod(&in);
         n.dot_inst = (int)k;
       } else if (in.op == Op::Reduce && red_root.count(v)) {
         auto [x, axes] = red_root[v];
@@ -781,7 +786,7 @@ struct Planner {
   void fuse_epilogues() {
     if (opt.no_fusion) return;
     for (size_t d = 0; d < nodes.size(); ++d) {
-      if (!nodes[d].is_dot) continue;
+      if (!nodes[d].is_dot || nodes[d].is_prod) continue;
       int dv = f.insts[nodes[d].dot_inst].result;
       for (size_t g = 0; g < nodes.size(); ++g) {
         Node& G = nodes[g];
@@ -899,7 +904,7 @@ struct Planner {
       } else {
         others_read = x.group_use;
       }
-      bool need32 = others_read || !x.outs.empty() || x.out_home >= 0 ||
+      bool need32 = others_read || !x.outs.empty() || x.out_home >= 0 || x.prod_use ||
                     (x.dot_use && opt.policy == Policy::F32);
       if (x.out_home >= 0) {
         x.homes.push_back(make_home(output_buf(x.out_home), (int)v,
@@ -1436,7 +1441,8 @@ struct Planner {
     for (int ni : order) {
       Node& n = nodes[ni];
       if (n.is_dot) {
-        emit_gemm(n);
+        if (n.is_prod) emit_prod(n);
+        else emit_gemm(n);
         continue;
       }
       Step s;
@@ -1479,6 +1485,56 @@ struct Planner {
     plan.workspace_bytes = (plan.workspace_bytes + 255) / 256 * 256;
     plan.n_inputs = plan.seed_is_input ? f.num_args() - 1 : f.num_args();
     plan.n_outputs = (int)f.ret.size();
+  }
+
+  // `reduce %x by multiply along a` (Table 1; forward only):
+  // an element-wise step over the result's index space whose one input walks
+  // the reduced axis as nchunks = shape[a] chunks at the axis stride,
+  // multiplied in index order by the load (chunk_mul), then stored to every
+  // home of the result.  Its consumers read those homes.
+  void emit_prod(Node& n) {
+    const Inst& in = f.insts[n.dot_inst];
+    const int v = in.result, x = in.ops[0].value;
+    TensorRef r;
+    if (!ref_of(x, false, &r)) unsupported("reduce operand not addressable");
+    const int rx = ty(x).rank();
+    Step s;
+    s.kind = Step::EW;
+    EwGroup& g = s.ew;
+    IterRef it;
+    it.buf = r.buf;
+    it.offset = r.offset;
+    it.st = r.st;
+    it.nchunks = (int)r.shape[in.axis];
+    it.chunk_stride = r.strides[in.axis];
+    it.chunk_mul = true;
+    for (int d = 0, j = 0; d < rx; ++d)
+      if (d != in.axis) it.strides[j++] = r.strides[d];
+    g.inputs.push_back(it);
+    g.prog.n_in = 1;
+    const int rk = ty(v).rank();
+    for (auto& h : vi[v].homes) {
+      if ((int)g.stores.size() >= kMaxStores) unsupported("too many stores in one fused kernel");
+      IterRef o = store_ref(h.ref, identity(rk));
+      o.st = h.st;
+      g.prog.store_slot[g.stores.size()] = 0;
+      g.stores.push_back(o);
+    }
+    g.prog.n_stores = (uint8_t)g.stores.size();
+    std::vector<int64_t> shape = ty(v).shape;
+    if (shape.empty()) shape = {1};
+    collapse(g, shape, -1);
+    rows_of_long_1d(g);
+    ew_launch(g);
+    g.sig = program_signature(g.prog);
+    std::ostringstream d;
+    d << "ew [";
+    for (int k = 0; k < g.ndims; ++k) d << (k ? "," : "") << g.dims[k];
+    d << "] vec" << g.vec << " product of %" << f.names[x] << " along " << in.axis << " (" << it.nchunks
+      << " factors) -> %" << f.names[v];
+    s.desc = d.str();
+    g.desc = s.desc;
+    plan.steps.push_back(s);
   }
 
   void emit_gemm(Node& n) {

@@ -59,6 +59,7 @@ struct IterRef {
   int64_t strides[kPlanDims] = {0, 0, 0, 0, 0, 0, 0, 0};  // per iteration dim
   int nchunks = 1;
   int64_t chunk_stride = 0;
+  bool chunk_mul = false;        // chunks multiplied in order (`reduce ... by multiply`), else summed
   SType st = SType::F32;
   // reductions with a single partial: the value's f32 home, which the
   // producer writes directly when that buffer is bound as f32 at run time

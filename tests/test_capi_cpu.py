@@ -412,3 +412,23 @@ def test_tall_thin_launch_grids_stay_legal():
     f = _plan_only(w.text, w.fn, w.grad)
     counts = [int(x) for x in _re.findall(r"\((\d+) partials", f.print(3))]
     assert counts and max(counts) <= 65535, counts  # one partial per grid row block
+
+
+def test_reduce_multiply_plans_one_product_step():
+    """`reduce ... by multiply` (Table 1, forward only): its operand is
+    materialised and the product is one element-wise step whose input walks
+    the reduced axis (chunked load, multiplied in order); the sum over a
+    product and later element-wise consumers plan as usual."""
+    import prod_programs as PP
+    f = _plan_only(PP.prod_chain(40, 24), "f")
+    plan = f.print(2)
+    assert "unsupported" not in plan, plan
+    assert plan.count("product of") == 3, plan
+    assert "(40 factors)" in plan and "(24 factors)" in plan and "(3 factors)" in plan, plan
+    g = _plan_only(PP.prod_grad(16, 8), "f", "g")
+    assert g.print(3).count("product of") == 1, g.print(3)
+    # a product of a splat literal folds at create time
+    t = ('module "m"\nstage raw\nfunc @f: (<4 x f32>) -> <4 x f32> {\n\'entry(%a: <4 x f32>):\n'
+         '    %r = reduce 2: <3 x 4 x f32> by multiply along 0\n    %s = multiply %a: <4 x f32>, %r: <4 x f32>\n'
+         '    return %s: <4 x f32>\n}\n')
+    assert "product of" not in _plan_only(t, "f").print(2)

@@ -431,3 +431,36 @@ def test_bf16_policy_dot_exact_on_bf16_inputs():
     c = a + 1e-3  # not bf16-representable: the policy result differs from the exact one
     assert not np.array_equal(oracle.run(m, "f", [c, b], dot_policy="bf16")[0], c @ b)
     np.testing.assert_array_equal(oracle.run(m, "f", [c, b], dot_policy="bf16")[0], bf16_round(c) @ b)
+
+
+def _prod_module(shape, axis):
+    rt = [d for k, d in enumerate(shape) if k != axis]
+    T = lambda s: "<" + " x ".join(str(d) for d in s) + " x f32>" if s else "f32"
+    return oracle.parse(f'module "m"\nstage raw\nfunc @f: ({T(shape)}) -> {T(rt)} {{\n'
+                        f"'entry(%a: {T(shape)}):\n"
+                        f"    %r = reduce %a: {T(shape)} by multiply along {axis}\n"
+                        f"    return %r: {T(rt)}\n}}\n")
+
+
+def test_reduce_multiply_forward_pins():
+    """`reduce ... by multiply along d` (Table 1): the product
+    over axis d, axis removed.  Pinned by hand-computed values, brute force
+    over indices, and the identity prod(exp x) = exp(sum x) along the axis."""
+    a = np.array([[1.0, 2.0, 3.0], [4.0, 5.0, 6.0]])
+    np.testing.assert_array_equal(oracle.run(_prod_module((2, 3), 0), "f", [a])[0], [4.0, 10.0, 18.0])
+    np.testing.assert_array_equal(oracle.run(_prod_module((2, 3), 1), "f", [a])[0], [6.0, 120.0])
+    assert float(oracle.run(_prod_module((4,), 0), "f", [np.array([1.5, -2.0, 0.5, 4.0])])[0]) == -6.0
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (3, 4, 5))
+    for ax in range(3):
+        got = oracle.run(_prod_module(x.shape, ax), "f", [x])[0]
+        rest = [d for k, d in enumerate(x.shape) if k != ax]
+        for idx in itertools.product(*[range(d) for d in rest]):
+            p = 1.0
+            for t in range(x.shape[ax]):
+                full = list(idx)
+                full.insert(ax, t)
+                p *= x[tuple(full)]
+            assert got[idx] == pytest.approx(p, rel=1e-14, abs=0)
+        e = oracle.run(_prod_module(x.shape, ax), "f", [np.exp(x)])[0]
+        np.testing.assert_allclose(e, np.exp(x.sum(axis=ax)), rtol=1e-13)
