@@ -115,8 +115,11 @@ dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_
  * signatures of the primal (4) / gradient (5) launches (one per line, the
  * keys of the compile-time specialisations), the optimised primal (6) /
  * gradient (7) that the plans execute (identical to 0/1 with DLVM_NO_OPT),
- * or (8) the kernels specialised at create time by NVRTC (one line each:
- * plan, step, status, instantiation).  Writes at most `cap` bytes
+ * (8) the kernels specialised at create time by NVRTC (one line each:
+ * plan, step, status, instantiation), or the detailed plan of the primal (9)
+ * / gradient (10): buffers, then every step's iteration space, launch shape,
+ * program signature and operand refs (buffer, offset, strides, chunks).
+ * Writes at most `cap` bytes
  * including the NUL; *needed receives the full size including the NUL. */
 dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);
 

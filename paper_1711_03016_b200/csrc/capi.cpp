@@ -524,8 +524,15 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
       case 8:
         s = fn->jit_report;
         break;
+      case 9:
+      case 10: {
+        int w = which - 9;
+        if (w == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        s = fn->planned[w] ? fn->plan[w].detail() : "unsupported: " + fn->plan_error[w] + "\n";
+        break;
+      }
       default:
-        return fail(DLVM_ERR_USAGE, "which must be 0..8");
+        return fail(DLVM_ERR_USAGE, "which must be 0..10");
     }
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());

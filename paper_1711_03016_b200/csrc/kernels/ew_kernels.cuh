@@ -1,5 +1,5 @@
 // Element-wise program kernel (K1/K2/K3/K7/K8 of SURVEY.md §2.5): one pass
-// over an [R, C] iteration space (R = product of up to three row dims)
+// over an [R, C] iteration space (R = product of up to kMaxIterDims - 1 row dims)
 // evaluating a fused chain of the IR's element-wise ops with broadcasting
 // ("fuse compatible element-wise operators to a single
 // kernel"; P:L213 broadcasting), storing results and producing
@@ -61,9 +61,16 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
   for (int d = 0; d < nd; ++d) (d < nrd ? R : C) *= p.dims[d];
   const int64_t c = ((int64_t)blockIdx.x * bx + tx) * VEC;
   const bool cval = c < C;
-  const int64_t c_hi = p.ncols == 2 ? c / p.dims[nd - 1] : 0, c_lo = p.ncols == 2 ? c % p.dims[nd - 1] : c;
-  // element offset of column c for strides s (two column dims only with VEC == 1)
-  auto col_off = [&](const int64_t* s) -> int64_t { return c_lo * s[nd - 1] + (p.ncols == 2 ? c_hi * s[nd - 2] : 0); };
+  // element offset of column c for strides s (several column dims only with VEC == 1)
+  auto col_off = [&](const int64_t* s) -> int64_t {
+    if (p.ncols == 1) return c * s[nd - 1];
+    int64_t off = 0, cc = c;
+    for (int d = nd - 1; d >= nrd; --d) {
+      off += (cc % p.dims[d]) * s[d];
+      cc /= p.dims[d];
+    }
+    return off;
+  };
   const int n_in = SPEC ? 0 : Pg.n_in;
   float v[NS][VEC];
   if constexpr (SPEC) {

@@ -18,7 +18,7 @@
 
 namespace dlvm {
 
-constexpr int kMaxIterDims = 4;
+constexpr int kMaxIterDims = 6;  // rank <= 5 with any broadcast pattern (+ a unit column)
 constexpr int kMaxIn = 12;
 constexpr int kMaxLits = 12;
 constexpr int kMaxIns = 40;

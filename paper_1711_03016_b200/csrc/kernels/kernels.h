@@ -29,7 +29,7 @@ struct EwDevOut {
 
 struct EwParams {
   int32_t ndims;
-  int32_t ncols;   // trailing dims forming the column index (1, or 2 when they do not collapse)
+  int32_t ncols;   // trailing dims forming the column index (1, or more when they do not collapse)
   int32_t vec;     // 1 or 4 elements per thread along the column dim
   int32_t rpt;     // rows per thread (EW kernel)
   int64_t dims[kMaxIterDims];

@@ -69,6 +69,45 @@ std::string Plan::str() const {
 }
 
 namespace {
+void print_group(std::ostringstream& o, const EwGroup& g) {
+  o << "    space [";
+  for (int d = 0; d < g.ndims; ++d) o << (d ? "," : "") << g.dims[d];
+  o << "] ncols " << g.ncols << " vec " << g.vec << " block " << g.bx << "x" << g.by << " rpt " << g.rpt << " grid "
+    << g.gx << "x" << g.gy << "  prog " << g.sig << "\n";
+  auto ref = [&](const char* what, size_t k, const IterRef& r) {
+    o << "    " << what << k << ": buf " << r.buf << " +" << r.offset << " strides [";
+    for (int d = 0; d < g.ndims; ++d) o << (d ? "," : "") << r.strides[d];
+    o << "] st " << (int)r.st;
+    if (r.nchunks != 1) o << " chunks " << r.nchunks << "x" << r.chunk_stride << (r.chunk_mul ? " (product)" : "");
+    if (r.direct_buf >= 0) o << " direct buf " << r.direct_buf;
+    o << "\n";
+  };
+  for (size_t k = 0; k < g.inputs.size(); ++k) ref("in", k, g.inputs[k]);
+  for (size_t k = 0; k < g.stores.size(); ++k) ref("store", k, g.stores[k]);
+  for (size_t k = 0; k < g.reduces.size(); ++k) ref("reduce", k, g.reduces[k]);
+}
+}  // namespace
+
+std::string Plan::detail() const {
+  std::ostringstream o;
+  o << str() << "buffers:\n";
+  for (size_t b = 0; b < bufs.size(); ++b) {
+    const BufferSlot& x = bufs[b];
+    static const char* kinds[] = {"input", "output", "seed", "work"};
+    o << "  buf " << b << ": " << kinds[(int)x.kind] << " " << x.index << " bytes " << x.bytes << " st " << (int)x.st;
+    if (x.kind == BufferSlot::Work) o << " offset " << x.offset;
+    o << "\n";
+  }
+  for (size_t i = 0; i < steps.size(); ++i) {
+    const Step& s = steps[i];
+    o << "  [" << i << "] " << s.desc << "\n";
+    if (s.kind == Step::EW) print_group(o, s.ew);
+    if (s.kind == Step::GEMM) print_group(o, s.gemm.epi);
+  }
+  return o.str();
+}
+
+namespace {
 
 std::vector<int64_t> contig_strides(const std::vector<int64_t>& shape) {
   std::vector<int64_t> st(shape.size());
@@ -1041,7 +1080,10 @@ struct Planner {
       if (inline_it && is_view(in)) {
         int src = in->ops[0].value;
         Map ma;
-        if (P.vi[src].inl && P.view_map(*in, m, &ma)) return node(src, ma);
+        // through the view to an inlined source, or to a value this group
+        // stores (computed in registers: merge_groups lets a group read its
+        // own stores only at the identity map, so a load would race the store)
+        if ((P.vi[src].inl || stored.count(src)) && P.view_map(*in, m, &ma)) return node(src, ma);
         TensorRef sr, r;
         if (!P.ref_of(src, false, &sr) || !P.view_ref(*in, sr, &r))
           unsupported("cannot address view %" + P.f.names[v]);
@@ -1211,7 +1253,7 @@ struct Planner {
     g.reduces.assign(red_slots.size(), IterRef{});
   }
 
-  // collapse the iteration space to <= 4 dims: row dims + one column dim
+  // collapse the iteration space to <= kMaxIterDims dims: row dims + one column dim
   void collapse(EwGroup& g, std::vector<int64_t> dims, int split) {
     int r = (int)dims.size();
     std::vector<std::vector<int64_t>> in_s(g.inputs.size()), st_s(g.stores.size());
@@ -1252,8 +1294,7 @@ struct Planner {
       for (auto* s : refs) s->push_back(0);
       n_col = 1;
     }
-    if (n_col > 2) unsupported("reduction over a strided column space of more than 2 dims");
-    if ((int)dims.size() > kMaxIterDims) unsupported("iteration space does not collapse to 4 dims");
+    if ((int)dims.size() > kMaxIterDims) unsupported("iteration space does not collapse to " + std::to_string(kMaxIterDims) + " dims");
     g.ndims = (int)dims.size();
     g.ncols = n_col;
     for (int d = 0; d < kMaxIterDims; ++d) g.dims[d] = d < g.ndims ? dims[d] : 1;
@@ -1456,10 +1497,9 @@ struct Planner {
       if (reds.empty() || only_all) split = -1;
       if (shape.empty()) shape = {1};
       collapse(s.ew, shape, split);
-      for (auto& ri : reds) {  // kinds in the collapsed space
-        if (s.ew.ndims == 1 && ri.kind == RED_COL) ri.kind = RED_ALL;
-        s.ew.prog.reduce_kind[ri.slot_index] = ri.kind;
-      }
+      // kinds in the collapsed space.  A column reduction whose row dims were
+      // all unit (erased) keeps its kind: R = 1, one partial per column.
+      for (auto& ri : reds) s.ew.prog.reduce_kind[ri.slot_index] = ri.kind;
       rows_of_long_1d(s.ew);
       ew_launch(s.ew);
       s.ew.sig = program_signature(s.ew.prog);
@@ -1771,6 +1811,37 @@ struct Planner {
     fuse_epilogues();
     assign_homes();
     emit_steps(schedule());
+    check_no_self_reads();
+  }
+
+  // every launch reads only buffers it does not write: a load of a value the
+  // same launch stores would race the store (another thread's, or its own
+  // later in program order)
+  void check_no_self_reads() const {
+    for (size_t i = 0; i < plan.steps.size(); ++i) {
+      const Step& s = plan.steps[i];
+      const EwGroup* g = s.kind == Step::EW ? &s.ew : s.kind == Step::GEMM ? &s.gemm.epi : nullptr;
+      if (!g) continue;
+      std::set<int> w;
+      for (auto& r : g->stores) w.insert(r.buf);
+      for (auto& r : g->reduces) {
+        w.insert(r.buf);
+        if (r.direct_buf >= 0) w.insert(r.direct_buf);
+      }
+      std::vector<int> rd;
+      for (auto& r : g->inputs)
+        if (r.buf >= 0) rd.push_back(r.buf);
+      if (s.kind == Step::GEMM)
+        for (auto& sg : s.gemm.seg) {
+          rd.push_back(sg.a.buf);
+          rd.push_back(sg.b.buf);
+        }
+      for (int b : rd)
+        if (w.count(b))
+          throw Error(kStatusRuntime, 0, 0,
+                      "planner: step " + std::to_string(i) + " (" + s.desc + ") reads buffer " + std::to_string(b) +
+                          " that it writes");
+    }
   }
 };
 

@@ -70,8 +70,9 @@ struct EwGroup {
   // iteration space, row-major: dims[0..ndims-2] are "row" dims, dims[ndims-1]
   // is the column dim (ndims <= kMaxIterDims).
   int ndims = 1;
-  int ncols = 1;                 // trailing dims forming the column index (1 or 2)
-  int64_t dims[kMaxIterDims] = {1, 1, 1, 1};
+  int ncols = 1;                 // trailing dims forming the column index (1, or more when they do not collapse)
+  int64_t dims[kMaxIterDims] = {1, 1, 1, 1, 1, 1};
+  static_assert(kMaxIterDims == 6, "initialise every dim to 1");
   // launch shape (fixed at plan time: it determines the partials layout)
   int vec = 1, bx = 32, by = 8, rpt = 1;
   int64_t gx = 1, gy = 1;
@@ -138,6 +139,7 @@ struct Plan {
   std::vector<int> input_bf16_ok;  // per input: 1 if it may be passed as bf16 (see make_plan)
   int launches() const;
   std::string str() const;
+  std::string detail() const;  // str() + buffers and every step's operand refs
 };
 
 struct PlanOptions {

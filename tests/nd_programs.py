@@ -1,0 +1,104 @@
+"""Random rank-1..5 straight-line programs (test corpus): NumPy
+broadcasting between operands of different ranks and unit dims (reading
+A1), full-reversal transposes of rank > 2 (Table 1), reductions along
+random axes re-broadcast through shapeCast (L173, L181), compare/select, and
+a scalar loss; gradient w.r.t. every argument.  Shared by the CPU (types,
+AD, plan) and GPU (parity) tests; holds no arithmetic of the method."""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def T(s):
+    return "<" + " x ".join(str(d) for d in s) + " x f32>" if s else "f32"
+
+
+def TB(s):
+    return "<" + " x ".join(str(d) for d in s) + " x bool>"
+
+
+def bcast_shape(rng, S):
+    """A shape that broadcasts to S: some dims set to 1, some leading dims dropped."""
+    s = [1 if rng.random() < 0.5 else d for d in S]
+    drop = int(rng.integers(0, len(S)))
+    return tuple(s[drop:])
+
+
+def nd_program(rng, max_elems=6000, all_values=False):
+    """(text, args); with all_values the primal returns every f32 value it
+    defines (a tuple, no gradient declaration) instead of the loss."""
+    r = int(rng.integers(1, 6))
+    while True:
+        S = [int(rng.integers(1, 6)) for _ in range(r)]
+        S[int(rng.integers(r))] = int(rng.integers(8, 41))  # one long dim: several tiles and a ragged tail
+        if int(np.prod(S)) <= max_elems:
+            break
+    S = tuple(S)
+    RS = tuple(reversed(S))
+    args = [("x", S), ("b1", bcast_shape(rng, S)), ("b2", bcast_shape(rng, S)), ("y", S)]
+    L, vals, cur, k = [], [], "%x", 0
+
+    def d(name, rhs, shape):  # one definition of an f32 value
+        L.append(f"    {name} = {rhs}")
+        vals.append((name, shape))
+
+    def other():
+        c = int(rng.integers(4))
+        return [f"%b1: {T(args[1][1])}", f"%b2: {T(args[2][1])}", "0.3: f32", f"%y: {T(S)}"][c]
+
+    for _ in range(int(rng.integers(4, 9))):
+        kind = ["bin", "bin_rev", "unary", "transpose", "reduce", "select"][int(rng.integers(6))]
+        k += 1
+        i = k
+        if kind in ("bin", "bin_rev"):
+            op = ["add", "subtract", "multiply"][int(rng.integers(3))]
+            a, b = f"{cur}: {T(S)}", other()
+            if kind == "bin_rev":
+                a, b = b, a
+            d(f"%t{i}", f"{op} {a}, {b}", S)
+        elif kind == "unary":
+            op = ["tanh", "negate", "sigmoid"][int(rng.integers(3))]
+            if op == "sigmoid":
+                d(f"%n{i}", f"negate {cur}: {T(S)}", S)
+                d(f"%e{i}", f"exp %n{i}: {T(S)}", S)
+                d(f"%d{i}", f"add %e{i}: {T(S)}, 1: f32", S)
+                d(f"%t{i}", f"divide 1: f32, %d{i}: {T(S)}", S)
+            else:
+                d(f"%t{i}", f"{op} {cur}: {T(S)}", S)
+        elif kind == "transpose":  # (cur^T * y^T)^T: a rank-r reversal and back
+            d(f"%p{i}", f"transpose {cur}: {T(S)}", RS)
+            d(f"%q{i}", f"transpose %y: {T(S)}", RS)
+            d(f"%m{i}", f"multiply %p{i}: {T(RS)}, %q{i}: {T(RS)}", RS)
+            d(f"%t{i}", f"transpose %m{i}: {T(RS)}", S)
+        elif kind == "reduce":  # cur + 0.1 * shapeCast(sum_a cur) (keepdims broadcast)
+            a = int(rng.integers(r))
+            RSH = tuple(dd for j, dd in enumerate(S) if j != a)
+            KS = tuple(1 if j == a else dd for j, dd in enumerate(S))
+            d(f"%r{i}", f"reduce {cur}: {T(S)} by add along {a}", RSH)
+            d(f"%k{i}", f"shapeCast %r{i}: {T(RSH)} to {' x '.join(map(str, KS))}", KS)
+            d(f"%s{i}", f"multiply %k{i}: {T(KS)}, 0.1: f32", KS)
+            d(f"%t{i}", f"add {cur}: {T(S)}, %s{i}: {T(KS)}", S)
+        else:  # relu-like select against a broadcast threshold
+            L.append(f"    %c{i} = gt {cur}: {T(S)}, {other()}")
+            d(f"%t{i}", f"select %c{i}: {TB(S)}, {cur}: {T(S)}, %b1: {T(args[1][1])}", S)
+        cur = f"%t{i}"
+    d("%sq", f"multiply {cur}: {T(S)}, {cur}: {T(S)}", S)
+    sh, v = list(S), "%sq"
+    for j in range(r):
+        d(f"%z{j}", f"reduce {v}: {T(tuple(sh))} by add along 0", tuple(sh[1:]))
+        v, sh = f"%z{j}", sh[1:]
+    sig = ", ".join(T(s) for _, s in args)
+    entry = "'entry(" + ", ".join(f"%{n}: {T(s)}" for n, s in args) + "):"
+    if all_values:
+        rtys = ", ".join(T(s) for _, s in vals)
+        rets = ", ".join(f"{n}: {T(s)}" for n, s in vals)
+        head = ['module "nd"', "stage raw", f"func @f: ({sig}) -> ({rtys}) {{", entry]
+        return "\n".join(head + L + [f"    return ({rets})", "}", ""]), args
+    head = ['module "nd"', "stage raw", f"func @f: ({sig}) -> f32 {{", entry]
+    tail = [f"    return {v}: f32", "}", "", "[gradient @f]", f"func @g: ({sig}) -> ({sig})", ""]
+    return "\n".join(head + L + tail), args
+
+
+def nd_inputs(rng, args):
+    return [rng.uniform(-1, 1, s).astype(np.float32) for _, s in args]

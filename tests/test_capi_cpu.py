@@ -432,3 +432,24 @@ def test_reduce_multiply_plans_one_product_step():
          '    %r = reduce 2: <3 x 4 x f32> by multiply along 0\n    %s = multiply %a: <4 x f32>, %r: <4 x f32>\n'
          '    return %s: <4 x f32>\n}\n')
     assert "product of" not in _plan_only(t, "f").print(2)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_nd_programs_types_ad_and_plan(seed):
+    """Rank-1..5 programs with NumPy broadcasting across ranks, rank>2
+    transposes and reductions along random axes: the C++ types match the
+    oracle's, the C++ adjoint IR (interpreted in f64) equals the oracle's
+    reverse sweep, and both plans (primal, gradient) are supported."""
+    import nd_programs as ND
+    rng = np.random.default_rng(5000 + seed)
+    text, args = ND.nd_program(rng)
+    m = oracle.parse(text)
+    f = _ad_cross_check(text, "f", "g", [x.astype(np.float64) for x in ND.nd_inputs(rng, args)])
+    assert f.signature(0) == _oracle_sig(m, "f")
+    assert f.signature(1) == _oracle_sig(m, "g")
+    for mode in (2, 3):
+        assert "unsupported" not in f.print(mode), text + f.print(mode)
+    body, _ = ND.nd_program(np.random.default_rng(5000 + seed), all_values=True)
+    fb = _plan_only(body, "f")
+    assert fb.signature(0) == _oracle_sig(oracle.parse(body), "f")
+    assert "unsupported" not in fb.print(2), body + fb.print(2)

@@ -653,3 +653,60 @@ def test_tma_staged_ew_kernel_bit_identical(tmp_path):
         outs[tma] = np.load(out)
     for k in outs["0"].files:
         np.testing.assert_array_equal(outs["0"][k], outs["1"][k])
+
+
+def _min_compare_margin(mod, fname, ins64):
+    """Smallest |a - b| over the operands of every compare in the function (f64)."""
+    fn = mod.functions[fname]
+    env = oracle.interp.evaluate(fn, ins64)
+    margin = np.inf
+    for ins in fn.insts:
+        if ins.opcode in ("lt", "le", "gt", "ge", "eq", "ne"):
+            a, b = [oracle.interp.literal_value(o) if o.kind == "literal" else env[o.name] for o in ins.operands]
+            d = np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))
+            d = d[d > 0]  # exact ties (a value compared with its own copy) decide the same on both sides
+            if d.size:
+                margin = min(margin, float(np.min(d)))
+    return margin
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_nd_programs(seed):
+    """Rank-1..5 programs (NumPy broadcasting across ranks, rank>2
+    transposes, reductions along random axes, compare/select) run on the GPU
+    against the oracle: primal loss and every gradient."""
+    import nd_programs as ND
+    rng = np.random.default_rng(5000 + seed)
+    text, args = ND.nd_program(rng)
+    m = oracle.parse(text)
+    # a comparison is a discrete decision: inputs whose compares come within
+    # 1e-4 of a tie are redrawn (fp32 and f64 may decide a near-tie differently)
+    best = None
+    for _ in range(50):
+        cand = ND.nd_inputs(rng, args)
+        mg = _min_compare_margin(m, "f", [x.astype(np.float64) for x in cand])
+        if best is None or mg > best[0]:
+            best = (mg, cand)
+        if mg > 1e-4:
+            break
+    ins = best[1]
+    res = gpu_run(text, "f", "g", ins)
+    ins64 = [x.astype(np.float64) for x in ins]
+    rp = oracle.run(m, "f", ins64)[0]
+    assert_f32_parity(res["primal"][0], rp, term_bound(m, "f", ins64)[0], what="nd primal\n" + text)
+    ref = oracle.run(m, "g", ins64)
+    gm = _grad_module(res)
+    bg = term_bound(gm, "g", ins64)
+    emu = f32_emulation(gm, "g", ins64)
+    for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, bg, emu)):
+        assert_f32_parity(g, r, b, what=f"nd grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
+    # the same program returning every value it defines: returned views
+    # (transposes, shapeCasts) and values stored by the kernel that reads them
+    body, _ = ND.nd_program(np.random.default_rng(5000 + seed), all_values=True)
+    mb = oracle.parse(body)
+    gs = gpu_run(body, "f", None, ins, which="primal")["primal"]
+    rs = oracle.run(mb, "f", ins64)
+    bs = term_bound(mb, "f", ins64)
+    es = f32_emulation(mb, "f", ins64)
+    for k, (g, r, b, e) in enumerate(zip(gs, rs, bs, es)):
+        assert_f32_parity(g, r, b, what=f"nd value {k}\n{body}", extra=4.0 * float(np.max(np.abs(e - r))))
