@@ -446,18 +446,15 @@ struct Planner {
       if (m[j] >= 0) out->strides[m[j]] = src.strides[j];
     return true;
   }
-  // would the materialised ref of view value v be expressible?
-  bool structurally_contiguous(int v) const {
+  // a materialised shapeCast view that merges or splits dims: its copy
+  // kernel iterates in the source's shape (any source layout reads at the
+  // identity map) and stores into the value's unpadded home viewed in that
+  // shape (row-major homes of equal size share their element order)
+  bool reshape_copy(int v) const {
     const Inst* in = def(v);
-    if (!in || !is_view(in) || !vi[v].inl) return true;
-    int src = in->ops[0].value;
-    if (in->op == Op::Transpose) {
-      int nonunit = 0;
-      for (auto d : ty(v).shape) nonunit += d != 1;
-      return nonunit <= 1 && structurally_contiguous(src);
-    }
-    if (in->op == Op::Slice) return structurally_contiguous(src);
-    return structurally_contiguous(src);
+    if (!in || in->op != Op::ShapeCast || !vi[v].mat) return false;
+    Map m;
+    return !view_map(*in, identity(ty(v).rank()), &m);
   }
 
   // -------------------------------------------------------- availability
@@ -558,8 +555,8 @@ struct Planner {
         r.kind = Root::Store;
         r.v = v;
         n.roots.push_back(r);
-        n.shape = ty(v).shape;
-        n.perm = identity(ty(v).rank());
+        n.shape = reshape_copy(v) ? ty(in.ops[0].value).shape : ty(v).shape;
+        n.perm = identity((int)n.shape.size());
       } else {
         continue;
       }
@@ -649,7 +646,9 @@ struct Planner {
         if (is_view(in)) {  // forced view copy: reads its source through the view
           int src = in->ops[0].value;
           Map ma;
-          if (in->op != Op::Slice && view_map(*in, id, &ma)) {
+          if (reshape_copy(r.v)) {
+            walk(src, identity(ty(src).rank()));
+          } else if (in->op != Op::Slice && view_map(*in, id, &ma)) {
             walk(src, ma);
           } else {
             n.reads.insert(base_of(src));
@@ -911,6 +910,10 @@ struct Planner {
   void assign_homes() {
     plan.bufs.clear();
     plan.workspace_bytes = 0;
+    for (auto& x : vi) {  // (re-planning after force_unaddressable_operands)
+      x.homes.clear();
+      x.group_use = false;
+    }
     // group_use: read by a (non-dot) kernel, through views
     for (auto& n : nodes) {  // reads by another kernel (values a group stores itself stay in registers)
       if (n.is_dot || n.merged_into >= 0) continue;
@@ -951,12 +954,15 @@ struct Planner {
         for (int k : x.more_outs)
           x.homes.push_back(make_home(output_buf(k), (int)v, ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
       } else if (need32) {
-        int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(v), natural((int)v)), natural((int)v));
-        x.homes.push_back(make_home(b, (int)v, natural((int)v), padded_ld(ty(v))));
+        const bool pad = !reshape_copy((int)v);
+        int b = add_buf(BufferSlot::Work, -1, pad ? padded_bytes(ty(v), natural((int)v)) : ty(v).numel() * stype_size(natural((int)v)),
+                        natural((int)v));
+        x.homes.push_back(make_home(b, (int)v, natural((int)v), pad ? padded_ld(ty(v)) : 0));
       }
       if (x.dot_use && opt.policy == Policy::BF16) {
-        int b = add_buf(BufferSlot::Work, -1, padded_bytes(ty(v), SType::BF16), SType::BF16);
-        x.homes.push_back(make_home(b, (int)v, SType::BF16, padded_ld(ty(v))));
+        const bool pad = !reshape_copy((int)v);
+        int b = add_buf(BufferSlot::Work, -1, pad ? padded_bytes(ty(v), SType::BF16) : ty(v).numel() * 2, SType::BF16);
+        x.homes.push_back(make_home(b, (int)v, SType::BF16, pad ? padded_ld(ty(v)) : 0));
       }
       if (x.homes.empty() && !(is_dot && fused_dot_group.count((int)v))) {
         int b = add_buf(BufferSlot::Work, -1, ty(v).numel() * stype_size(natural((int)v)), natural((int)v));
@@ -1211,6 +1217,21 @@ struct Planner {
         out.st = plan.bufs[out.buf].st;
         store_slots.push_back(s);
         stores.push_back(store_ref(out, identity(rk)));
+        continue;
+      }
+      if (reshape_copy(v)) {  // iterate in the source's shape (see reshape_copy)
+        const int src = def(v)->ops[0].value;
+        const int s = pb.node(src, identity(ty(src).rank()));
+        for (auto& h : vi[v].homes) {
+          TensorRef hr = h.ref;
+          if (!hr.contiguous()) unsupported("padded home of a reshaped copy");
+          hr.shape = ty(src).shape;
+          hr.strides = contig_strides(hr.shape);
+          store_slots.push_back(s);
+          IterRef st = store_ref(hr, identity(rk));
+          st.st = h.st;
+          stores.push_back(st);
+        }
         continue;
       }
       int s;
@@ -1790,26 +1811,58 @@ struct Planner {
     plan.steps.swap(out);
   }
 
+  // a dot / product operand reached through views must be one strided ref
+  // (dots: a unit stride in one dim); a view that is not (e.g. a shapeCast
+  // merging the dims of a transposed or row-padded home) is materialised by
+  // its own copy root, and planning repeats
+  bool force_unaddressable_operands() {
+    for (auto& in : f.insts) {
+      const bool dot = is_dotlike(in.op);
+      if (!dot && !is_prod(&in)) continue;
+      const bool bf = dot && opt.policy == Policy::BF16;
+      for (auto& o : in.ops) {
+        if (o.is_lit() || vi[o.value].dead) continue;
+        const int v = o.value;
+        TensorRef r;
+        bool ok = ref_of(v, bf, &r) && (!bf || r.st == SType::BF16);
+        if (ok && dot)
+          ok = r.strides.size() == 2 &&
+               (r.strides[1] == 1 || r.strides[0] == 1 || r.shape[0] == 1 || r.shape[1] == 1);
+        if (ok) continue;
+        int u = v;  // the outermost inlined view that is not addressable
+        if (!(vi[u].inl && is_view(def(u))) || force_mat.count(u))
+          unsupported(dot ? "dot operand not addressable" : "reduce operand not addressable");
+        force_mat.insert(u);
+        return true;
+      }
+    }
+    return false;
+  }
+
   void run() {
     check_supported();
     peepholes();
     analyse();
     reduce_chains();
-    for (int iter = 0;; ++iter) {
-      if (iter > 1000) throw Error(kStatusRuntime, 0, 0, "planner did not converge");
-      need_iterate = false;
-      decide();
-      alias_outputs();
-      build_nodes();
-      for (auto& n : nodes) region_of(n);
-      if (need_iterate) continue;
-      if (split_oversized()) continue;
-      build_edges();
-      merge_groups();
-      if (!duplicates()) break;
+    for (int outer = 0;; ++outer) {
+      if (outer > 100) throw Error(kStatusRuntime, 0, 0, "planner did not converge");
+      for (int iter = 0;; ++iter) {
+        if (iter > 1000) throw Error(kStatusRuntime, 0, 0, "planner did not converge");
+        need_iterate = false;
+        decide();
+        alias_outputs();
+        build_nodes();
+        for (auto& n : nodes) region_of(n);
+        if (need_iterate) continue;
+        if (split_oversized()) continue;
+        build_edges();
+        merge_groups();
+        if (!duplicates()) break;
+      }
+      fuse_epilogues();
+      assign_homes();
+      if (!force_unaddressable_operands()) break;
     }
-    fuse_epilogues();
-    assign_homes();
     emit_steps(schedule());
     check_no_self_reads();
   }

@@ -25,9 +25,10 @@ def bcast_shape(rng, S):
     return tuple(s[drop:])
 
 
-def nd_program(rng, max_elems=6000, all_values=False):
+def nd_program(rng, max_elems=6000, all_values=False, allow_select=True):
     """(text, args); with all_values the primal returns every f32 value it
-    defines (a tuple, no gradient declaration) instead of the loss."""
+    defines (a tuple, no gradient declaration) instead of the loss; without
+    allow_select no compare/select (discrete decisions) is drawn."""
     r = int(rng.integers(1, 6))
     while True:
         S = [int(rng.integers(1, 6)) for _ in range(r)]
@@ -36,7 +37,8 @@ def nd_program(rng, max_elems=6000, all_values=False):
             break
     S = tuple(S)
     RS = tuple(reversed(S))
-    args = [("x", S), ("b1", bcast_shape(rng, S)), ("b2", bcast_shape(rng, S)), ("y", S)]
+    args = [("x", S), ("b1", bcast_shape(rng, S)), ("b2", bcast_shape(rng, S)), ("y", S), ("w", (S[-1], S[-1]))]
+    M2 = (int(np.prod(S[:-1])), S[-1])  # cur viewed as a matrix for dot
     L, vals, cur, k = [], [], "%x", 0
 
     def d(name, rhs, shape):  # one definition of an f32 value
@@ -48,7 +50,9 @@ def nd_program(rng, max_elems=6000, all_values=False):
         return [f"%b1: {T(args[1][1])}", f"%b2: {T(args[2][1])}", "0.3: f32", f"%y: {T(S)}"][c]
 
     for _ in range(int(rng.integers(4, 9))):
-        kind = ["bin", "bin_rev", "unary", "transpose", "reduce", "select"][int(rng.integers(6))]
+        kind = ["bin", "bin_rev", "unary", "transpose", "reduce", "select", "dot", "math"][int(rng.integers(8))]
+        if kind == "select" and not allow_select:
+            kind = "math"
         k += 1
         i = k
         if kind in ("bin", "bin_rev"):
@@ -79,6 +83,23 @@ def nd_program(rng, max_elems=6000, all_values=False):
             d(f"%k{i}", f"shapeCast %r{i}: {T(RSH)} to {' x '.join(map(str, KS))}", KS)
             d(f"%s{i}", f"multiply %k{i}: {T(KS)}, 0.1: f32", KS)
             d(f"%t{i}", f"add {cur}: {T(S)}, %s{i}: {T(KS)}", S)
+        elif kind == "dot":  # shapeCast to [prod(S[:-1]), S[-1]], dot with w, shapeCast back
+            d(f"%v{i}", f"shapeCast {cur}: {T(S)} to {M2[0]} x {M2[1]}", M2)
+            d(f"%o{i}", f"dot %v{i}: {T(M2)}, %w: {T(args[4][1])}", M2)
+            d(f"%t{i}", f"shapeCast %o{i}: {T(M2)} to {' x '.join(map(str, S))}", S)
+        elif kind == "math":  # power, divide, log / sqrt of 1 + x^2, abs
+            op = ["power2", "power3", "divide", "log", "sqrt", "abs"][int(rng.integers(6))]
+            if op.startswith("power"):
+                d(f"%t{i}", f"power {cur}: {T(S)}, {op[-1]}: f32", S)
+            elif op == "abs":
+                d(f"%t{i}", f"abs {cur}: {T(S)}", S)
+            else:
+                d(f"%u{i}", f"multiply {cur}: {T(S)}, {cur}: {T(S)}", S)
+                d(f"%a{i}", f"add %u{i}: {T(S)}, 1: f32", S)
+                if op == "divide":
+                    d(f"%t{i}", f"divide {cur}: {T(S)}, %a{i}: {T(S)}", S)
+                else:
+                    d(f"%t{i}", f"{op} %a{i}: {T(S)}", S)
         else:  # relu-like select against a broadcast threshold
             L.append(f"    %c{i} = gt {cur}: {T(S)}, {other()}")
             d(f"%t{i}", f"select %c{i}: {TB(S)}, {cur}: {T(S)}, %b1: {T(args[1][1])}", S)
@@ -101,4 +122,6 @@ def nd_program(rng, max_elems=6000, all_values=False):
 
 
 def nd_inputs(rng, args):
-    return [rng.uniform(-1, 1, s).astype(np.float32) for _, s in args]
+    # w scaled so a chain of dots keeps values O(1)
+    return [(rng.uniform(-1, 1, s) * (1.0 / np.sqrt(s[0]) if n == "w" else 1.0)).astype(np.float32)
+            for n, s in args]

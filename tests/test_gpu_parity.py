@@ -710,3 +710,25 @@ def test_random_nd_programs(seed):
     es = f32_emulation(mb, "f", ins64)
     for k, (g, r, b, e) in enumerate(zip(gs, rs, bs, es)):
         assert_f32_parity(g, r, b, what=f"nd value {k}\n{body}", extra=4.0 * float(np.max(np.abs(e - r))))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_nd_programs_bf16(seed):
+    """The N-d corpus (without compare/select) under the bf16 dot policy:
+    loss and gradients within A18' (2e-2 normwise) of the oracle under the
+    same bf16 operand rounding, every intermediate of the all-values
+    variant likewise."""
+    import nd_programs as ND
+    text, args = ND.nd_program(np.random.default_rng(7000 + seed), allow_select=False)
+    ins = ND.nd_inputs(np.random.default_rng(17 + seed), args)
+    m = oracle.parse(text)
+    res = gpu_run(text, "f", "g", ins, dot_precision="bf16")
+    ins64 = [x.astype(np.float64) for x in ins]
+    assert_normwise(res["primal"][0], oracle.run(m, "f", ins64, dot_policy="bf16")[0], what="nd bf16 loss\n" + text)
+    for k, (g, r) in enumerate(zip(res["grad"], oracle.run(m, "g", ins64, dot_policy="bf16"))):
+        assert_normwise(g, r, what=f"nd bf16 grad out{k}\n{text}")
+    body, _ = ND.nd_program(np.random.default_rng(7000 + seed), all_values=True, allow_select=False)
+    mb = oracle.parse(body)
+    gs = gpu_run(body, "f", None, ins, dot_precision="bf16", which="primal")["primal"]
+    for k, (g, r) in enumerate(zip(gs, oracle.run(mb, "f", ins64, dot_policy="bf16"))):
+        assert_normwise(g, r, what=f"nd bf16 value {k}\n{body}")
