@@ -419,6 +419,48 @@ struct Planner {
     Map m;
     return in.op != Op::Slice && view_map(in, identity(ty(in.result).rank()), &m);
   }
+  // strides of a row-major reshape of a strided tensor, when one exists:
+  // old and new dims are grouped into blocks of equal element count; each
+  // old block must be contiguous within itself (e.g. the rows of a padded
+  // home may be split or merged, its last dim kept)
+  static bool reshape_strides(const std::vector<int64_t>& os, const std::vector<int64_t>& ost,
+                              const std::vector<int64_t>& ns, std::vector<int64_t>* nst) {
+    std::vector<int64_t> a, as;  // old dims without unit dims
+    for (size_t i = 0; i < os.size(); ++i)
+      if (os[i] != 1) {
+        a.push_back(os[i]);
+        as.push_back(ost[i]);
+      }
+    nst->assign(ns.size(), 0);
+    size_t oi = 0, ni = 0;
+    while (ni < ns.size() && ns[ni] == 1) ++ni;
+    while (oi < a.size() && ni < ns.size()) {
+      int64_t np = ns[ni], op = a[oi];
+      size_t nj = ni + 1, oj = oi + 1;
+      while (np != op) {
+        if (np < op) {
+          if (nj >= ns.size()) return false;
+          np *= ns[nj++];
+        } else {
+          if (oj >= a.size()) return false;
+          op *= a[oj++];
+        }
+      }
+      for (size_t k = oi; k + 1 < oj; ++k)
+        if (as[k] != a[k + 1] * as[k + 1]) return false;
+      // new dims ni..nj-1 (unit dims among them get stride 0)
+      int64_t st = as[oj - 1];
+      for (size_t k = nj; k-- > ni;) {
+        (*nst)[k] = ns[k] == 1 ? 0 : st;
+        if (ns[k] != 1) st *= ns[k];
+      }
+      oi = oj;
+      ni = nj;
+      while (ni < ns.size() && ns[ni] == 1) ++ni;
+    }
+    return oi == a.size() && ni == ns.size();
+  }
+
   // strided view of a materialised source
   bool view_ref(const Inst& in, const TensorRef& src, TensorRef* out) const {
     *out = src;
@@ -438,6 +480,10 @@ struct Planner {
       out->strides = contig_strides(su);
       return true;
     }
+    if (in.op == Op::ShapeCast && reshape_strides(src.shape, src.strides, su, &out->strides)) {
+      out->shape = su;
+      return true;
+    }
     Map m;
     if (!view_map(in, identity((int)su.size()), &m)) return false;
     out->shape = su;
@@ -450,6 +496,15 @@ struct Planner {
   // kernel iterates in the source's shape (any source layout reads at the
   // identity map) and stores into the value's unpadded home viewed in that
   // shape (row-major homes of equal size share their element order)
+  // may the value's workspace homes have padded rows?  Not for reshaped
+  // copies (stored in another shape's element order) nor for reductions
+  // (their finalize, and a single-partial producer, write the result
+  // contiguously)
+  bool row_padded(int v) const {
+    const Inst* in = def(v);
+    return !reshape_copy(v) && !(in && in->op == Op::Reduce && red_root.count(v));
+  }
+
   bool reshape_copy(int v) const {
     const Inst* in = def(v);
     if (!in || in->op != Op::ShapeCast || !vi[v].mat) return false;
@@ -954,13 +1009,13 @@ struct Planner {
         for (int k : x.more_outs)
           x.homes.push_back(make_home(output_buf(k), (int)v, ty(v).dtype == DType::Bool ? SType::U8 : SType::F32));
       } else if (need32) {
-        const bool pad = !reshape_copy((int)v);
+        const bool pad = row_padded((int)v);
         int b = add_buf(BufferSlot::Work, -1, pad ? padded_bytes(ty(v), natural((int)v)) : ty(v).numel() * stype_size(natural((int)v)),
                         natural((int)v));
         x.homes.push_back(make_home(b, (int)v, natural((int)v), pad ? padded_ld(ty(v)) : 0));
       }
       if (x.dot_use && opt.policy == Policy::BF16) {
-        const bool pad = !reshape_copy((int)v);
+        const bool pad = row_padded((int)v);
         int b = add_buf(BufferSlot::Work, -1, pad ? padded_bytes(ty(v), SType::BF16) : ty(v).numel() * 2, SType::BF16);
         x.homes.push_back(make_home(b, (int)v, SType::BF16, pad ? padded_ld(ty(v)) : 0));
       }
@@ -1462,6 +1517,8 @@ struct Planner {
       fg.inputs.push_back(in);
       fg.prog.n_in = 1;
       for (auto& h : vi[ri.value].homes) {
+        if (!h.ref.contiguous())  // the partial layout is the value's row-major order
+          throw Error(kStatusRuntime, 0, 0, "planner: reduction %" + f.names[ri.value] + " has a strided home");
         IterRef o;
         o.buf = h.buf;
         o.st = h.st;
@@ -1816,6 +1873,24 @@ struct Planner {
   // merging the dims of a transposed or row-padded home) is materialised by
   // its own copy root, and planning repeats
   bool force_unaddressable_operands() {
+    // a view of a materialised value read by an element-wise kernel at a
+    // map that does not pass through it (merging / splitting shapeCast,
+    // slice) must have a strided ref
+    for (size_t v = 0; v < f.types.size(); ++v) {
+      const Inst* in = def((int)v);
+      if (!in || !is_view(in) || !vi[v].inl || vi[v].dead || force_mat.count((int)v)) continue;
+      const int src = in->ops[0].value;
+      Map ma;
+      if (vi[src].inl && in->op != Op::Slice && view_map(*in, identity(ty((int)v).rank()), &ma)) continue;
+      bool read = false;
+      for (auto& n : nodes)
+        if (!n.is_dot && n.merged_into < 0 && n.inl.count((int)v)) read = true;
+      if (!read) continue;
+      TensorRef r;
+      if (ref_of((int)v, false, &r)) continue;
+      force_mat.insert((int)v);
+      return true;
+    }
     for (auto& in : f.insts) {
       const bool dot = is_dotlike(in.op);
       if (!dot && !is_prod(&in)) continue;

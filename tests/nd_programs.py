@@ -25,16 +25,26 @@ def bcast_shape(rng, S):
     return tuple(s[drop:])
 
 
-def nd_program(rng, max_elems=6000, all_values=False, allow_select=True):
+def nd_program(rng, max_elems=6000, all_values=False, allow_select=True, wide=False):
     """(text, args); with all_values the primal returns every f32 value it
     defines (a tuple, no gradient declaration) instead of the loss; without
-    allow_select no compare/select (discrete decisions) is drawn."""
-    r = int(rng.integers(1, 6))
-    while True:
-        S = [int(rng.integers(1, 6)) for _ in range(r)]
-        S[int(rng.integers(r))] = int(rng.integers(8, 41))  # one long dim: several tiles and a ragged tail
-        if int(np.prod(S)) <= max_elems:
-            break
+    allow_select no compare/select (discrete decisions) is drawn; wide
+    programs (rank 2..4, last dim 64..256, >= 128 rows) put their dots on the
+    tensor-core path."""
+    if wide:
+        r = int(rng.integers(2, 5))
+        while True:
+            S = [int(rng.integers(1, 6)) for _ in range(r - 1)] + [int(rng.choice([64, 96, 128, 200, 256]))]
+            S[int(rng.integers(r - 1))] = int(rng.integers(130, 600))
+            if int(np.prod(S)) <= 400000:
+                break
+    else:
+        r = int(rng.integers(1, 6))
+        while True:
+            S = [int(rng.integers(1, 6)) for _ in range(r)]
+            S[int(rng.integers(r))] = int(rng.integers(8, 41))  # one long dim: several tiles and a ragged tail
+            if int(np.prod(S)) <= max_elems:
+                break
     S = tuple(S)
     RS = tuple(reversed(S))
     args = [("x", S), ("b1", bcast_shape(rng, S)), ("b2", bcast_shape(rng, S)), ("y", S), ("w", (S[-1], S[-1]))]
@@ -53,6 +63,8 @@ def nd_program(rng, max_elems=6000, all_values=False, allow_select=True):
         kind = ["bin", "bin_rev", "unary", "transpose", "reduce", "select", "dot", "math"][int(rng.integers(8))]
         if kind == "select" and not allow_select:
             kind = "math"
+        if all_values and kind == "reduce" and rng.random() < 0.3:
+            kind = "prod"  # forward only (no derivative): all-values programs
         k += 1
         i = k
         if kind in ("bin", "bin_rev"):
@@ -83,6 +95,15 @@ def nd_program(rng, max_elems=6000, all_values=False, allow_select=True):
             d(f"%k{i}", f"shapeCast %r{i}: {T(RSH)} to {' x '.join(map(str, KS))}", KS)
             d(f"%s{i}", f"multiply %k{i}: {T(KS)}, 0.1: f32", KS)
             d(f"%t{i}", f"add {cur}: {T(S)}, %s{i}: {T(KS)}", S)
+        elif kind == "prod":  # cur * shapeCast(prod_a (1 + 0.05 cur)) (factors near 1)
+            a = int(rng.integers(r))
+            RSH = tuple(dd for j, dd in enumerate(S) if j != a)
+            KS = tuple(1 if j == a else dd for j, dd in enumerate(S))
+            d(f"%f{i}", f"multiply {cur}: {T(S)}, 0.05: f32", S)
+            d(f"%g{i}", f"add %f{i}: {T(S)}, 1: f32", S)
+            d(f"%r{i}", f"reduce %g{i}: {T(S)} by multiply along {a}", RSH)
+            d(f"%k{i}", f"shapeCast %r{i}: {T(RSH)} to {' x '.join(map(str, KS))}", KS)
+            d(f"%t{i}", f"multiply {cur}: {T(S)}, %k{i}: {T(KS)}", S)
         elif kind == "dot":  # shapeCast to [prod(S[:-1]), S[-1]], dot with w, shapeCast back
             d(f"%v{i}", f"shapeCast {cur}: {T(S)} to {M2[0]} x {M2[1]}", M2)
             d(f"%o{i}", f"dot %v{i}: {T(M2)}, %w: {T(args[4][1])}", M2)

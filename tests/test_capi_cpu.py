@@ -392,7 +392,10 @@ def test_kernel_templates_compile_under_nvrtc():
         nvrtc.nvrtcAddNameExpression(p, e.encode())
     (r,) = nvrtc.nvrtcCompileProgram(p, len(opts), opts)
     _, n = nvrtc.nvrtcGetProgramLogSize(p)
-    log = b" " * n
+    # NVRTC writes into this buffer: it must be a fresh object.  `b" " * n`
+    # with n == 1 (an empty log) is CPython's shared one-byte b" ", and
+    # overwriting it corrupts every later " " in the process
+    log = bytes(n + 8)
     nvrtc.nvrtcGetProgramLog(p, log)
     assert r == nvrtc.nvrtcResult.NVRTC_SUCCESS, log.decode()[:3000]
     for e in exprs:

@@ -732,3 +732,45 @@ def test_random_nd_programs_bf16(seed):
     gs = gpu_run(body, "f", None, ins, dot_precision="bf16", which="primal")["primal"]
     for k, (g, r) in enumerate(zip(gs, oracle.run(mb, "f", ins64, dot_policy="bf16"))):
         assert_normwise(g, r, what=f"nd bf16 value {k}\n{body}")
+
+
+@pytest.mark.parametrize("seed,prec", [(s, "f32") for s in range(4)] + [(s, "bf16") for s in range(8)])
+def test_random_nd_programs_wide(seed, prec):
+    """Wide N-d programs (last dim 64..256, >= 128 rows): dots through
+    reshapes of padded homes run on tcgen05 (bf16) / SIMT (fp32); the
+    all-values variant adds forward products (`reduce ... by multiply`)."""
+    import nd_programs as ND
+    kw = dict(wide=True, allow_select=prec == "f32")
+    text, args = ND.nd_program(np.random.default_rng(9000 + seed), **kw)
+    m = oracle.parse(text)
+    rng = np.random.default_rng(99 + seed)
+    best = None
+    for _ in range(20):
+        cand = ND.nd_inputs(rng, args)
+        mg = _min_compare_margin(m, "f", [x.astype(np.float64) for x in cand])
+        if best is None or mg > best[0]:
+            best = (mg, cand)
+        if mg > 1e-4:
+            break
+    ins = best[1]
+    ins64 = [x.astype(np.float64) for x in ins]
+    pol = "bf16" if prec == "bf16" else None
+    res = gpu_run(text, "f", "g", ins, dot_precision=prec)
+    body, _ = ND.nd_program(np.random.default_rng(9000 + seed), all_values=True, **kw)
+    mb = oracle.parse(body)
+    gs = gpu_run(body, "f", None, ins, dot_precision=prec, which="primal")["primal"]
+    rs = oracle.run(mb, "f", ins64, dot_policy=pol)
+    if prec == "bf16":
+        assert_normwise(res["primal"][0], oracle.run(m, "f", ins64, dot_policy=pol)[0], what="wide loss\n" + text)
+        for k, (g, r) in enumerate(zip(res["grad"], oracle.run(m, "g", ins64, dot_policy=pol))):
+            assert_normwise(g, r, what=f"wide grad out{k}\n{text}")
+        for k, (g, r) in enumerate(zip(gs, rs)):
+            assert_normwise(g, r, what=f"wide value {k}\n{body}")
+        return
+    assert_f32_parity(res["primal"][0], oracle.run(m, "f", ins64)[0], term_bound(m, "f", ins64)[0], what="wide loss")
+    ref = oracle.run(m, "g", ins64)
+    gm = _grad_module(res)
+    for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, term_bound(gm, "g", ins64), f32_emulation(gm, "g", ins64))):
+        assert_f32_parity(g, r, b, what=f"wide grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
+    for k, (g, r, b, e) in enumerate(zip(gs, rs, term_bound(mb, "f", ins64), f32_emulation(mb, "f", ins64))):
+        assert_f32_parity(g, r, b, what=f"wide value {k}\n{body}", extra=4.0 * float(np.max(np.abs(e - r))))
