@@ -670,7 +670,7 @@ def _min_compare_margin(mod, fname, ins64):
     return margin
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(16))
 def test_random_nd_programs(seed):
     """Rank-1..5 programs (NumPy broadcasting across ranks, rank>2
     transposes, reductions along random axes, compare/select) run on the GPU
@@ -712,7 +712,7 @@ def test_random_nd_programs(seed):
         assert_f32_parity(g, r, b, what=f"nd value {k}\n{body}", extra=4.0 * float(np.max(np.abs(e - r))))
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(8))
 def test_random_nd_programs_bf16(seed):
     """The N-d corpus (without compare/select) under the bf16 dot policy:
     loss and gradients within A18' (2e-2 normwise) of the oracle under the
@@ -734,7 +734,7 @@ def test_random_nd_programs_bf16(seed):
         assert_normwise(g, r, what=f"nd bf16 value {k}\n{body}")
 
 
-@pytest.mark.parametrize("seed,prec", [(s, "f32") for s in range(4)] + [(s, "bf16") for s in range(8)])
+@pytest.mark.parametrize("seed,prec", [(s, "f32") for s in range(3)] + [(s, "bf16") for s in range(5)])
 def test_random_nd_programs_wide(seed, prec):
     """Wide N-d programs (last dim 64..256, >= 128 rows): dots through
     reshapes of padded homes run on tcgen05 (bf16) / SIMT (fp32); the
