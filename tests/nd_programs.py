@@ -146,3 +146,42 @@ def nd_inputs(rng, args):
     # w scaled so a chain of dots keeps values O(1)
     return [(rng.uniform(-1, 1, s) * (1.0 / np.sqrt(s[0]) if n == "w" else 1.0)).astype(np.float32)
             for n, s in args]
+
+
+def nd_grad_config(rng, max_elems=6000):
+    """A random program whose primal returns a tuple (loss, last tensor
+    value) with a random gradient configuration (Fig. 3 / Fig. 4: `wrt` a
+    subset, `keeping` some outputs, `from` either output, `seedable` with a
+    scalar or tensor seed).  Returns (text, args, cfg)."""
+    text, args = nd_program(rng, max_elems)
+    S = args[0][1]
+    lines = text.split("\n[gradient")[0].splitlines()
+    body = [l for l in lines if l.startswith("    %")]
+    tail = [l for l in body if l.strip().startswith("%sq =")][0]
+    last = tail.split("multiply ")[1].split(":")[0]  # the value squared into the loss
+    ret = [l for l in lines if l.strip().startswith("return")][0]
+    loss = ret.split("return ")[1].split(":")[0]
+    n = len(args)
+    wrt = sorted(int(i) for i in rng.choice(n, size=int(rng.integers(1, n + 1)), replace=False))
+    frm = int(rng.integers(2))
+    keeping = [k for k in range(2) if rng.random() < 0.5]
+    seedable = bool(rng.random() < 0.6)
+    sig = ", ".join(T(s) for _, s in args)
+    rtys = ["f32", T(S)]
+    out = [l for l in lines if not l.strip().startswith("return") and not l.startswith("func @f")]
+    head = [l for l in lines if l.startswith("func @f")][0]
+    head = head.replace("-> f32 {", f"-> (f32, {T(S)}) {{")
+    i_entry = [k for k, l in enumerate(out) if l.startswith("'entry")][0]
+    out.insert(i_entry, head)
+    out = [l for l in out if l != "}"]
+    out += [f"    return ({loss}: f32, {last}: {T(S)})", "}", ""]
+    gin = sig + (", " + rtys[frm] if seedable else "")
+    gout = [T(args[i][1]) for i in wrt] + [rtys[k] for k in keeping]
+    attr = f"[gradient @f from {frm} wrt {', '.join(map(str, wrt))}"
+    if keeping:
+        attr += f" keeping {', '.join(map(str, keeping))}"
+    attr += " seedable]" if seedable else "]"
+    gsig = gout[0] if len(gout) == 1 else "(" + ", ".join(gout) + ")"
+    out += [attr, f"func @g: ({gin}) -> {gsig}", ""]
+    cfg = dict(wrt=wrt, frm=frm, keeping=keeping, seedable=seedable, seed_shape=() if frm == 0 else S)
+    return "\n".join(out), args, cfg

@@ -456,3 +456,22 @@ def test_random_nd_programs_types_ad_and_plan(seed):
     fb = _plan_only(body, "f")
     assert fb.signature(0) == _oracle_sig(oracle.parse(body), "f")
     assert "unsupported" not in fb.print(2), body + fb.print(2)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_gradient_configurations(seed):
+    """Random `[gradient @f from F wrt W keeping K seedable]` declarations on
+    N-d programs returning (loss, tensor) (Fig. 3, Fig. 4
+    P:L358-365): C++ signature and adjoint IR (in f64) equal the oracle's,
+    both plans supported."""
+    import nd_programs as ND
+    rng = np.random.default_rng(300 + seed)
+    text, args, cfg = ND.nd_grad_config(rng)
+    m = oracle.parse(text)
+    ins = [x.astype(np.float64) for x in ND.nd_inputs(rng, args)]
+    s = rng.uniform(-1, 1, cfg["seed_shape"]) if cfg["seedable"] else None
+    f = _ad_cross_check(text, "f", "g", ins, s)
+    assert f.signature(0) == _oracle_sig(m, "f")
+    assert f.signature(1) == _oracle_sig(m, "g")
+    for mode in (2, 3):
+        assert "unsupported" not in f.print(mode), text + f.print(mode)

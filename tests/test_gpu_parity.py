@@ -774,3 +774,31 @@ def test_random_nd_programs_wide(seed, prec):
         assert_f32_parity(g, r, b, what=f"wide grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
     for k, (g, r, b, e) in enumerate(zip(gs, rs, term_bound(mb, "f", ins64), f32_emulation(mb, "f", ins64))):
         assert_f32_parity(g, r, b, what=f"wide value {k}\n{body}", extra=4.0 * float(np.max(np.abs(e - r))))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_gradient_configurations(seed):
+    """Random gradient declarations (`from` either output of a (loss,
+    tensor) tuple, `wrt` subsets, `keeping`, scalar or tensor seeds) run on
+    the GPU against the oracle: every gradient and kept output."""
+    import nd_programs as ND
+    rng = np.random.default_rng(300 + seed)
+    text, args, cfg = ND.nd_grad_config(rng)
+    m = oracle.parse(text)
+    best = None
+    for _ in range(20):
+        cand = ND.nd_inputs(rng, args)
+        mg = _min_compare_margin(m, "f", [x.astype(np.float64) for x in cand])
+        if best is None or mg > best[0]:
+            best = (mg, cand)
+        if mg > 1e-4:
+            break
+    ins = best[1]
+    seed_v = rng.uniform(-1, 1, cfg["seed_shape"]).astype(np.float32) if cfg["seedable"] else None
+    res = gpu_run(text, "f", "g", ins, seed=seed_v, which="grad")
+    ins64 = [x.astype(np.float64) for x in ins]
+    gargs = ins64 + ([seed_v.astype(np.float64)] if seed_v is not None else [])
+    ref = oracle.run(m, "g", gargs)
+    gm = _grad_module(res)
+    for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, term_bound(gm, "g", gargs), f32_emulation(gm, "g", gargs))):
+        assert_f32_parity(g, r, b, what=f"grad-config out{k} {cfg}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
