@@ -130,9 +130,9 @@ def to_dev(x, dev, bf16=False):
 
 def mlp_setup(w, dev, rank):
     """Inputs of the MLP gradient on this rank: x and W as bf16 (the bf16 dot
-    policy rounds them anyway), one-hot t as bf16 (exact), the rest f32
-    (dlvm.h storage rule).  Returns (handle, dev inputs, seed, host inputs,
-    n_grads)."""
+    policy rounds them anyway), one-hot t as bool bytes (0/1 values, exact),
+    the rest f32 (dlvm.h storage rule).  Returns (handle, dev inputs, seed,
+    host inputs, n_grads)."""
     import numpy as np
     import torch
     import paper_1711_03016_b200 as P
@@ -140,10 +140,13 @@ def mlp_setup(w, dev, rank):
     host = w.inputs(row_offset=rank * w.batch)
     dev_in = []
     for a, x in zip(w.args, host):
-        # bf16 storage (dlvm.h): the dot operands the bf16 policy rounds anyway,
-        # and one-hot targets (exact in bf16) -- halves their upload in e2e
-        bf = (w.dot_precision == "bf16" and (a.name == "x" or a.name.startswith("w"))) or a.dist[0] == "onehot"
-        dev_in.append(to_dev(x, dev, bf))
+        # bf16 storage (dlvm.h): the dot operands the bf16 policy rounds anyway;
+        # one-hot targets as bool bytes (exact) -- a quarter of their f32 upload in e2e
+        bf = w.dot_precision == "bf16" and (a.name == "x" or a.name.startswith("w"))
+        if a.dist[0] == "onehot":
+            dev_in.append(torch.from_numpy(x != 0).to(dev))
+        else:
+            dev_in.append(to_dev(x, dev, bf))
     seed = torch.tensor(np.float32(w.seed()), device=dev)
     return f, dev_in, seed, host, 2 * len(w.layers)
 
@@ -505,6 +508,8 @@ def main():
             t = torch.from_numpy(host[i])
             if dev_in[i].dtype == torch.bfloat16:
                 t = t.to(torch.bfloat16)
+            elif dev_in[i].dtype == torch.bool:
+                t = t != 0
             pinned.append(t.pin_memory())
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
         h2d = sum(p.numel() * p.element_size() for p in pinned)

@@ -51,8 +51,11 @@ typedef enum {
  * SURVEY.md §8(c)): an f32 argument may be passed as bf16 -- its values are
  * then exactly the f32 widening of the bf16 elements (e.g. one-hot targets,
  * or operands the bf16 dot policy rounds anyway) -- under DLVM_DOT_BF16, or
- * under DLVM_DOT_F32 if it feeds no `dot`; an f32 output may be requested as
- * bf16 (stored with round-to-nearest-even). */
+ * under DLVM_DOT_F32 if it feeds no `dot`.  An f32 argument that feeds no
+ * `dot` may also be passed as DLVM_BOOL bytes: its values are then 1.0
+ * where the byte is nonzero, else 0.0 (exact for 0/1 data such as one-hot
+ * targets or masks).  An f32 output may be requested as bf16 (stored with
+ * round-to-nearest-even). */
 typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3 } dlvm_dtype;
 
 #define DLVM_MAX_RANK 8

@@ -149,7 +149,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     const Type& t = f.params[i];
     if (!shape_matches(in[i], t)) return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " shape mismatch");
     bool ok = t.dtype == DType::Bool ? in[i].dtype == DLVM_BOOL
-                                     : (in[i].dtype == DLVM_F32 || (in[i].dtype == DLVM_BF16 && P.input_bf16_ok[i]));
+                                     : (in[i].dtype == DLVM_F32 || (in[i].dtype == DLVM_BF16 && P.input_bf16_ok[i]) ||
+                                        (in[i].dtype == DLVM_BOOL && P.input_u8_ok[i]));
     if (!ok) return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " dtype mismatch");
     if (!in[i].data || reinterpret_cast<uintptr_t>(in[i].data) % 16)
       return fail(DLVM_ERR_USAGE, "input " + std::to_string(i) + " NULL or not 16-byte aligned");

@@ -1031,6 +1031,11 @@ struct Planner {
     plan.input_bf16_ok.assign(f.num_args(), 0);
     for (int i = 0; i < f.num_args(); ++i)
       plan.input_bf16_ok[i] = ty(i).dtype == DType::F32 && (opt.policy == Policy::BF16 || !vi[i].dot_use);
+    // ... or as bool bytes (value 1.0 where nonzero, else 0.0: exact for 0/1
+    // data such as one-hot targets), unless a dot reads it (the bf16 cast /
+    // pack of dot operands and fp32 SIMT operands read f32 or bf16)
+    plan.input_u8_ok.assign(f.num_args(), 0);
+    for (int i = 0; i < f.num_args(); ++i) plan.input_u8_ok[i] = ty(i).dtype == DType::F32 && !vi[i].dot_use;
     if (opt.policy == Policy::BF16) {
       for (int i = 0; i < f.num_args(); ++i) {
         if (!vi[i].dot_use || ty(i).dtype != DType::F32) continue;

@@ -137,6 +137,7 @@ struct Plan {
   int n_inputs = 0, n_outputs = 0;
   bool seed_is_input = false;    // gradient plans: last parameter is the seed
   std::vector<int> input_bf16_ok;  // per input: 1 if it may be passed as bf16 (see make_plan)
+  std::vector<int> input_u8_ok;    // per input: 1 if it may be passed as bool bytes (0/1 values; not a dot operand)
   int launches() const;
   std::string str() const;
   std::string detail() const;  // str() + buffers and every step's operand refs

@@ -537,6 +537,38 @@ def test_bf16_storage_inputs_bit_identical(case):
         np.testing.assert_array_equal(x, y)
 
 
+@pytest.mark.parametrize("case", ["c3", "c2"])
+def test_bool_byte_storage_inputs_bit_identical(case):
+    """dlvm.h: an f32 argument that feeds no dot may be passed as DLVM_BOOL
+    bytes (1.0 where nonzero, else 0.0).  One-hot targets (c3: read by the
+    loss in the last GEMM's epilogue) and the c2 mask (EW kernel) as bytes
+    give bit-identical results to the same 0/1 values as f32; a dot operand
+    passed as bytes is a usage error."""
+    import torch
+    import paper_1711_03016_b200 as P
+    dev = torch.device("cuda:0")
+    if case == "c3":
+        w, prec, name = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)]), "bf16", "t"
+    else:
+        w, prec, name = W.c2(96, 4096), "f32", "m"
+    f = P.Function(w.text, w.fn, w.grad, dot_precision=prec)
+    host = w.inputs()
+    ins32 = [torch.from_numpy(x).to(dev) for x in host]
+    insb = [(t != 0) if a.name == name else t for t, a in zip(ins32, w.args)]
+    sd = w.seed()
+    seed = torch.from_numpy(np.array(np.asarray(sd, np.float32))).to(dev)
+    a = [o.cpu().numpy() for o in f.run(ins32) + f.grad_run(ins32, seed=seed)]
+    b = [o.cpu().numpy() for o in f.run(insb) + f.grad_run(insb, seed=seed)]
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    if case == "c3":
+        bad = [(t != 0) if a.name == "x" else t for t, a in zip(ins32, w.args)]
+        with pytest.raises(P.DlvmError) as e:
+            f.run(bad)
+        from paper_1711_03016_b200.dlvm import DLVM_ERR_USAGE
+        assert e.value.status == DLVM_ERR_USAGE
+
+
 @pytest.mark.parametrize("case", ["c3", "c5"])
 def test_A20_kept_loss_bit_equal_bf16(case):
     """Reading A20: the kept loss of the gradient run equals
