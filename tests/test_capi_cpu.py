@@ -475,3 +475,15 @@ def test_random_gradient_configurations(seed):
     assert f.signature(1) == _oracle_sig(m, "g")
     for mode in (2, 3):
         assert "unsupported" not in f.print(mode), text + f.print(mode)
+
+
+def test_zero_size_dimensions_are_parse_errors():
+    """Reading A25: tensor dimensions are >= 1 (an empty tensor is not an IR
+    value); both front ends reject `<0 x 5 x f32>` as a parse error (class 2)."""
+    t = ('module "m"\nstage raw\nfunc @f: (<0 x 5 x f32>) -> <0 x 5 x f32> {\n'
+         "'entry(%x: <0 x 5 x f32>):\n    %y = tanh %x: <0 x 5 x f32>\n    return %y: <0 x 5 x f32>\n}\n")
+    with pytest.raises(oracle.ParseError):
+        oracle.parse(t)
+    with pytest.raises(P.DlvmError) as e:
+        P.Function(t, "f", None, flags=P.DLVM_PLAN_ONLY)
+    assert e.value.status == 2

@@ -834,3 +834,52 @@ def test_random_gradient_configurations(seed):
     gm = _grad_module(res)
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, term_bound(gm, "g", gargs), f32_emulation(gm, "g", gargs))):
         assert_f32_parity(g, r, b, what=f"grad-config out{k} {cfg}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
+
+
+DEGENERATE = '''module "deg"
+stage raw
+func @f: (f32, <1 x f32>, <1 x 1 x f32>, <1 x 1 x 1 x 1 x 1 x f32>, <1 x 1 x f32>) -> (f32, <1 x 1 x f32>) {
+'entry(%s: f32, %v: <1 x f32>, %m: <1 x 1 x f32>, %q: <1 x 1 x 1 x 1 x 1 x f32>, %w: <1 x 1 x f32>):
+    %a = multiply %s: f32, %v: <1 x f32>
+    %b = add %a: <1 x f32>, %m: <1 x 1 x f32>
+    %c = tanh %b: <1 x 1 x f32>
+    %d = dot %c: <1 x 1 x f32>, %w: <1 x 1 x f32>
+    %e = transpose %d: <1 x 1 x f32>
+    %g = multiply %e: <1 x 1 x f32>, %q: <1 x 1 x 1 x 1 x 1 x f32>
+    %h = reduce %g: <1 x 1 x 1 x 1 x 1 x f32> by add along 3
+    %pq = reduce %q: <1 x 1 x 1 x 1 x 1 x f32> by multiply along 2
+    %hp = multiply %h: <1 x 1 x 1 x 1 x f32>, %pq: <1 x 1 x 1 x 1 x f32>
+    %k = reduce %hp: <1 x 1 x 1 x 1 x f32> by add along 0
+    %r = shapeCast %k: <1 x 1 x 1 x f32> to 1 x 1
+    %t = subtract %r: <1 x 1 x f32>, 0.5: f32
+    %l = reduce %t: <1 x 1 x f32> by add along 1
+    %z = reduce %l: <1 x f32> by add along 0
+    %y = power %z: f32, 2: f32
+    return (%y: f32, %c: <1 x 1 x f32>)
+}
+
+[gradient @f from 0 wrt 0, 1, 2, 4 keeping 1 seedable]
+func @g: (f32, <1 x f32>, <1 x 1 x f32>, <1 x 1 x 1 x 1 x 1 x f32>, <1 x 1 x f32>, f32) -> (f32, <1 x f32>, <1 x 1 x f32>, <1 x 1 x f32>, <1 x 1 x f32>)
+'''
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_degenerate_unit_and_scalar_shapes(prec):
+    """Degenerate shapes (SURVEY §8(c) edge cases): scalars, <1>, <1 x 1>,
+    rank-5 all-unit tensors, a 1x1x1 dot, reductions along unit axes
+    (add and multiply), transposes of unit matrices; primal and a seeded
+    gradient with a kept output (the product sits off the active path of
+    %q, which is not in wrt)."""
+    m = oracle.parse(DEGENERATE)
+    vals = [np.float32(0.7), np.array([0.3], np.float32), np.array([[-0.2]], np.float32),
+            np.full((1, 1, 1, 1, 1), 1.5, np.float32), np.array([[0.9]], np.float32)]
+    if prec == "bf16":
+        vals = [bf16_round(np.asarray(v)).reshape(np.shape(v)) for v in vals]
+    seed = np.float32(-1.25)
+    res = gpu_run(DEGENERATE, "f", "g", vals, seed=seed, dot_precision=prec)
+    pol = "bf16" if prec == "bf16" else None
+    ins64 = [np.asarray(v, np.float64) for v in vals]
+    for g, r in zip(res["primal"], oracle.run(m, "f", ins64, dot_policy=pol)):
+        np.testing.assert_allclose(g, r, rtol=1e-5, atol=1e-7)
+    for g, r in zip(res["grad"], oracle.run(m, "g", ins64 + [np.float64(seed)], dot_policy=pol)):
+        np.testing.assert_allclose(g, r, rtol=1e-5, atol=1e-7)
