@@ -71,15 +71,19 @@ def test_c2_full_size_sampled():
     assert_f32_parity(y.cpu().numpy()[rows], yr, what="c2 y rows")
     dxr, _, _ = oracle.run(mm, "chain_grad", sub + [g[rows]])
     assert_f32_parity(dx.cpu().numpy()[rows], dxr, what="c2 dx rows")
-    # dw, db over all 16384 rows: float64 column sums of the oracle's own per-element terms
-    z = xs[0] * xs[1] + xs[2]
-    a1 = g * xs[3] * (1.0 - np.tanh(z) ** 2)
-    del z
-    dbr = a1.sum(axis=0, keepdims=True)
-    dwt = a1 * xs[0]
-    dwr = dwt.sum(axis=0, keepdims=True)
-    assert_f32_parity(db.cpu().numpy(), dbr, np.abs(a1).sum(axis=0, keepdims=True), what="c2 db")
-    assert_f32_parity(dw.cpu().numpy(), dwr, np.abs(dwt).sum(axis=0, keepdims=True), what="c2 dw")
+    # dw, db over all 16384 rows and all columns: the oracle runs the same
+    # program on 1024-column blocks (column sums are column-local)
+    B = 1024
+    mb = oracle.parse(W.chain_ir(16384, B))
+    gb = oracle.parse('module "g"\nstage optimizable\n' +
+                      P.Function(W.chain_ir(16384, B), "chain", "chain_grad", flags=P.DLVM_PLAN_ONLY).print(1))
+    dwg, dbg = dw.cpu().numpy(), db.cpu().numpy()
+    for c0 in range(0, 16384, B):
+        blk = [xs[0][:, c0:c0 + B], xs[1][:, c0:c0 + B], xs[2][:, c0:c0 + B], xs[3][:, c0:c0 + B], g[:, c0:c0 + B]]
+        _, rdw, rdb = oracle.run(mb, "chain_grad", blk)
+        _, bdw, bdb = term_bound(gb, "chain_grad", blk)
+        assert_f32_parity(dwg[:, c0:c0 + B], rdw, bdw, what=f"c2 dw cols {c0}+")
+        assert_f32_parity(dbg[:, c0:c0 + B], rdb, bdb, what=f"c2 db cols {c0}+")
 
 
 def test_fig3_fig4_programs():
@@ -883,3 +887,39 @@ def test_degenerate_unit_and_scalar_shapes(prec):
         np.testing.assert_allclose(g, r, rtol=1e-5, atol=1e-7)
     for g, r in zip(res["grad"], oracle.run(m, "g", ins64 + [np.float64(seed)], dot_policy=pol)):
         np.testing.assert_allclose(g, r, rtol=1e-5, atol=1e-7)
+
+
+def test_c2_beyond_int32_element_count():
+    """Maximum sizes: the c2 chain over [2^21, 1025] = 2,149,580,800 elements
+    (> 2^31: 64-bit element offsets in the EW kernel, 32768-row column-sum
+    partials), mask passed as bool bytes.  Oracle checks: sampled rows of y
+    and dx (row-local), and dw/db of sampled columns (the oracle runs the
+    same program on each full [R, 1] column)."""
+    import torch
+    import paper_1711_03016_b200 as P
+    R, C = 1 << 21, 1025
+    dev = torch.device("cuda:0")
+    f = P.Function(W.chain_ir(R, C), "chain", "chain_grad")
+    gen = torch.Generator(device=dev).manual_seed(2031)
+    u = lambda *s: torch.rand(*s, device=dev, generator=gen) * 2 - 1
+    x, w, b = u(R, C), u(1, C), u(1, C)
+    m = torch.rand(R, C, device=dev, generator=gen) < 0.5
+    s = u(R, C)
+    (y,) = f.run([x, w, b, m])
+    dx, dw, db = f.grad_run([x, w, b, m], seed=s)
+    torch.cuda.synchronize()
+    h = lambda t: t.cpu().numpy().astype(np.float64)
+    rows = [0, 1, R // 2 + 3, R - 1]
+    mr = oracle.parse(W.chain_ir(len(rows), C))
+    sub = [h(x[rows]), h(w), h(b), h(m[rows])]
+    assert_f32_parity(h(y[rows]), oracle.run(mr, "chain", sub)[0], what="y rows")
+    assert_f32_parity(h(dx[rows]), oracle.run(mr, "chain_grad", sub + [h(s[rows])])[0], what="dx rows")
+    mc = oracle.parse(W.chain_ir(R, 1))
+    gc = oracle.parse('module "g"\nstage optimizable\n' +
+                      P.Function(W.chain_ir(R, 1), "chain", "chain_grad", flags=P.DLVM_PLAN_ONLY).print(1))
+    for j in (0, 1, 511, C - 1):
+        col = [h(x[:, j:j + 1]), h(w[:, j:j + 1]), h(b[:, j:j + 1]), h(m[:, j:j + 1]), h(s[:, j:j + 1])]
+        _, rdw, rdb = oracle.run(mc, "chain_grad", col)
+        _, bdw, bdb = term_bound(gc, "chain_grad", col)
+        assert_f32_parity(h(dw[:, j:j + 1]), rdw, bdw, what=f"dw col {j}")
+        assert_f32_parity(h(db[:, j:j + 1]), rdb, bdb, what=f"db col {j}")
