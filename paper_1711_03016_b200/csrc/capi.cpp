@@ -116,6 +116,10 @@ void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
 }
 
 // epilogue vectorisation along n: every ref must allow 4-wide access
+// Coarse filter for the tcgen05 epilogue's vector path (contiguous rows,
+// 16-byte base pointers); the kernel additionally checks, per tile row, that
+// each row start is aligned to the vector width it uses (a u8 row of 1000
+// elements is 8-byte aligned on odd rows).
 int epi_vec(const EwParams& e) {
   for (int i = 1; i < e.prog.n_in; ++i) {
     const EwDevIn& r = e.in[i];

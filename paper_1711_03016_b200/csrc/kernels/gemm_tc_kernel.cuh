@@ -779,6 +779,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       const bool block_live = (int64_t)tm * BM < g.M;
       const int64_t m = (int64_t)tm * BM + 32 * q + lane;
       const bool mval = m < g.M;
+      // this row's segments take the vector path only if every row-contiguous
+      // operand's row starts on its vector width (min(16, CW * element bytes))
+      bool row_vec = vec_ok;
+      if (row_vec) {
+        auto al = [&](const void* p, int64_t s0, uint8_t st) {
+          const int es = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+          const int w = CW * es < 16 ? CW * es : 16;
+          return ((reinterpret_cast<uintptr_t>(p) + (uintptr_t)(m * s0 * es)) & (uintptr_t)(w - 1)) == 0;
+        };
+        int nin, nst;
+        if constexpr (SPEC) {
+          nin = T::kIn;
+          nst = T::Stores::n;
+        } else {
+          nin = Pg.n_in;
+          nst = Pg.n_stores;
+        }
+        for (int s2 = 1; s2 < nin; ++s2)
+          if (E.in[s2].s[1] == 1) row_vec &= al(E.in[s2].ptr, E.in[s2].s[0], E.in[s2].st);
+        for (int s2 = 0; s2 < nst; ++s2) row_vec &= al(s2 == 0 ? out0.ptr : E.out[s2].ptr, E.out[s2].s[0], E.out[s2].st);
+      }
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull_bar + 8 * as, aph);
@@ -790,7 +811,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       RawSeg<CW> pf[NPF];  // next chunk's row segments of the vector operands
       auto seg_full = [&](int ch) {
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
-        return mval && vec_ok && n0 + CW <= g.N;
+        return mval && row_vec && n0 + CW <= g.N;
       };
       // warp h takes every other 16-column block (chunks of CW < 16 walk a
       // block in order), so which warp sums which columns -- and with
@@ -812,7 +833,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const int ch = chunk_of(it);
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
-        const bool full = mval && ncol == CW && vec_ok;
+        const bool full = mval && ncol == CW && row_vec;
         RawSeg<CW> cur[NPF];
         if constexpr (SPEC) {
 #pragma unroll

@@ -924,3 +924,46 @@ def test_c2_beyond_int32_element_count():
         _, bdw, bdb = term_bound(gc, "chain_grad", col)
         assert_f32_parity(h(dw[:, j:j + 1]), rdw, bdw, what=f"dw col {j}")
         assert_f32_parity(h(db[:, j:j + 1]), rdb, bdb, what=f"db col {j}")
+
+
+@pytest.mark.parametrize("N", [1000, 200, 72])
+def test_tcgen05_epilogue_unaligned_byte_rows(N):
+    """tcgen05 epilogues with caller-owned byte tensors whose rows are not
+    16-byte aligned (N % 16 == 8: odd rows start 8 bytes off): a bool mask
+    input, a bool output and a byte-stored f32 input.  Rows whose segments
+    are not aligned to the epilogue's vector width take its scalar path
+    (this crashed with a misaligned address before)."""
+    import torch
+    M, K = 1024, 256
+    A, Bt, Y, Bl = f"<{M} x {K} x f32>", f"<{K} x {N} x f32>", f"<{M} x {N} x f32>", f"<{M} x {N} x bool>"
+    text = (f'module "u"\nstage raw\nfunc @f: ({A}, {Bt}, {Bl}, {Y}) -> ({Y}, {Bl}, <{N} x f32>) {{\n'
+            f"'entry(%a: {A}, %b: {Bt}, %c: {Bl}, %t: {Y}):\n"
+            f"    %r = dot %a: {A}, %b: {Bt}\n"
+            f"    %m = select %c: {Bl}, %r: {Y}, 0: f32\n"
+            f"    %d = subtract %m: {Y}, %t: {Y}\n"
+            f"    %g = gt %d: {Y}, 0: f32\n"
+            f"    %s = reduce %d: {Y} by add along 0\n"
+            f"    return (%d: {Y}, %g: {Bl}, %s: <{N} x f32>)\n}}\n")
+    rng = np.random.default_rng(N)
+    a = bf16_round(rng.uniform(-1, 1, (M, K)).astype(np.float32))
+    b = bf16_round(rng.uniform(-1, 1, (K, N)).astype(np.float32))
+    c = rng.random((M, N)) < 0.5
+    t = (rng.random((M, N)) < 0.3).astype(np.float32)
+    m = oracle.parse(text)
+    ref = oracle.run(m, "f", [a.astype(np.float64), b.astype(np.float64), c, t.astype(np.float64)], dot_policy="bf16")
+    for jit in (0, 1):  # compile-time epilogue program (JIT) and the interpreter
+        import paper_1711_03016_b200 as P
+        fl = 0 if jit else P.DLVM_NO_JIT | P.DLVM_NO_SPECIALIZE
+        dev = torch.device("cuda:0")
+        f = P.Function(text, "f", None, dot_precision="bf16", flags=fl)
+        ins = [torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev), torch.from_numpy(c).to(dev),
+               torch.from_numpy(t != 0).to(dev)]  # t passed as bool bytes
+        d, g, s = f.run(ins)
+        torch.cuda.synchronize()
+        assert_f32_parity(d.cpu().numpy().astype(np.float64), ref[0], np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64)) + 1,
+                          what=f"d N={N} jit={jit}")
+        gd = d.cpu().numpy()
+        np.testing.assert_array_equal(g.cpu().numpy(), gd > 0)  # the stored compare agrees with the stored value
+        assert_f32_parity(s.cpu().numpy().astype(np.float64), ref[2],
+                          term_bound(m, "f", [a.astype(np.float64), b.astype(np.float64), c, t.astype(np.float64)])[2] * 16,
+                          what=f"colsum N={N} jit={jit}")
