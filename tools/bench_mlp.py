@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Quick per-kernel timing of one MLP workload's fwd+adjoint step (no oracle,
-no e2e): python tools/bench_mlp.py [c4|c3|c5] [steps]"""
+no e2e): python tools/bench_mlp.py [c4|c4xN|c3|c5] [steps]"""
 import json
 import os
 import sys
@@ -15,7 +15,8 @@ from paper_1711_03016_b200.dp import DataParallelStep  # noqa: E402
 if __name__ == "__main__":
     name = sys.argv[1] if len(sys.argv) > 1 else "c4"
     K = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-    w = {"c4": lambda: W.c4(1), "c3": W.c3, "c5": W.c5}[name]()
+    # c4xN: one rank's share of c4 at N GPUs (global batch 65536 / N rows)
+    w = W.c4(int(name[3:])) if name.startswith("c4x") else {"c4": lambda: W.c4(1), "c3": W.c3, "c5": W.c5}[name]()
     dev = torch.device("cuda:0")
     f, dev_in, seed, host, n_grads = bench.mlp_setup(w, dev, 0)
     dps = DataParallelStep(f, n_grads, dev)
