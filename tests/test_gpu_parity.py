@@ -967,3 +967,30 @@ def test_tcgen05_epilogue_unaligned_byte_rows(N):
         assert_f32_parity(s.cpu().numpy().astype(np.float64), ref[2],
                           term_bound(m, "f", [a.astype(np.float64), b.astype(np.float64), c, t.astype(np.float64)])[2] * 16,
                           what=f"colsum N={N} jit={jit}")
+
+
+def test_c4_full_size_in_bench_launch_configuration():
+    """c4 at full size (batch 65536 on one GPU) exactly as bench.py times it:
+    bench.mlp_setup's storage (x, W as bf16; one-hot t as bool bytes) and
+    dp.DataParallelStep, i.e. the same plans (CTA-pair tcgen05 GEMMs, split-K
+    dW) and launches.  Every gradient is a sum over all 65536 rows, so the
+    oracle runs the whole problem (float64, bf16 operand policy A18')."""
+    import os
+    import sys
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_1711_03016_b200.dp import DataParallelStep
+    w = W.c4(1)
+    dev = torch.device("cuda:0")
+    f, dev_in, seed, host, n_grads = bench.mlp_setup(w, dev, 0)
+    assert dev_in[-1].dtype == torch.bool  # one-hot targets as bytes, as timed
+    dps = DataParallelStep(f, n_grads, dev)
+    outs = [o.double().cpu().numpy() for o in dps.step(dev_in, seed)]
+    torch.cuda.synchronize()
+    m = oracle.parse(w.text)
+    ins64 = [x.astype(np.float64) for x in host]
+    ref = oracle.run(m, w.grad, ins64 + [np.float64(w.seed())], dot_policy="bf16")
+    assert len(outs) == len(ref)
+    for k, (g, r) in enumerate(zip(outs, ref)):
+        assert_normwise(g, r, what=f"c4 full grad out{k}")
