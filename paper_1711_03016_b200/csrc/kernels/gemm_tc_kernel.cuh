@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const uint32_t tmem_base = *tmem_holder;
   // prologue done: let the next kernel start its own, then wait for the
   // previous kernel's results (PDL, launch.cuh)
-  pdl_trigger();
+  pdl_trigger_gemm();
   pdl_wait();
 
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
