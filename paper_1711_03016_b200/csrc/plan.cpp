@@ -1715,6 +1715,9 @@ struct Planner {
     const int64_t simt_tiles64 = ((gm.M + 63) / 64) * ((gm.N + 63) / 64);
     gm.bm = gm.tensor_core ? 128 : (simt_tiles64 < 2 * 148 ? 32 : 64);
     gm.bn = gm.tensor_core ? (gm.N >= 256 ? 256 : 128) : 64;
+    // very few 256 x 256 pair tiles (under half the 74 CTA pairs): 128 x 128
+    // single-CTA tiles spread the contraction over 4x as many SMs
+    if (gm.tensor_core && gm.bn == 256 && ((gm.M + 255) / 256) * ((gm.N + 255) / 256) < 37) gm.bn = 128;
     if (!gm.tensor_core && (gm.M + gm.bm - 1) / gm.bm > 65535)
       unsupported("SIMT dot with more than 65535 row tiles (over 4M rows under the fp32 dot policy)");
     Node epi;
