@@ -994,3 +994,79 @@ def test_c4_full_size_in_bench_launch_configuration():
     assert len(outs) == len(ref)
     for k, (g, r) in enumerate(zip(outs, ref)):
         assert_normwise(g, r, what=f"c4 full grad out{k}")
+
+
+SLICE_CAST = '''module "sc"
+stage raw
+func @f: (<300 x 96 x f32>, <96 x 64 x f32>, <300 x 96 x f32>) -> (<120 x 96 x f32>, <120 x 64 x f32>, <96 x f32>, <120 x 96 x bool>, <120 x 96 x f32>, <200 x 96 x f32>, <96 x f32>) {
+'entry(%x: <300 x 96 x f32>, %w: <96 x 64 x f32>, %y: <300 x 96 x f32>):
+    %s = slice %x: <300 x 96 x f32> from 37 upto 157
+    %t = tanh %s: <120 x 96 x f32>
+    %d = dot %t: <120 x 96 x f32>, %w: <96 x 64 x f32>
+    %r = reduce %s: <120 x 96 x f32> by add along 0
+    %c = gt %s: <120 x 96 x f32>, 0.25: f32
+    %cf = dataTypeCast %c: <120 x 96 x bool> to f32
+    %m = multiply %cf: <120 x 96 x f32>, %t: <120 x 96 x f32>
+    %b = dataTypeCast %m: <120 x 96 x f32> to bool
+    %bf = dataTypeCast %b: <120 x 96 x bool> to f32
+    %yt = transpose %y: <300 x 96 x f32>
+    %ys = slice %x: <300 x 96 x f32> from 100 upto 300
+    %e = add %ys: <200 x 96 x f32>, 1: f32
+    %q = multiply %e: <200 x 96 x f32>, 0.001: f32
+    %qq = add %q: <200 x 96 x f32>, 1: f32
+    %p = reduce %qq: <200 x 96 x f32> by multiply along 0
+    return (%t: <120 x 96 x f32>, %d: <120 x 64 x f32>, %r: <96 x f32>, %b: <120 x 96 x bool>, %bf: <120 x 96 x f32>, %ys: <200 x 96 x f32>, %p: <96 x f32>)
+}
+'''
+
+SLICE_CAST_GRAD = '''module "scg"
+stage raw
+func @f: (<64 x 32 x f32>, <64 x 32 x f32>) -> f32 {
+'entry(%x: <64 x 32 x f32>, %y: <64 x 32 x f32>):
+    %c = gt %y: <64 x 32 x f32>, 0: f32
+    %cf = dataTypeCast %c: <64 x 32 x bool> to f32
+    %t = tanh %x: <64 x 32 x f32>
+    %m = multiply %t: <64 x 32 x f32>, %cf: <64 x 32 x f32>
+    %s = multiply %m: <64 x 32 x f32>, %m: <64 x 32 x f32>
+    %r = reduce %s: <64 x 32 x f32> by add along 1
+    %l = reduce %r: <64 x f32> by add along 0
+    return %l: f32
+}
+
+[gradient @f wrt 0]
+func @g: (<64 x 32 x f32>, <64 x 32 x f32>) -> <64 x 32 x f32>
+'''
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_slice_and_datatypecast(prec):
+    """`slice` (Table 1 L175; forward) and `dataTypeCast` (L177) on the GPU:
+    a slice feeding element-wise ops, a dot, a column sum and a product,
+    returned slices (strided views copied out), bool <-> f32 casts as
+    values and outputs; and a gradient through a cast mask."""
+    rng = np.random.default_rng(55)
+    x = rng.uniform(-1, 1, (300, 96)).astype(np.float32)
+    w = rng.uniform(-0.3, 0.3, (96, 64)).astype(np.float32)
+    y = rng.uniform(-1, 1, (300, 96)).astype(np.float32)
+    if prec == "bf16":
+        x, w = bf16_round(x), bf16_round(w)
+    m = oracle.parse(SLICE_CAST)
+    pol = "bf16" if prec == "bf16" else None
+    res = gpu_run(SLICE_CAST, "f", None, [x, w, y], which="primal", dot_precision=prec)["primal"]
+    ins64 = [x.astype(np.float64), w.astype(np.float64), y.astype(np.float64)]
+    ref = oracle.run(m, "f", ins64, dot_policy=pol)
+    bnd = term_bound(m, "f", ins64)
+    for k, (g, r, b) in enumerate(zip(res, ref, bnd)):
+        if r.dtype == np.bool_:
+            np.testing.assert_array_equal(g, r, err_msg=f"out{k}")
+        elif k == 6:
+            np.testing.assert_allclose(g, r, rtol=(200 + 4) * 2.0 ** -23)  # product of 200 factors (A24)
+        else:
+            assert_f32_parity(g, r, b * (8 if prec == "bf16" else 1), what=f"slice/cast out{k}")
+    mg = oracle.parse(SLICE_CAST_GRAD)
+    a = rng.uniform(-1, 1, (64, 32)).astype(np.float32)
+    c = rng.uniform(-1, 1, (64, 32)).astype(np.float32)
+    rg = gpu_run(SLICE_CAST_GRAD, "f", "g", [a, c], dot_precision=prec)
+    a64, c64 = a.astype(np.float64), c.astype(np.float64)
+    assert_f32_parity(rg["primal"][0], oracle.run(mg, "f", [a64, c64])[0], term_bound(mg, "f", [a64, c64])[0], what="loss")
+    assert_f32_parity(rg["grad"][0], oracle.run(mg, "g", [a64, c64])[0], what="grad through cast mask")
