@@ -1070,3 +1070,79 @@ def test_slice_and_datatypecast(prec):
     a64, c64 = a.astype(np.float64), c.astype(np.float64)
     assert_f32_parity(rg["primal"][0], oracle.run(mg, "f", [a64, c64])[0], term_bound(mg, "f", [a64, c64])[0], what="loss")
     assert_f32_parity(rg["grad"][0], oracle.run(mg, "g", [a64, c64])[0], what="grad through cast mask")
+
+
+OP_SWEEP = '''module "ops"
+stage raw
+func @f: (<96 x 80 x f32>, <1 x 80 x f32>, <96 x 1 x f32>, <96 x 80 x f32>) -> (f32, <96 x 80 x f32>, <96 x 80 x f32>, <96 x 80 x bool>, <96 x 80 x bool>) {
+'entry(%x: <96 x 80 x f32>, %v: <1 x 80 x f32>, %u: <96 x 1 x f32>, %z: <96 x 80 x f32>):
+    %x2 = multiply %x: <96 x 80 x f32>, %x: <96 x 80 x f32>
+    %a = add %x2: <96 x 80 x f32>, 1: f32
+    %e = multiply %v: <1 x 80 x f32>, 2: f32
+    %p = power %a: <96 x 80 x f32>, %e: <1 x 80 x f32>
+    %lg = log %a: <96 x 80 x f32>
+    %sq = sqrt %a: <96 x 80 x f32>
+    %ab = abs %x: <96 x 80 x f32>
+    %sg = sign %z: <96 x 80 x f32>
+    %ex = exp %u: <96 x 1 x f32>
+    %dv = divide %lg: <96 x 80 x f32>, %ex: <96 x 1 x f32>
+    %s1 = subtract %p: <96 x 80 x f32>, %sq: <96 x 80 x f32>
+    %s2 = add %s1: <96 x 80 x f32>, %dv: <96 x 80 x f32>
+    %s3 = multiply %s2: <96 x 80 x f32>, %sg: <96 x 80 x f32>
+    %s4 = add %s3: <96 x 80 x f32>, %ab: <96 x 80 x f32>
+    %c1 = lt %x: <96 x 80 x f32>, %u: <96 x 1 x f32>
+    %c2 = le %z: <96 x 80 x f32>, 0: f32
+    %c3 = ge %x: <96 x 80 x f32>, %v: <1 x 80 x f32>
+    %c4 = eq %sg: <96 x 80 x f32>, 1: f32
+    %c5 = ne %sg: <96 x 80 x f32>, -1: f32
+    %n1 = negate %s4: <96 x 80 x f32>
+    %k1 = select %c1: <96 x 80 x bool>, %s4: <96 x 80 x f32>, %n1: <96 x 80 x f32>
+    %k2 = select %c2: <96 x 80 x bool>, %k1: <96 x 80 x f32>, %x: <96 x 80 x f32>
+    %k3 = select %c3: <96 x 80 x bool>, %k2: <96 x 80 x f32>, 0.5: f32
+    %k4 = select %c5: <96 x 80 x bool>, %k3: <96 x 80 x f32>, %p: <96 x 80 x f32>
+    %q = multiply %k4: <96 x 80 x f32>, %k4: <96 x 80 x f32>
+    %r = reduce %q: <96 x 80 x f32> by add along 1
+    %l = reduce %r: <96 x f32> by add along 0
+    return (%l: f32, %k4: <96 x 80 x f32>, %dv: <96 x 80 x f32>, %c4: <96 x 80 x bool>, %c1: <96 x 80 x bool>)
+}
+
+[gradient @f from 0 wrt 0, 1, 2]
+func @g: (<96 x 80 x f32>, <1 x 80 x f32>, <96 x 1 x f32>, <96 x 80 x f32>) -> (<96 x 80 x f32>, <1 x 80 x f32>, <96 x 1 x f32>)
+'''
+
+
+def test_op_sweep_every_vm_opcode():
+    """Every element-wise opcode of the GPU path with broadcasting (Table 1
+    L170-L178): negate, tanh-free transcendental set (exp, log, sqrt, abs,
+    sign), add/subtract/multiply/divide/power (tensor exponent), all six
+    compares (eq/ne on exact +-1 values from sign), select; primal values,
+    bool outputs bit-exact, and the gradient wrt three broadcast arguments."""
+    m = oracle.parse(OP_SWEEP)
+    rng = np.random.default_rng(808)
+    best = None
+    for _ in range(30):
+        ins = [rng.uniform(-1, 1, (96, 80)).astype(np.float32), rng.uniform(-1, 1, (1, 80)).astype(np.float32),
+               rng.uniform(-1, 1, (96, 1)).astype(np.float32), rng.uniform(-1, 1, (96, 80)).astype(np.float32)]
+        ins[3][rng.random((96, 80)) < 0.1] = 0.0  # sign(0) = 0 cases
+        mg = _min_compare_margin(m, "f", [x.astype(np.float64) for x in ins])
+        if best is None or mg > best[0]:
+            best = (mg, ins)
+        if mg > 1e-4:
+            break
+    ins = best[1]
+    ins64 = [x.astype(np.float64) for x in ins]
+    res = gpu_run(OP_SWEEP, "f", "g", ins)
+    ref = oracle.run(m, "f", ins64)
+    bnd = term_bound(m, "f", ins64)
+    emu = f32_emulation(m, "f", ins64)
+    for k, (g, r, b, e) in enumerate(zip(res["primal"], ref, bnd, emu)):
+        if r.dtype == np.bool_:
+            np.testing.assert_array_equal(g, r, err_msg=f"op sweep bool out{k}")
+        else:
+            assert_f32_parity(g, r, b, what=f"op sweep out{k}", extra=4.0 * float(np.max(np.abs(e - r))))
+    refg = oracle.run(m, "g", ins64)
+    gm = _grad_module(res)
+    bg = term_bound(gm, "g", ins64)
+    eg = f32_emulation(gm, "g", ins64)
+    for k, (g, r, b, e) in enumerate(zip(res["grad"], refg, bg, eg)):
+        assert_f32_parity(g, r, b, what=f"op sweep grad out{k}", extra=4.0 * float(np.max(np.abs(e - r))))
