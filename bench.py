@@ -356,6 +356,7 @@ def main():
     ap.add_argument("--no-elementwise", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the rnn / mlp_hvp legs (SURVEY §8(f) rows)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c3 leg (BASELINE config 3, batch 1024)")
     ap.add_argument("--cpu-rows", type=int, default=None)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: on for the launch-bound c1)")
@@ -592,6 +593,12 @@ def main():
             for v in legs.values():
                 out["gpu_launches"] += v["launches"] * K
             out["next_rows"] = legs
+        if not args.no_configs and args.workload == "c4":
+            # BASELINE config 3 (the same MLP at batch 1024; target >= 975.5 TFLOP/s,
+            # BASELINE.md §3) through dlvm_grad_run, x and W as bf16 storage
+            c3 = bench_grad_leg(WL.c3(), lambda r: WL.c3(r), dev, K, W_, {"x", "w1", "w2", "w3"}, 64)
+            out["gpu_launches"] += c3["launches"] * K
+            out["other_configs"] = {"c3": c3}
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
