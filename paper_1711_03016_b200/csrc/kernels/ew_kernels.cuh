@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
 // Streaming row loads of the f32 fast path.  Measured on c2 (GB/s fwd /
 // fwd+adjoint): __ldg 6289 / 5809; DLVM_EW_LDHINT=1 (L1::no_allocate +
 // L2::256B prefetch hint) 5980 / 5659; =2 (L1::no_allocate + L2 evict_first
-// policy) 5956 / 5603.  Default: plain __ldg.
+// policy) 5956 / 5603.  Default: plain __ldg.  Streaming (__stcs) stores of
+// the row loop measured no change (6273 / 5803).
 #ifndef DLVM_EW_LDHINT
 #define DLVM_EW_LDHINT 0
 #endif
