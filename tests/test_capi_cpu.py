@@ -487,3 +487,29 @@ def test_zero_size_dimensions_are_parse_errors():
     with pytest.raises(P.DlvmError) as e:
         P.Function(t, "f", None, flags=P.DLVM_PLAN_ONLY)
     assert e.value.status == 2
+
+
+def test_planner_layout_heuristics():
+    """Regression guards for plan-time layout choices:
+    few-tile GEMMs use 128-wide tiles; weights get row-padded bf16 copies
+    only for large-batch dots; reduction results get unpadded homes; row
+    splits of a row-padded dot result stay views (no copy launch)."""
+    c3 = _plan_only(W.c3().text, W.c3().fn, W.c3().grad, "bf16")
+    assert any(l.startswith("GEMM 128") for l in c3.print(4).splitlines())   # %z3: 16 pair tiles -> 128 x 128
+    assert "pack %" not in c3.print(3)                                         # batch 1024: no padded weight copy
+    c4 = _plan_only(W.c4().text, W.c4().fn, W.c4().grad, "bf16")
+    assert "pack %w3 to bf16 rows of 1024" in c4.print(3)                      # batch 65536: padded copy
+    # a [2, 96] reduction result (rank 2, last dim 96 -> would pad to 128): unpadded, 768 bytes
+    t = ('module "m"\nstage raw\nfunc @f: (<2 x 50 x 96 x f32>) -> <2 x 96 x f32> {\n'
+         "'entry(%x: <2 x 50 x 96 x f32>):\n    %t = tanh %x: <2 x 50 x 96 x f32>\n"
+         "    %r = reduce %t: <2 x 50 x 96 x f32> by add along 1\n    %s = multiply %r: <2 x 96 x f32>, %r: <2 x 96 x f32>\n"
+         "    return %s: <2 x 96 x f32>\n}\n")
+    det = _plan_only(t, "f").print(9)
+    assert "work -1 bytes 768 " in det, det
+    # dot result [512, 200] (row-padded home, ld 256) split into [4, 128, 200]: a strided view
+    t2 = ('module "m"\nstage raw\nfunc @f: (<512 x 64 x f32>, <64 x 200 x f32>) -> <4 x 128 x 200 x f32> {\n'
+          "'entry(%a: <512 x 64 x f32>, %b: <64 x 200 x f32>):\n    %d = dot %a: <512 x 64 x f32>, %b: <64 x 200 x f32>\n"
+          "    %v = shapeCast %d: <512 x 200 x f32> to 4 x 128 x 200\n    %y = tanh %v: <4 x 128 x 200 x f32>\n"
+          "    return %y: <4 x 128 x 200 x f32>\n}\n")
+    p2 = _plan_only(t2, "f", None, "bf16")
+    assert p2.print(2).count("ew [") == 1, p2.print(2)   # one element-wise launch reads the padded home directly
