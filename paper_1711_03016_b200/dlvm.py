@@ -97,6 +97,8 @@ def _dtype_code(t) -> int:
 
 
 def _tensor(t) -> dlvm_tensor:
+    if not t.is_cuda:
+        raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
     if not t.is_contiguous():
         raise ValueError("dlvm tensors must be contiguous (row-major)")
     d = dlvm_tensor()

@@ -513,3 +513,13 @@ def test_planner_layout_heuristics():
           "    return %y: <4 x 128 x 200 x f32>\n}\n")
     p2 = _plan_only(t2, "f", None, "bf16")
     assert p2.print(2).count("ew [") == 1, p2.print(2)   # one element-wise launch reads the padded home directly
+
+
+def test_binding_refuses_host_tensors():
+    """The C ABI takes device pointers: the binding refuses CPU tensors (a
+    host pointer would fault in the kernels) before anything is launched."""
+    import torch
+    w = W.c2(8, 16)
+    f = _plan_only(w.text, w.fn, w.grad)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        f.run([torch.from_numpy(x) for x in w.inputs()])
