@@ -96,6 +96,12 @@ def _dtype_code(t) -> int:
     return _TORCH_TO_DLVM[t.dtype]
 
 
+def _require_cuda(ts) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
+
+
 def _tensor(t) -> dlvm_tensor:
     if not t.is_cuda:
         raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
@@ -206,6 +212,7 @@ class Function:
 
     def run(self, inputs: Sequence, outputs=None, workspace=None, stream=None):
         import torch
+        _require_cuda(inputs)
         dev = inputs[0].device if inputs else torch.device("cuda")
         outs = self._outputs(0, dev, outputs)
         ws = self._workspace(0, dev) if workspace is None else workspace
@@ -216,6 +223,7 @@ class Function:
 
     def grad_run(self, inputs: Sequence, seed=None, outputs=None, workspace=None, stream=None, events=None):
         import torch
+        _require_cuda(list(inputs) + ([seed] if seed is not None else []))
         dev = inputs[0].device if inputs else torch.device("cuda")
         outs = self._outputs(1, dev, outputs)
         ws = self._workspace(1, dev) if workspace is None else workspace
