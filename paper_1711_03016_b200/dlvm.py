@@ -98,7 +98,7 @@ def _dtype_code(t) -> int:
 
 def _require_cuda(ts) -> None:
     for t in ts:
-        if not t.is_cuda:
+        if hasattr(t, "is_cuda") and not t.is_cuda:
             raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
 
 
