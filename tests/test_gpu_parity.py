@@ -1146,3 +1146,41 @@ def test_op_sweep_every_vm_opcode():
     eg = f32_emulation(gm, "g", ins64)
     for k, (g, r, b, e) in enumerate(zip(res["grad"], refg, bg, eg)):
         assert_f32_parity(g, r, b, what=f"op sweep grad out{k}", extra=4.0 * float(np.max(np.abs(e - r))))
+
+
+def test_concurrent_runs_on_separate_streams_bit_identical():
+    """dlvm_fn_run / dlvm_grad_run keep no mutable state in the handle (the
+    caller owns workspace and outputs): the same handle run concurrently on
+    two streams, and a second handle on a third, give bit-identical results
+    to sequential runs."""
+    import torch
+    import paper_1711_03016_b200 as P
+    dev = torch.device("cuda:0")
+    w3 = W.c3(256, layers=[(512, 512, "relu"), (512, 256, None)])
+    f3 = P.Function(w3.text, w3.fn, w3.grad, dot_precision="bf16")
+    w2 = W.c2(512, 4096)
+    f2 = P.Function(w2.text, w2.fn, w2.grad)
+    ins3 = [torch.from_numpy(x).to(dev) for x in w3.inputs()]
+    ins2 = [torch.from_numpy(x).to(dev) for x in w2.inputs()]
+    s3 = torch.tensor(np.float32(w3.seed()), device=dev)
+    s2 = torch.from_numpy(w2.seed()).to(dev)
+    ref3 = [o.cpu() for o in f3.grad_run(ins3, seed=s3)]
+    ref2 = [o.cpu() for o in f2.grad_run(ins2, seed=s2)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    outs = []
+    for rep in range(4):
+        res = []
+        for k, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                if k < 2:
+                    res.append(f3.grad_run(ins3, seed=s3, stream=st.cuda_stream))
+                else:
+                    res.append(f2.grad_run(ins2, seed=s2, stream=st.cuda_stream))
+        torch.cuda.synchronize()
+        outs.append(res)
+    for res in outs:
+        for k, r in enumerate(res):
+            ref = ref3 if k < 2 else ref2
+            for a, b in zip(r, ref):
+                assert torch.equal(a.cpu(), b), f"stream {k}"
