@@ -1226,3 +1226,36 @@ def test_cuda_graph_capture_and_replay_bit_identical(case):
         torch.cuda.synchronize()
         for a, b in zip(got, eager):
             assert torch.equal(a, b), case
+
+
+def test_gradient_ready_events_fire_after_each_gradient_is_final():
+    """dlvm_grad_run records gradient k's event after the last step that
+    writes it (incl. split-K sum steps): a second stream that waits on the
+    event and copies gradient k while later kernels still run must see the
+    final value (the data-parallel all-reduce relies on this)."""
+    import torch
+    import paper_1711_03016_b200 as P
+    dev = torch.device("cuda:0")
+    w = W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)])  # dW GEMMs with K = 8192 split in two
+    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
+    ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
+    seed = torch.tensor(np.float32(w.seed()), device=dev)
+    n_grads = 2 * len(w.layers)
+    for rep in range(3):
+        events = [torch.cuda.Event() for _ in range(n_grads)]
+        for e in events:
+            e.record()
+        main = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
+        outs = f._outputs(1, dev, None)
+        for o in outs:
+            o.fill_(float("nan"))  # a copy taken too early shows NaN or a partial sum
+        f.grad_run(ins, seed=seed, outputs=outs, stream=main.cuda_stream, events=events)
+        copies = []
+        with torch.cuda.stream(side):
+            for k in reversed(range(n_grads)):
+                side.wait_event(events[k])
+                copies.append((k, outs[k].clone()))
+        torch.cuda.synchronize()
+        for k, c in copies:
+            assert torch.equal(c, outs[k]), f"gradient {k} copied before it was final"
