@@ -1259,3 +1259,39 @@ def test_gradient_ready_events_fire_after_each_gradient_is_final():
         torch.cuda.synchronize()
         for k, c in copies:
             assert torch.equal(c, outs[k]), f"gradient {k} copied before it was final"
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+w = W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)])
+r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
+wr = W.rnn(4, 256, 256, 256)
+rr = gpu_run(wr.text, wr.fn, wr.grad, wr.inputs(), seed=wr.seed(), dot_precision="bf16")
+w2 = W.c2(300, 4096)
+r2 = gpu_run(w2.text, w2.fn, w2.grad, w2.inputs(), seed=w2.seed())
+np.savez({out!r}, *(r["primal"] + r["grad"] + rr["grad"] + r2["primal"] + r2["grad"]))
+"""
+
+
+def test_pdl_launches_bit_identical_to_plain_launches(tmp_path):
+    """Every kernel waits (griddepcontrol.wait) before touching memory its
+    predecessor writes, so programmatic dependent launch changes timing
+    only: DLVM_PDL=1 and DLVM_PDL=0 give bit-identical c3 (split-K dW),
+    rnn (multi-segment GEMMs) and c2 results."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for pdl in ("1", "0"):
+        out = str(tmp_path / f"p{pdl}.npz")
+        script = _PDL_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_PDL=pdl),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        outs[pdl] = np.load(out)
+    for k in outs["1"].files:
+        np.testing.assert_array_equal(outs["1"][k], outs["0"][k])
