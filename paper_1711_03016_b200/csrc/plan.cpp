@@ -1449,7 +1449,14 @@ struct Planner {
     g.vec = v4 ? 4 : 1;
     int64_t cols = (C + g.vec - 1) / g.vec;
     int bx = 32;
-    while (bx < 256 && bx < cols) bx *= 2;
+    // column threads per CTA: at most 64 (by = 4 rows per step), measured on
+    // c2 (GB/s fwd / fwd+adj): bx 256 6288 / 5803, 128 6255 / 5799, 64 6293 /
+    // 5857, 32 6255 / 5835.  DLVM_EW_BX overrides.
+    static const int bx_max = [] {
+      const char* e = std::getenv("DLVM_EW_BX");
+      return e ? std::atoi(e) : 64;
+    }();
+    while (bx < bx_max && bx < cols) bx *= 2;
     g.bx = bx;
     g.by = 256 / bx;
     g.gx = (cols + bx - 1) / bx;
