@@ -510,7 +510,7 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
         if (w == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
         if (!fn->planned[w]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[w]);
         for (const Step& st : fn->plan[w].steps) {
-          if (st.kind == Step::EW)
+          if (st.kind == Step::EW && !st.ew.finalize)  // finalize has a fixed kernel of its own
             s += "EW " + std::to_string(st.ew.vec) + " " + st.ew.sig + "\n";
           else if (st.kind == Step::GEMM && st.gemm.tensor_core)
             s += "GEMM " + std::to_string(st.gemm.bn) + " " + st.gemm.epi.sig + "\n";

@@ -137,10 +137,14 @@ cudaError_t launch_ew_fn(void* fn, const EwParams& p, int bx, int by, cudaStream
 }
 
 cudaError_t launch_finalize(const EwParams& p, cudaStream_t stream) {
-  const int64_t n = p.dims[0];
-  dim3 block = n >= 32 ? dim3(32, 8) : dim3(1, 256);
-  dim3 grid((unsigned)((n + block.x - 1) / block.x));
-  LaunchCfg L(grid, block, 0, stream);
+  const int nq = p.prog.n_in > 0 ? p.prog.n_in : 1;
+  int64_t nb = 1;  // CTAs of the longest reduction (32 or 1 outputs per CTA)
+  for (int q = 0; q < nq; ++q) {
+    const int64_t n = p.dims[q];
+    const int64_t b = n >= 32 ? (n + 31) / 32 : n;
+    nb = b > nb ? b : nb;
+  }
+  LaunchCfg L(dim3((unsigned)nb, (unsigned)nq), dim3(256), 0, stream);
   cudaError_t e = cudaLaunchKernelEx(&L.cfg, finalize_kernel, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

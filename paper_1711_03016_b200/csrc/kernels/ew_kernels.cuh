@@ -262,20 +262,28 @@ __global__ void __launch_bounds__(256) ew_kernel(const __grid_constant__ EwParam
 
 #ifdef DLVM_EW_DEFINE_FIXED_KERNELS  // non-template kernels: one definition, in ew.cu
 // Deterministic finalize of reduction partials: out[e] = sum_k P[k*cs + e*es]
-// in a fixed order (threadIdx.y strides the chunks, then a fixed-order sum
-// over threadIdx.y), written to every home of the reduced value.
+// in a fixed order (a logical (ex, cy) thread grid: ty strides the chunks,
+// then a fixed-order tree over ty), written to every home of the reduced
+// value.  One launch finalizes up to kMaxIterDims reductions of one producer:
+// blockIdx.y = input q, n = dims[q] its length, its homes the stores with
+// store_slot == q.  The logical shape depends on n alone ((32, 8) for n >= 32,
+// else (1, 256)), so every sum is the one a launch of its own would produce.
 __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ EwParams p) {
   pdl_trigger();
   pdl_wait();
   __shared__ float part[256];
-  const int ex = blockDim.x, cy = blockDim.y;
-  const int64_t e = (int64_t)blockIdx.x * ex + threadIdx.x;
-  const EwDevIn& in = p.in[0];
+  const int qi = blockIdx.y;
+  const int64_t n = p.dims[qi];
+  const int ex = n >= 32 ? 32 : 1, cy = 256 / ex;
+  if ((int64_t)blockIdx.x * ex >= n) return;  // CTA-uniform: this reduction needs fewer CTAs
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, tx = tid % ex, ty = tid / ex;
+  const int64_t e = (int64_t)blockIdx.x * ex + tx;
+  const EwDevIn& in = p.in[qi];
   const float* P = reinterpret_cast<const float*>(in.ptr);
   float s = 0.f;
-  if (e < p.dims[0]) {
+  if (e < n) {
     const float* q = P + e * in.s[0];
-    int k = threadIdx.y;
+    int k = ty;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     for (; k + 3 * cy < in.nchunks; k += 4 * cy) {
       a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
@@ -286,16 +294,16 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
     for (; k < in.nchunks; k += cy) a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
     s = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
   }
-  part[threadIdx.y * ex + threadIdx.x] = s;
+  part[tid] = s;  // == part[ty * ex + tx]
   __syncthreads();
-  for (int w = cy / 2; w > 0; w >>= 1) {  // fixed-order tree over threadIdx.y
-    if (threadIdx.y < w) part[threadIdx.y * ex + threadIdx.x] =
-        __fadd_rn(part[threadIdx.y * ex + threadIdx.x], part[(threadIdx.y + w) * ex + threadIdx.x]);
+  for (int w = cy / 2; w > 0; w >>= 1) {  // fixed-order tree over ty
+    if (ty < w) part[ty * ex + tx] = __fadd_rn(part[ty * ex + tx], part[(ty + w) * ex + tx]);
     __syncthreads();
   }
-  if (threadIdx.y == 0 && e < p.dims[0]) {
-    const float t = part[threadIdx.x];
-    for (int o = 0; o < p.prog.n_stores; ++o) st1(p.out[o].ptr, e * p.out[o].s[0], p.out[o].st, t);
+  if (ty == 0 && e < n) {
+    const float t = part[tx];
+    for (int o = 0; o < p.prog.n_stores; ++o)
+      if (p.prog.store_slot[o] == qi) st1(p.out[o].ptr, e * p.out[o].s[0], p.out[o].st, t);
   }
 }
 

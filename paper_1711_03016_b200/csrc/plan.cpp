@@ -1512,8 +1512,33 @@ struct Planner {
   }
 
   // --------------------------------------------------------------- emit
+  // The reductions of one producer share ONE finalize launch (blockIdx.y
+  // selects the reduction, dims[q] is its length n_out, its stores are the
+  // ones whose store_slot names input q).  The kernel's summation order
+  // depends only on n_out, so every reduction is summed exactly as a launch of
+  // its own would (kept outputs stay bit-equal to dlvm_fn_run, reading A20).
   void finalize_reds(const std::vector<RedInfo>& reds, int step_index, int64_t gx, int64_t gy, int64_t R,
                      int64_t C, const std::string& who) {
+    EwGroup fg;
+    std::string names, shape;
+    auto flush = [&]() {
+      if (fg.inputs.empty()) return;
+      fg.prog.n_in = (uint8_t)fg.inputs.size();
+      fg.prog.n_stores = (uint8_t)fg.stores.size();
+      ew_launch(fg);
+      fg.sig = program_signature(fg.prog);
+      fg.finalize = true;
+      Step s;
+      s.kind = Step::EW;
+      s.ew = fg;
+      s.desc = "finalize " + names + " (" + shape + ") of " + who +
+               (fg.direct_buf >= 0 ? " [only when the output is bound as bf16; else written by the producer]" : "");
+      s.ew.desc = s.desc;
+      plan.steps.push_back(s);
+      fg = EwGroup();
+      names.clear();
+      shape.clear();
+    };
     for (auto& ri : reds) {
       int64_t n_out = ri.kind == RED_COL ? C : ri.kind == RED_ROW ? R : 1;
       int64_t nch = ri.kind == RED_COL ? gy : ri.kind == RED_ROW ? gx : gx * gy;
@@ -1526,9 +1551,14 @@ struct Planner {
       int pbuf = add_buf(BufferSlot::Work, -1, (size_t)(n_out * nch) * 4, SType::F32);
       pg.reduces[ri.slot_index].buf = pbuf;
       pg.reduces[ri.slot_index].direct_buf = direct;
-      EwGroup fg;
+      // a skippable finalize keeps a launch of its own; others merge while
+      // n_out matches and the input/store tables have room
+      const bool merge = !fg.inputs.empty() && direct < 0 && fg.direct_buf < 0 &&
+                         (int)fg.inputs.size() < kMaxIterDims && fg.stores.size() + homes.size() <= (size_t)kMaxStores;
+      if (!merge) flush();
       fg.ndims = 1;
-      fg.dims[0] = n_out;
+      fg.dims[fg.inputs.size()] = n_out;
+      if (fg.inputs.empty()) fg.direct_buf = direct;
       IterRef in;
       in.buf = pbuf;
       in.nchunks = (int)nch;
@@ -1541,32 +1571,23 @@ struct Planner {
       } else {
         in.chunk_stride = 1;
       }
+      const uint8_t q = (uint8_t)fg.inputs.size();
       fg.inputs.push_back(in);
-      fg.prog.n_in = 1;
-      for (auto& h : vi[ri.value].homes) {
+      for (auto& h : homes) {
         if (!h.ref.contiguous())  // the partial layout is the value's row-major order
           throw Error(kStatusRuntime, 0, 0, "planner: reduction %" + f.names[ri.value] + " has a strided home");
         IterRef o;
         o.buf = h.buf;
         o.st = h.st;
         o.strides[0] = 1;
-        fg.prog.store_slot[fg.stores.size()] = 0;
+        fg.prog.store_slot[fg.stores.size()] = q;
         fg.stores.push_back(o);
       }
-      fg.prog.n_stores = (uint8_t)fg.stores.size();
-      ew_launch(fg);
-      fg.sig = program_signature(fg.prog);
-      fg.finalize = true;
-      fg.direct_buf = direct;
-      Step s;
-      s.kind = Step::EW;
-      s.ew = fg;
-      s.desc = "finalize %" + f.names[ri.value] + " (" + std::to_string(nch) + " partials x " +
-               std::to_string(n_out) + ") of " + who +
-               (direct >= 0 ? " [only when the output is bound as bf16; else written by the producer]" : "");
-      s.ew.desc = s.desc;
-      plan.steps.push_back(s);
+      names += (names.empty() ? "%" : ", %") + f.names[ri.value];
+      shape += (shape.empty() ? "" : ", ") + std::to_string(nch) + " partials x " + std::to_string(n_out);
+      if (direct >= 0) flush();
     }
+    flush();
   }
 
   void emit_steps(const std::vector<int>& order) {

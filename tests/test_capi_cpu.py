@@ -226,7 +226,22 @@ def test_plan_launch_counts_configs():
     assert plan.count("gemm tcgen05") == 8
     assert f.num_launches(1) <= 14
     f2 = _plan_only(W.c2(64, 128).text, "chain", "chain_grad")
-    assert f2.num_launches(0) == 1 and f2.num_launches(1) == 3
+    # one fused fwd+adjoint kernel + ONE finalize for both column sums (dw, db)
+    assert f2.num_launches(0) == 1 and f2.num_launches(1) == 2
+    assert "finalize %" in f2.print(3) and f2.print(3).count("finalize") == 1
+
+
+def test_reductions_of_one_producer_share_one_finalize():
+    """Column sums (n=1000), row sums (n=3000) and a full sum (n=1) of one
+    element-wise kernel are finalized by ONE launch; the c2 adjoint's dw/db
+    and c3's loss/db3 likewise."""
+    from merged_reductions import merged_reduction_program
+    f = _plan_only(merged_reduction_program(3000, 1000), "f")
+    plan = f.print(2)
+    assert f.num_launches(0) == 2, plan
+    assert "finalize %c, %r, %t (250 partials x 1000, 4 partials x 3000, 1000 partials x 1)" in plan, plan
+    c3 = _plan_only(W.c3().text, "mlp", "mlp_grad", "bf16").print(3)
+    assert "finalize %l, %d8 (" in c3, c3
 
 
 def test_higher_order_cpp_ad_equals_oracle():

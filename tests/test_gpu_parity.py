@@ -1295,3 +1295,27 @@ def test_pdl_launches_bit_identical_to_plain_launches(tmp_path):
         outs[pdl] = np.load(out)
     for k in outs["1"].files:
         np.testing.assert_array_equal(outs["1"][k], outs["0"][k])
+
+
+def test_merged_finalize_mixed_lengths():
+    """ONE finalize launch sums three reductions of one EW kernel with
+    different lengths and partial layouts (column sums n=1000 over 250 row
+    tiles, row sums n=3000 over 4 column tiles, a full sum n=1 over 1000
+    tiles): each vs the float64 oracle within the A16 term bound, and
+    bit-identical across runs (fixed summation order)."""
+    from merged_reductions import merged_reduction_program
+    R, C = 3000, 1000
+    text = merged_reduction_program(R, C)
+    rng = np.random.default_rng(1711)
+    x = rng.uniform(-1, 1, (R, C)).astype(np.float32)
+    res = gpu_run(text, "f", None, [x], which="primal")
+    assert res["fn"].num_launches(0) == 2
+    m = oracle.parse(text)
+    x64 = x.astype(np.float64)
+    ref = oracle.run(m, "f", [x64])
+    bnd = term_bound(m, "f", [x64])
+    for k, (g, r, b) in enumerate(zip(res["primal"], ref, bnd)):
+        assert_f32_parity(g, r, b, what=f"merged finalize out{k}")
+    again = gpu_run(text, "f", None, [x], which="primal")
+    for g, h in zip(res["primal"], again["primal"]):
+        assert np.array_equal(g, h)
