@@ -1319,3 +1319,32 @@ def test_merged_finalize_mixed_lengths():
     again = gpu_run(text, "f", None, [x], which="primal")
     for g, h in zip(res["primal"], again["primal"]):
         assert np.array_equal(g, h)
+
+
+def test_merged_finalize_outputs_bound_as_bf16():
+    """Small c3 under the bf16 policy (batch 256; tcgen05 and SIMT GEMMs): the
+    last forward GEMM's loss (16 partials) and db2 (8 partials x 100) share one
+    finalize launch; with every
+    bias gradient bound as bf16 (dlvm.h output dtype policy) that launch
+    stores bf16 into some homes and f32 into others, selected per reduction:
+    each output equals bf16_round / the f32 value of the all-f32 run."""
+    import torch
+    import paper_1711_03016_b200 as P
+    w = W.c3(256, layers=[(256, 256, "relu"), (256, 100, None)])
+    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
+    assert "finalize %l, %" in f.print(3)
+    dev = torch.device("cuda:0")
+    ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
+    seed = torch.tensor(np.float32(w.seed()), device=dev)
+    ref = [o.cpu().numpy() for o in f.grad_run(ins, seed=seed)]
+    outs = f._outputs(1, dev, None)
+    bf = [k for k, o in enumerate(outs) if o.dim() == 2 and o.shape[0] == 1]
+    assert len(bf) == 2, [tuple(o.shape) for o in outs]
+    for k in bf:
+        outs[k] = torch.empty(outs[k].shape, dtype=torch.bfloat16, device=dev)
+    f.grad_run(ins, seed=seed, outputs=outs)
+    torch.cuda.synchronize()
+    for k, (o, r) in enumerate(zip(outs, ref)):
+        got = o.cpu().to(torch.float32).numpy()
+        want = bf16_round(r) if k in bf else r
+        assert np.array_equal(got.reshape(-1).view(np.uint32), np.asarray(want, np.float32).reshape(-1).view(np.uint32)), k
