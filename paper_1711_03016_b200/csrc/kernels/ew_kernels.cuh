@@ -285,11 +285,28 @@ __global__ void __launch_bounds__(256) finalize_kernel(const __grid_constant__ E
     const float* q = P + e * in.s[0];
     int k = ty;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    for (; k + 3 * cy < in.nchunks; k += 4 * cy) {
-      a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
-      a1 = __fadd_rn(a1, __ldg(q + (int64_t)(k + cy) * in.chunk_stride));
-      a2 = __fadd_rn(a2, __ldg(q + (int64_t)(k + 2 * cy) * in.chunk_stride));
-      a3 = __fadd_rn(a3, __ldg(q + (int64_t)(k + 3 * cy) * in.chunk_stride));
+    const int64_t cs = in.chunk_stride, step = (int64_t)cy * cs;
+    const float* qk = q + (int64_t)k * cs;
+    for (; k + 7 * cy < in.nchunks; k += 8 * cy, qk += 8 * step) {  // 8 loads in flight
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(qk + j * step);
+      a0 = __fadd_rn(a0, v[0]);
+      a1 = __fadd_rn(a1, v[1]);
+      a2 = __fadd_rn(a2, v[2]);
+      a3 = __fadd_rn(a3, v[3]);
+      a0 = __fadd_rn(a0, v[4]);
+      a1 = __fadd_rn(a1, v[5]);
+      a2 = __fadd_rn(a2, v[6]);
+      a3 = __fadd_rn(a3, v[7]);
+    }
+    for (; k + 3 * cy < in.nchunks; k += 4 * cy, qk += 4 * step) {
+      // all four loads issue before the adds (same summation order)
+      const float v0 = __ldg(qk), v1 = __ldg(qk + step), v2 = __ldg(qk + 2 * step), v3 = __ldg(qk + 3 * step);
+      a0 = __fadd_rn(a0, v0);
+      a1 = __fadd_rn(a1, v1);
+      a2 = __fadd_rn(a2, v2);
+      a3 = __fadd_rn(a3, v3);
     }
     for (; k < in.nchunks; k += cy) a0 = __fadd_rn(a0, __ldg(q + (int64_t)k * in.chunk_stride));
     s = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
