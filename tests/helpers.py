@@ -53,10 +53,22 @@ def gpu_run(text: str, fn: str, grad: Optional[str], inputs: Sequence[np.ndarray
     return res
 
 
+def oracle_grad_module(mod, name: str):
+    """A module-like holder of `name` canonicalised by the oracle's adjoint
+    code generation (oracle.canonical: copy of the primal, then the VJP rules
+    as IR in reverse order).  Bounds derived from it depend on the
+    oracle only."""
+    from types import SimpleNamespace
+    return SimpleNamespace(functions={name: oracle.canonical(mod, name)})
+
+
 def term_bound(mod, fname: str, inputs: Sequence[np.ndarray]) -> List[np.ndarray]:
-    """sum|terms| of the last accumulation producing each output of function
-    `fname` in `mod` (an oracle-parsed module), evaluated in float64 by the
-    oracle; |value| for outputs not produced by an accumulation."""
+    """sum|terms| of the accumulation producing each output of function
+    `fname` in `mod` (an oracle-parsed module, or oracle_grad_module),
+    evaluated in float64 by the oracle.  The bound follows the terms through
+    the linear ops that carry an accumulation's rounding error unchanged
+    (add/subtract/negate, a literal scale, select of one branch, reshapes,
+    transposes, reductions); any other op ends it at |value|."""
     fn = mod.functions[fname]
     env = oracle.interp.evaluate(fn, inputs)
     defs = {ins.result: ins for ins in fn.insts}
@@ -84,8 +96,14 @@ def term_bound(mod, fname: str, inputs: Sequence[np.ndarray]) -> List[np.ndarray
             lit = [x for x in ins.operands if x.kind == "literal"][0]
             other = [x for x in ins.operands if x.kind != "literal"][0]
             return np.broadcast_to(abs(lit.literal) * bound(other), v.shape)
-        if ins.opcode == "add":
+        if ins.opcode in ("add", "subtract"):
             return np.broadcast_to(bound(ins.operands[0]) + bound(ins.operands[1]), v.shape)
+        if ins.opcode == "negate":
+            return bound(ins.operands[0])
+        if ins.opcode == "select":
+            c = np.broadcast_to(val(ins.operands[0]), v.shape)
+            return np.where(c, np.broadcast_to(bound(ins.operands[1]), v.shape),
+                            np.broadcast_to(bound(ins.operands[2]), v.shape))
         return np.abs(v).astype(np.float64)
 
     return [np.asarray(bound(o), dtype=np.float64) for o in fn.ret]

@@ -6,15 +6,19 @@ import pytest
 
 import oracle
 import workloads as W
-from helpers import assert_f32_parity, assert_normwise, bf16_round, f32_emulation, gpu_run, term_bound
+from helpers import oracle_grad_module, assert_f32_parity, assert_normwise, bf16_round, f32_emulation, gpu_run, term_bound
 
 pytestmark = pytest.mark.gpu
 
 
-def _grad_module(res):
-    """The C++-generated adjoint function, parsed by the oracle (for bounds)."""
-    f = res["fn"]
-    return oracle.parse('module "g"\nstage optimizable\n' + f.print(1))
+def _grad_module(m, name):
+    """The gradient declaration `name` of the oracle-parsed module `m`,
+    canonicalised to IR by the ORACLE's own adjoint code generation
+    (oracle.canonical).  Tolerance bounds (sum|terms| of each
+    output's last accumulation, the fp32-emulation allowance) are derived
+    from it, never from the library's printed adjoint, so a numerically worse
+    adjoint from the C++ AD cannot widen its own tolerance."""
+    return oracle_grad_module(m, name)
 
 
 def _check_f32(w, inputs, seed, primal_only=False):
@@ -30,7 +34,7 @@ def _check_f32(w, inputs, seed, primal_only=False):
         return res
     gargs = ins64 + ([np.asarray(seed, dtype=np.float64)] if seed is not None else [])
     ref_g = oracle.run(m, w.grad, gargs)
-    gm = _grad_module(res)
+    gm = _grad_module(m, w.grad)
     bg = term_bound(gm, w.grad, gargs)
     for k, (g, r, b) in enumerate(zip(res["grad"], ref_g, bg)):
         assert_f32_parity(g, r, b, what=f"{w.name} grad out{k}")
@@ -50,7 +54,7 @@ def test_c2_chain_parity(R, C):
 
 def test_c2_full_size_sampled():
     """c2 at BASELINE size [16384, 16384], the launch configuration bench.py
-    times; checked on sampled rows (oracle per row) and on all dw/db."""
+    times; every element of y, dx, dw and db checked against the oracle."""
     import torch
     import paper_1711_03016_b200 as P
     w = W.c2()
@@ -62,28 +66,29 @@ def test_c2_full_size_sampled():
     (y,) = f.run(ins)
     dx, dw, db = f.grad_run(ins, seed=seed)
     torch.cuda.synchronize()
-    rows = np.array([0, 1, 4097, 8191, 12345, 16383])
-    xs = [a.cpu().numpy().astype(np.float64) for a in ins]
-    g = seed.cpu().numpy().astype(np.float64)
-    sub = [xs[0][rows], xs[1], xs[2], xs[3][rows]]
-    mm = oracle.parse(W.chain_ir(len(rows), 16384))
-    (yr,) = oracle.run(mm, "chain", sub)
-    assert_f32_parity(y.cpu().numpy()[rows], yr, what="c2 y rows")
-    dxr, _, _ = oracle.run(mm, "chain_grad", sub + [g[rows]])
-    assert_f32_parity(dx.cpu().numpy()[rows], dxr, what="c2 dx rows")
-    # dw, db over all 16384 rows and all columns: the oracle runs the same
-    # program on 1024-column blocks (column sums are column-local)
+    xs = [a.cpu().numpy() for a in ins]
+    g = seed.cpu().numpy()
+    yg, dxg, dwg, dbg = y.cpu().numpy(), dx.cpu().numpy(), dw.cpu().numpy(), db.cpu().numpy()
+    # every output element: the chain is row-local and column-local, so the
+    # oracle runs the same program on [16384, 1024] column blocks (all rows)
+    # and compares y and dx element by element (A16) and dw, db (A17)
     B = 1024
     mb = oracle.parse(W.chain_ir(16384, B))
-    gb = oracle.parse('module "g"\nstage optimizable\n' +
-                      P.Function(W.chain_ir(16384, B), "chain", "chain_grad", flags=P.DLVM_PLAN_ONLY).print(1))
-    dwg, dbg = dw.cpu().numpy(), db.cpu().numpy()
+    gb = _grad_module(mb, "chain_grad")
+    h = lambda a: np.ascontiguousarray(a, dtype=np.float64)
     for c0 in range(0, 16384, B):
-        blk = [xs[0][:, c0:c0 + B], xs[1][:, c0:c0 + B], xs[2][:, c0:c0 + B], xs[3][:, c0:c0 + B], g[:, c0:c0 + B]]
-        _, rdw, rdb = oracle.run(mb, "chain_grad", blk)
+        cs = slice(c0, c0 + B)
+        blk = [h(xs[0][:, cs]), h(xs[1][:, cs]), h(xs[2][:, cs]), h(xs[3][:, cs])]
+        (ry,) = oracle.run(mb, "chain", blk)
+        assert_f32_parity(yg[:, cs], ry, what=f"c2 y cols {c0}+")
+        del ry
+        blk.append(h(g[:, cs]))
+        rdx, rdw, rdb = oracle.run(mb, "chain_grad", blk)
+        assert_f32_parity(dxg[:, cs], rdx, what=f"c2 dx cols {c0}+")
+        del rdx
         _, bdw, bdb = term_bound(gb, "chain_grad", blk)
-        assert_f32_parity(dwg[:, c0:c0 + B], rdw, bdw, what=f"c2 dw cols {c0}+")
-        assert_f32_parity(dbg[:, c0:c0 + B], rdb, bdb, what=f"c2 db cols {c0}+")
+        assert_f32_parity(dwg[:, cs], rdw, bdw, what=f"c2 dw cols {c0}+")
+        assert_f32_parity(dbg[:, cs], rdb, bdb, what=f"c2 db cols {c0}+")
 
 
 def test_fig3_fig4_programs():
@@ -99,7 +104,7 @@ def test_fig3_fig4_programs():
     ins = [rng.uniform(-1, 1, t.shape).astype(np.float32) for t in m4.functions["g"].param_types]
     res = gpu_run(text, "g", "dg", ins)
     ref = oracle.run(m4, "dg", [x.astype(np.float64) for x in ins])
-    bg = term_bound(_grad_module(res), "dg", [x.astype(np.float64) for x in ins])
+    bg = term_bound(_grad_module(m4, "dg"), "dg", [x.astype(np.float64) for x in ins])
     for k, (g, r, b) in enumerate(zip(res["grad"], ref, bg)):
         assert_f32_parity(g, r, b, what=f"fig4 out{k}")
 
@@ -185,12 +190,17 @@ def _check_c3(w, policy_tol=2e-2):
     ref_pol = oracle.run(m, w.grad, args, dot_policy="bf16")
     ref_raw = oracle.run(m, w.grad, args)
     n = len(w.layers)
+    kinked = any(act == "relu" for _, _, act in w.layers)
     rels = []
     for k, (g, rp, rr) in enumerate(zip(res["grad"], ref_pol, ref_raw)):
         rels.append(assert_normwise(g, rp, policy_tol, what=f"{w.name} grad out{k} vs bf16-policy oracle"))
-        if k >= 2 * (n - 1):  # last layer dW, db and the kept loss
+        # A18 against the unrounded oracle: every output of a kink-free
+        # (tanh) network; behind a ReLU only the outputs whose adjoint
+        # crosses no kink (last layer dW, db and the kept loss)
+        if not kinked or k >= 2 * (n - 1):
             assert_normwise(g, rr, 2e-2, what=f"{w.name} grad out{k} vs unrounded oracle")
     assert_normwise(res["primal"][0], oracle.run(m, w.fn, args[:-1], dot_policy="bf16")[0], policy_tol)
+    assert_normwise(res["primal"][0], oracle.run(m, w.fn, args[:-1])[0], 2e-2, what=f"{w.name} loss vs unrounded")
     return rels
 
 
@@ -283,7 +293,7 @@ def test_random_programs(seed):
     rp = oracle.run(m, "f", ins64)[0]
     assert_f32_parity(res["primal"][0], rp, term_bound(m, "f", ins64)[0], what="random primal")
     ref = oracle.run(m, "g", ins64)
-    gm = _grad_module(res)
+    gm = _grad_module(m, "g")
     bg = term_bound(gm, "g", ins64)
     emu = f32_emulation(gm, "g", ins64)   # fp32 conditioning of this random program
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, bg, emu)):
@@ -395,14 +405,14 @@ def test_higher_order_fig4_d2g_dw2_f32():
            for p, s in zip(m.functions["g"].param_types, (1.0, 0.1, 0.1))]
     res = gpu_run(t, "dg", "d2g_dw2", ins)
     ins64 = [x.astype(np.float64) for x in ins]
-    bp = term_bound(oracle.parse('module "p"\nstage raw\n' + res["fn"].print(0)), "dg", ins64)
+    bp = term_bound(_grad_module(m, "dg"), "dg", ins64)
     # out2 = tanh(x.w + b): the dot's accumulation error passes through the
     # 1-Lipschitz tanh, so its bound is the pre-activation's sum|terms|
     bp[2] = np.abs(ins64[0]) @ np.abs(ins64[1]) + np.abs(ins64[2])
     for k, (g, r) in enumerate(zip(res["primal"], oracle.run(m, "dg", ins64))):
         assert_f32_parity(g, r, bp[k], what=f"dg out{k}")
     (ref,) = oracle.run(m, "d2g_dw2", ins64)
-    bound = term_bound(_grad_module(res), "d2g_dw2", ins64)[0]
+    bound = term_bound(_grad_module(m, "d2g_dw2"), "d2g_dw2", ins64)[0]
     assert_f32_parity(res["grad"][0], ref, bound, what="d2g_dw2")
 
 
@@ -424,7 +434,7 @@ def test_higher_order_mlp_hessian_vector_product(prec, dims):
     if prec == "f32":
         res = gpu_run(text, "df", "hvp", ins, seed=v, which="grad")
         ref = oracle.run(m, "hvp", ins64)
-        bounds = term_bound(_grad_module(res), "hvp", ins64)
+        bounds = term_bound(_grad_module(m, "hvp"), "hvp", ins64)
         for k, (g, r, b) in enumerate(zip(res["grad"], ref, bounds)):
             assert_f32_parity(g, r, b, what=f"hvp out{k}")
     else:
@@ -651,10 +661,10 @@ def test_c2_tall_thin_column():
     assert_f32_parity(y.cpu().numpy()[rows], yr, what="tall y rows")
     dxr, _, _ = oracle.run(mm, "chain_grad", sub + [g[rows].astype(np.float64)])
     assert_f32_parity(dx.cpu().numpy()[rows], dxr, what="tall dx rows")
-    # full column sums: the oracle on the whole column, bounds from the C++ adjoint IR
+    # full column sums: the oracle on the whole column, bounds from the oracle's adjoint IR
     full = [x.astype(np.float64) for x in xs] + [g.astype(np.float64)]
     _, rdw, rdb = oracle.run(oracle.parse(w.text), "chain_grad", full)
-    gm = oracle.parse('module "g"\nstage optimizable\n' + f.print(1))
+    gm = _grad_module(oracle.parse(w.text), "chain_grad")
     _, bdw, bdb = term_bound(gm, "chain_grad", full)
     assert_f32_parity(db.cpu().numpy(), rdb, bdb, what="db")
     assert_f32_parity(dw.cpu().numpy(), rdw, bdw, what="dw")
@@ -732,7 +742,7 @@ def test_random_nd_programs(seed):
     rp = oracle.run(m, "f", ins64)[0]
     assert_f32_parity(res["primal"][0], rp, term_bound(m, "f", ins64)[0], what="nd primal\n" + text)
     ref = oracle.run(m, "g", ins64)
-    gm = _grad_module(res)
+    gm = _grad_module(m, "g")
     bg = term_bound(gm, "g", ins64)
     emu = f32_emulation(gm, "g", ins64)
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, bg, emu)):
@@ -806,7 +816,7 @@ def test_random_nd_programs_wide(seed, prec):
         return
     assert_f32_parity(res["primal"][0], oracle.run(m, "f", ins64)[0], term_bound(m, "f", ins64)[0], what="wide loss")
     ref = oracle.run(m, "g", ins64)
-    gm = _grad_module(res)
+    gm = _grad_module(m, "g")
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, term_bound(gm, "g", ins64), f32_emulation(gm, "g", ins64))):
         assert_f32_parity(g, r, b, what=f"wide grad out{k}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
     for k, (g, r, b, e) in enumerate(zip(gs, rs, term_bound(mb, "f", ins64), f32_emulation(mb, "f", ins64))):
@@ -836,7 +846,7 @@ def test_random_gradient_configurations(seed):
     ins64 = [x.astype(np.float64) for x in ins]
     gargs = ins64 + ([seed_v.astype(np.float64)] if seed_v is not None else [])
     ref = oracle.run(m, "g", gargs)
-    gm = _grad_module(res)
+    gm = _grad_module(m, "g")
     for k, (g, r, b, e) in enumerate(zip(res["grad"], ref, term_bound(gm, "g", gargs), f32_emulation(gm, "g", gargs))):
         assert_f32_parity(g, r, b, what=f"grad-config out{k} {cfg}\n{text}", extra=4.0 * float(np.max(np.abs(e - r))))
 
@@ -916,8 +926,7 @@ def test_c2_beyond_int32_element_count():
     assert_f32_parity(h(y[rows]), oracle.run(mr, "chain", sub)[0], what="y rows")
     assert_f32_parity(h(dx[rows]), oracle.run(mr, "chain_grad", sub + [h(s[rows])])[0], what="dx rows")
     mc = oracle.parse(W.chain_ir(R, 1))
-    gc = oracle.parse('module "g"\nstage optimizable\n' +
-                      P.Function(W.chain_ir(R, 1), "chain", "chain_grad", flags=P.DLVM_PLAN_ONLY).print(1))
+    gc = _grad_module(mc, "chain_grad")
     for j in (0, 1, 511, C - 1):
         col = [h(x[:, j:j + 1]), h(w[:, j:j + 1]), h(b[:, j:j + 1]), h(m[:, j:j + 1]), h(s[:, j:j + 1])]
         _, rdw, rdb = oracle.run(mc, "chain_grad", col)
@@ -960,13 +969,12 @@ def test_tcgen05_epilogue_unaligned_byte_rows(N):
                torch.from_numpy(t != 0).to(dev)]  # t passed as bool bytes
         d, g, s = f.run(ins)
         torch.cuda.synchronize()
-        assert_f32_parity(d.cpu().numpy().astype(np.float64), ref[0], np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64)) + 1,
-                          what=f"d N={N} jit={jit}")
+        # sum|terms| of d = select(c, a.b, 0) - t is |a|.|b| where c holds, plus |t|
+        bnd = term_bound(m, "f", [a.astype(np.float64), b.astype(np.float64), c, t.astype(np.float64)])
+        assert_f32_parity(d.cpu().numpy().astype(np.float64), ref[0], bnd[0], what=f"d N={N} jit={jit}")
         gd = d.cpu().numpy()
         np.testing.assert_array_equal(g.cpu().numpy(), gd > 0)  # the stored compare agrees with the stored value
-        assert_f32_parity(s.cpu().numpy().astype(np.float64), ref[2],
-                          term_bound(m, "f", [a.astype(np.float64), b.astype(np.float64), c, t.astype(np.float64)])[2] * 16,
-                          what=f"colsum N={N} jit={jit}")
+        assert_f32_parity(s.cpu().numpy().astype(np.float64), ref[2], bnd[2], what=f"colsum N={N} jit={jit}")
 
 
 def test_c4_full_size_in_bench_launch_configuration():
@@ -1141,7 +1149,7 @@ def test_op_sweep_every_vm_opcode():
         else:
             assert_f32_parity(g, r, b, what=f"op sweep out{k}", extra=4.0 * float(np.max(np.abs(e - r))))
     refg = oracle.run(m, "g", ins64)
-    gm = _grad_module(res)
+    gm = _grad_module(m, "g")
     bg = term_bound(gm, "g", ins64)
     eg = f32_emulation(gm, "g", ins64)
     for k, (g, r, b, e) in enumerate(zip(res["grad"], refg, bg, eg)):

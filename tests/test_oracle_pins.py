@@ -211,7 +211,7 @@ def test_F12_seed_scaling_bit_exact():
 
 # --- F14: finite differences on every adjoint rule --------
 
-UN = ["negate", "tanh", "exp", "log", "sqrt", "abs"]
+UN = ["negate", "tanh", "exp", "log", "sqrt", "abs", "sign"]
 BIN = ["add", "subtract", "multiply", "divide", "power"]
 
 
@@ -464,3 +464,144 @@ def test_reduce_multiply_forward_pins():
             assert got[idx] == pytest.approx(p, rel=1e-14, abs=0)
         e = oracle.run(_prod_module(x.shape, ax), "f", [np.exp(x)])[0]
         np.testing.assert_allclose(e, np.exp(x.sum(axis=ax)), rtol=1e-13)
+
+
+# --- bf16-policy VJP (reading A15, A18'): pinned by triple loops ---
+#
+# Under the bf16 dot policy every `dot` -- the forward ones and the two dots of
+# each `dot` adjoint (dot(g, transpose b), dot(transpose a, g)) --
+# rounds its operands RNE to bf16 (from their f32 value) and accumulates the
+# exact products; element-wise math is not rounded.  The expected values below
+# are written with torch's bf16 conversion (an implementation independent of
+# oracle.interp.bf16_round) and Python triple loops.
+
+def _tbf16(a):
+    import torch
+    t = torch.from_numpy(np.asarray(a, dtype=np.float64)).to(torch.float32).to(torch.bfloat16)
+    return t.to(torch.float64).numpy()
+
+
+def _loop_matmul(a, b):
+    m, k = a.shape
+    k2, n = b.shape
+    assert k == k2
+    out = np.zeros((m, n))
+    for i in range(m):
+        for j in range(n):
+            s = 0.0
+            for t in range(k):
+                s += a[i, t] * b[t, j]
+            out[i, j] = s
+    return out
+
+
+def _dot_grad_text(M, K, N):
+    A, B, Y = f"<{M} x {K} x f32>", f"<{K} x {N} x f32>", f"<{M} x {N} x f32>"
+    return (f'module "p"\nstage raw\nfunc @f: ({A}, {B}) -> {Y} {{\n'
+            f"'entry(%x: {A}, %w: {B}):\n    %y = dot %x: {A}, %w: {B}\n    return %y: {Y}\n}}\n\n"
+            f"[gradient @f wrt 0, 1 seedable]\nfunc @g: ({A}, {B}, {Y}) -> ({A}, {B})\n")
+
+
+def test_bf16_policy_dot_vjp_rounds_operands_and_seed():
+    """One `dot` with a seed that is not bf16-representable (1/3 and random
+    values): dX = bf16(g)·bf16(W)ᵀ and dW = bf16(x)ᵀ·bf16(g) by triple loops.
+    Not rounding g, or rounding the products instead of the operands, moves
+    the result by ~1e-3 relative and fails the 1e-12 check."""
+    M, K, N = 3, 5, 4
+    m = oracle.parse(_dot_grad_text(M, K, N))
+    rng = np.random.default_rng(41)
+    x, w = rng.normal(size=(M, K)), rng.normal(size=(K, N))
+    for g in (np.full((M, N), 1.0 / 3.0), rng.normal(size=(M, N))):
+        dx, dw = oracle.run(m, "g", [x, w, g], dot_policy="bf16")
+        want_dx = _loop_matmul(_tbf16(g), _tbf16(w).T)
+        want_dw = _loop_matmul(_tbf16(x).T, _tbf16(g))
+        np.testing.assert_allclose(dx, want_dx, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(dw, want_dw, rtol=1e-12, atol=0)
+        # the unrounded VJP is measurably different (the policy is not a no-op)
+        ux, uw = oracle.run(m, "g", [x, w, g])
+        assert np.max(np.abs(uw - want_dw)) > 1e-5 * np.max(np.abs(want_dw))
+
+
+def test_bf16_policy_two_layer_vjp_by_hand():
+    """z = x·W1, h = tanh z, y = h·W2 under the bf16 policy with seed g:
+    dW2 = bf16(h)ᵀ·bf16(g), dh = bf16(g)·bf16(W2)ᵀ (not rounded: it is
+    element-wise input), dz = dh ⊙ (1 − h²) with h = tanh(bf16(x)·bf16(W1)),
+    dW1 = bf16(x)ᵀ·bf16(dz).  Triple loops; the adjoint dZ is rounded where
+    it enters the weight-gradient dot, as the GPU stores it (bf16)."""
+    B, I, H, O = 4, 6, 5, 3
+    X, W1, W2, Z, Y = (f"<{B} x {I} x f32>", f"<{I} x {H} x f32>", f"<{H} x {O} x f32>",
+                       f"<{B} x {H} x f32>", f"<{B} x {O} x f32>")
+    text = (f'module "p"\nstage raw\nfunc @f: ({X}, {W1}, {W2}) -> {Y} {{\n'
+            f"'entry(%x: {X}, %w1: {W1}, %w2: {W2}):\n"
+            f"    %z = dot %x: {X}, %w1: {W1}\n    %h = tanh %z: {Z}\n"
+            f"    %y = dot %h: {Z}, %w2: {W2}\n    return %y: {Y}\n}}\n\n"
+            f"[gradient @f wrt 1, 2 seedable]\nfunc @g: ({X}, {W1}, {W2}, {Y}) -> ({W1}, {W2})\n")
+    m = oracle.parse(text)
+    rng = np.random.default_rng(43)
+    x, w1, w2 = rng.normal(size=(B, I)), rng.normal(size=(I, H)) * 0.5, rng.normal(size=(H, O))
+    g = np.full((B, O), 1.0 / 3.0) + rng.normal(size=(B, O)) * 0.1
+    dw1, dw2 = oracle.run(m, "g", [x, w1, w2, g], dot_policy="bf16")
+    h = np.tanh(_loop_matmul(_tbf16(x), _tbf16(w1)))
+    want_dw2 = _loop_matmul(_tbf16(h).T, _tbf16(g))
+    dh = _loop_matmul(_tbf16(g), _tbf16(w2).T)
+    dz = dh * (1.0 - h * h)
+    want_dw1 = _loop_matmul(_tbf16(x).T, _tbf16(dz))
+    np.testing.assert_allclose(dw2, want_dw2, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(dw1, want_dw1, rtol=1e-12, atol=1e-15)
+    # and its forward loss under the policy
+    (y,) = oracle.run(m, "f", [x, w1, w2], dot_policy="bf16")
+    np.testing.assert_allclose(y, _loop_matmul(_tbf16(h), _tbf16(w2)), rtol=1e-12, atol=1e-15)
+
+
+def test_bf16_policy_vjp_equals_plain_vjp_on_dyadic_data():
+    """On bf16-exact dyadic inputs and seed every rounding is the identity and
+    every product and sum is exact in f64: policy VJP == plain VJP, bit for bit."""
+    M, K, N = 4, 6, 3
+    m = oracle.parse(_dot_grad_text(M, K, N))
+    rng = np.random.default_rng(47)
+    vals = np.array([-2.0, -1.0, -0.5, -0.25, 0.0, 0.25, 0.5, 1.0, 1.5, 2.0])
+    x, w, g = (rng.choice(vals, size=s) for s in ((M, K), (K, N), (M, N)))
+    pol = oracle.run(m, "g", [x, w, g], dot_policy="bf16")
+    plain = oracle.run(m, "g", [x, w, g])
+    for a, b in zip(pol, plain):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(plain[0], _loop_matmul(g, w.T))
+    np.testing.assert_array_equal(plain[1], _loop_matmul(x.T, g))
+
+
+def test_F14_fd_sign():
+    """sign has derivative 0 away from 0 (S:L338 via S:L365): FD of
+    sum(seed * sign(a) * a) = sum(seed * |a|) must equal seed * sign(a),
+    which needs the sign rule to contribute exactly 0 (a wrong rule that
+    passes g through would add seed * a)."""
+    T = "<3 x 4 x f32>"
+    text = (f'module "s"\nstage raw\nfunc @f: ({T}) -> {T} {{\n\'entry(%a: {T}):\n'
+            f"    %s = sign %a: {T}\n    %r = multiply %s: {T}, %a: {T}\n    return %r: {T}\n}}\n")
+    rng = np.random.default_rng(5)
+    a = rng.uniform(0.2, 2.0, (3, 4)) * rng.choice([-1, 1], (3, 4))
+    _fd_check(text, "f", [a], [0])
+    src = oracle.parse(text).functions["f"]
+    seed = np.random.default_rng(7).uniform(-1, 1, (3, 4))
+    (g,) = oracle.grad(src, [a], wrt=[0], seed=seed)
+    np.testing.assert_allclose(g, seed * np.sign(a), rtol=1e-14, atol=0)
+    # the sign rule alone is zero
+    t2 = f'module "s"\nstage raw\nfunc @f: ({T}) -> {T} {{\n\'entry(%a: {T}):\n    %s = sign %a: {T}\n    return %s: {T}\n}}\n'
+    (g0,) = oracle.grad(oracle.parse(t2).functions["f"], [a], wrt=[0], seed=seed)
+    np.testing.assert_array_equal(g0, np.zeros((3, 4)))
+    _fd_check(t2, "f", [a], [0])
+
+
+def test_F14_fd_dataTypeCast_f32_to_f64():
+    """dataTypeCast between float types is the identity on values (the
+    oracle evaluates both in float64), so its adjoint passes the incoming
+    adjoint through (cast back to the operand type): FD of
+    sum(seed * tanh(cast(a))^2)."""
+    T, T64 = "<3 x 4 x f32>", "<3 x 4 x f64>"
+    text = (f'module "c"\nstage raw\nfunc @f: ({T}) -> {T64} {{\n\'entry(%a: {T}):\n'
+            f"    %c = dataTypeCast %a: {T} to f64\n    %t = tanh %c: {T64}\n"
+            f"    %r = multiply %t: {T64}, %t: {T64}\n    return %r: {T64}\n}}\n")
+    a = np.random.default_rng(6).uniform(-1.5, 1.5, (3, 4))
+    _fd_check(text, "f", [a], [0])
+    src = oracle.parse(text).functions["f"]
+    (g,) = oracle.grad(src, [a], wrt=[0])
+    np.testing.assert_allclose(g, 2 * np.tanh(a) * (1 - np.tanh(a) ** 2), rtol=1e-14)
