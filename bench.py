@@ -15,9 +15,12 @@ fp32 elements) as `fused_elementwise` (HBM GB/s) when N == 1.
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 synchronize, CUDA events on the launching stream, max over ranks.  Inputs
 are larger than L2 (x alone is 512 MiB per rank at N=1).  Per-kernel times
-come from CUDA events recorded between launches (dlvm_fn_launch_events) in
-the same timed steps; `roofline` reports the dominant kernel class (the
-tcgen05 GEMMs) against the measured sustained bf16 peak.
+come from CUPTI kernel activity records in a separate short pass after the
+timed region (PDL overlap intact); `roofline` reports the dominant kernel
+(the longest GEMM) against the measured bf16 peak -- burst for timed regions
+under 2 s, sustained beyond -- and the GEMM class from exclusive times.
+`--gpus N` outside torchrun re-runs the command as N ranks under
+torch.distributed.run.  Per-kernel lists go to a detail file (`--detail`).
 """
 
 from __future__ import annotations
@@ -176,10 +179,51 @@ def time_steps(step, K, dev, world, group=None):
 
 
 def kernel_breakdown(f, which, step, K, dev):
-    """Per-launch CUDA-event times over K steps (events recorded between the
-    launches on the launching stream).  Returns a list of dicts."""
+    """Per-launch device times of K steps from CUPTI kernel activity records
+    (torch.profiler / kineto), which -- unlike CUDA events recorded between
+    launches -- leave programmatic dependent launch (PDL) overlap intact.
+    For launch i: `ms` = mean CUPTI duration (start to end of the kernel,
+    including any PDL wait at its griddepcontrol.wait) and `excl_ms` = the
+    part of the step timeline it alone accounts for (end minus the later of
+    its start and every earlier kernel's end), so the exclusive times of a
+    step add up to its busy time.  Falls back to inter-launch events (marked
+    `timing: events`) if the activity records do not match the plan."""
     import torch
     n = f.num_launches(which)
+    out = None
+    try:
+        from torch.autograd import DeviceType
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize(dev)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(K):
+                step()
+            torch.cuda.synchronize(dev)
+        ks = [e for e in prof.profiler.kineto_results.events()
+              if e.device_type() == DeviceType.CUDA and "memcpy" not in e.name().lower()
+              and "memset" not in e.name().lower()]
+        ks.sort(key=lambda e: e.start_ns())
+        if len(ks) == K * n:
+            dur = [[0.0] * K for _ in range(n)]
+            exc = [[0.0] * K for _ in range(n)]
+            names = [""] * n
+            last_end = None
+            for j, e in enumerate(ks):
+                k, i = divmod(j, n)
+                s0, e0 = e.start_ns(), e.start_ns() + e.duration_ns()
+                dur[i][k] = e.duration_ns() * 1e-6
+                exc[i][k] = max(0, e0 - (s0 if last_end is None else max(s0, last_end))) * 1e-6
+                last_end = e0 if last_end is None else max(last_end, e0)
+                names[i] = e.name()
+            out = []
+            for i in range(n):
+                desc, flops, nbytes = f.launch_info(which, i)
+                out.append({"desc": desc, "kernel": names[i][:60], "ms": statistics.mean(dur[i]),
+                            "excl_ms": statistics.mean(exc[i]), "flops": flops, "bytes": nbytes, "timing": "cupti"})
+    except Exception:  # noqa: BLE001
+        out = None
+    if out is not None:
+        return out
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(K)]
     for row in evs:
         for e in row:
@@ -193,9 +237,36 @@ def kernel_breakdown(f, which, step, K, dev):
     out = []
     for i in range(n):
         desc, flops, nbytes = f.launch_info(which, i)
-        ms = [evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K)]
-        out.append({"desc": desc, "ms": statistics.mean(ms), "flops": flops, "bytes": nbytes})
+        ms = statistics.mean(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K))
+        out.append({"desc": desc, "ms": ms, "excl_ms": ms, "flops": flops, "bytes": nbytes, "timing": "events"})
     return out
+
+
+def gemm_roofline(kb, pk, region_s):
+    """Tensor roofline of a step's GEMMs.  `achieved` is the DOMINANT kernel's
+    algorithmic FLOP (2*M*N*K summed over K segments) / its mean CUPTI
+    duration.  Peak: the measured burst bf16 figure for timed regions under
+    2 s (they run at max clock), the sustained one for longer regions
+    (MEASURED_PEAKS.json; both fractions reported).  The GEMM class
+    (all tcgen05/SIMT dots) is reported from exclusive times."""
+    gemm = [r for r in kb if r["flops"] > 0]
+    if not gemm:
+        return None
+    top = max(gemm, key=lambda r: r["ms"])
+    burst, sus = pk["bf16_tflops"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    peak, kind = (burst, "burst") if region_s < 2.0 else (sus, "sustained")
+    ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
+    g_ms = sum(r["excl_ms"] for r in gemm)
+    g_fl = sum(r["flops"] for r in gemm)
+    cls = g_fl / (g_ms * 1e-3) / 1e12 if g_ms else 0.0
+    busy = sum(r["excl_ms"] for r in kb)
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(ach / peak, 4), "traffic": None, "kernel": top["desc"][:100],
+            "kernel_ms": round(top["ms"], 4), "kernel_flops": top["flops"], "timing": top["timing"],
+            "peak_kind": f"{kind} bf16 ({pk['source']})", "frac_of_burst": round(ach / burst, 4),
+            "frac_of_sustained": round(ach / sus, 4),
+            "gemm_class": {"tflops": round(cls, 1), "frac_of_burst": round(cls / burst, 4),
+                           "share_of_step": round(g_ms / busy, 4) if busy else None, "launches": len(gemm)}}
 
 
 # -------------------------------------------------------- cpu baseline
@@ -286,14 +357,19 @@ def bench_chain(dev, K, W_):
     kb = kernel_breakdown(f, 1, adj, min(K, 5), dev)
     main = max(kb, key=lambda r: r["ms"])
     pk = peaks()
-    gbs_a = ba / (main["ms"] * 1e-3) / 1e9
-    return {"workload": "c2_chain [16384,16384] f32", "fwd_ms": ms_f, "fwd_gbs": bf / (ms_f * 1e-3) / 1e9,
-            "fwd_adj_ms": ms_a, "fwd_adj_gbs": ba / (ms_a * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "achieved": gbs_a, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": gbs_a / pk["hbm_gbs"],
+    hb = pk["hbm_gbs"]
+    gbs_k = ba / (main["ms"] * 1e-3) / 1e9
+    gbs_f, gbs_a = bf / (ms_f * 1e-3) / 1e9, ba / (ms_a * 1e-3) / 1e9
+    detail = {"fwd_adj_kernels": [{"desc": r["desc"][:100], "ms": round(r["ms"], 4), "excl_ms": round(r["excl_ms"], 4)}
+                                  for r in kb]}
+    return {"workload": "c2_chain [16384,16384] f32", "fwd_ms": round(ms_f, 4), "fwd_gbs": round(gbs_f, 1),
+            "fwd_frac": round(gbs_f / hb, 4), "fwd_adj_ms": round(ms_a, 4), "fwd_adj_gbs": round(gbs_a, 1),
+            "fwd_adj_frac": round(gbs_a / hb, 4),
+            "roofline": {"bound": "hbm", "achieved": round(gbs_k, 1), "peak": hb, "unit": "GB/s",
+                         "frac": round(gbs_k / hb, 4),
                          "traffic": (ncu_traffic("c2_chain") or {}).get("traffic_bytes"),
-                         "kernel": main["desc"][:90], "algorithmic_bytes": ba},
-            "launches_fwd_adj": f.num_launches(1), "kernels": [{"desc": r["desc"][:80], "ms": r["ms"]} for r in kb]}
+                         "kernel": main["desc"][:80], "algorithmic_bytes": ba, "timing": main["timing"]},
+            "launches_fwd_adj": f.num_launches(1)}, detail
 
 
 def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
@@ -316,18 +392,13 @@ def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
         step()
     ms = time_steps(step, K, dev, 1)
     kb = kernel_breakdown(f, 1, step, min(K, 5), dev)
-    gemm = [r for r in kb if r["flops"] > 0]
-    flops = sum(r["flops"] for r in gemm)
-    gemm_ms = sum(r["ms"] for r in gemm)
+    flops = sum(r["flops"] for r in kb)
     pk = peaks()
-    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    ach = flops / (gemm_ms * 1e-3) / 1e12
-    out = {"workload": w.name, "value": w.global_batch / (ms * 1e-3), "unit": "samples/s", "ms_per_step": ms,
-           "step_tflops": flops / (ms * 1e-3) / 1e12, "launches": f.num_launches(1),
-           "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                        "kernel": "all GEMMs of the step", "algorithmic_flops_per_step": flops,
-                        "gemm_share_of_step": gemm_ms / sum(r["ms"] for r in kb)},
-           "kernels": [{"desc": r["desc"][:110], "ms": round(r["ms"], 4)} for r in sorted(kb, key=lambda r: -r["ms"])[:6]]}
+    out = {"workload": w.name, "value": round(w.global_batch / (ms * 1e-3), 1), "unit": "samples/s",
+           "ms_per_step": round(ms, 4), "step_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+           "step_frac_of_burst": round(flops / (ms * 1e-3) / 1e12 / pk["bf16_tflops"], 4),
+           "launches": f.num_launches(1), "roofline": gemm_roofline(kb, pk, ms * K * 1e-3)}
+    detail = [{"desc": r["desc"][:110], "ms": round(r["ms"], 4), "excl_ms": round(r["excl_ms"], 4)} for r in kb]
     try:
         cores = oracle_threads()
         ws_ = small(cpu_rows)
@@ -343,7 +414,33 @@ def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
                                "sample": f"{cpu_rows} rows of {w.name} (full-size weights), float64 numpy ({dt:.2f} s)"}
     except Exception as ex:  # noqa: BLE001
         out["cpu_baseline"] = {"error": repr(ex)}
-    return out
+    return out, detail
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-run this command as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def write_detail(args, detail):
+    """Per-kernel lists and the other long records go to a file, so the one
+    JSON line stays short (`--detail PATH`; default gpurun_out/ when it
+    exists)."""
+    path = args.detail
+    if path is None and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        path = os.path.join(ROOT, "gpurun_out", f"bench_detail_{args.workload}_n{detail['n_gpus']}.json")
+    if path:
+        with open(path, "w") as fh:
+            json.dump(detail, fh, indent=1)
+    return path
 
 
 def main():
@@ -355,17 +452,23 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-elementwise", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-f32", action="store_true", help="skip the e2e variant with f32 host inputs")
     ap.add_argument("--no-next", action="store_true", help="skip the rnn / mlp_hvp legs (SURVEY §8(f) rows)")
     ap.add_argument("--no-configs", action="store_true", help="skip the c3 leg (BASELINE config 3, batch 1024)")
     ap.add_argument("--cpu-rows", type=int, default=None)
+    ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: on for the launch-bound c1)")
     args = ap.parse_args()
     W_ = max(3, args.warmup)
     K = args.steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     import workloads as WL
 
     def make_workload():
@@ -412,10 +515,11 @@ def main():
     import paper_1711_03016_b200 as P
     from paper_1711_03016_b200.dp import DataParallelStep
 
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
     pk = peaks()
     w = make_workload()
     f, dev_in, seed, host, n_grads = mlp_setup(w, dev, rank)
@@ -475,48 +579,43 @@ def main():
         clk.window = (t0, time.time())
     clocks = clk.summary()
     value = w.global_batch / (ms * 1e-3)
-    # per-kernel breakdown (separate short pass with inter-launch events)
+    # per-kernel breakdown: a separate short pass under CUPTI activity tracing
+    # (the timed region above runs without any profiler)
     kb = kernel_breakdown(f, 1, eager_step, min(K, 5), dev)
-    gemm = [r for r in kb if r["flops"] > 0]
-    gemm_ms = sum(r["ms"] for r in gemm)
-    gemm_flops = sum(r["flops"] for r in gemm)
-    step_flops = gemm_flops
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
-    tc = [r for r in gemm if "tcgen05" in r["desc"]]
-    roof = {"bound": "tensor", "achieved": achieved, "peak": pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
-            "unit": "TFLOP/s", "frac": achieved / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
-            "traffic": None, "kernel": "gemm_tcgen05 (all dots of the step)",
-            "peak_kind": "sustained bf16 " + pk["source"], "frac_of_burst": achieved / pk["bf16_tflops"],
-            "gemm_share_of_step": gemm_ms / sum(r["ms"] for r in kb) if kb else None,
-            "algorithmic_flops_per_step": step_flops, "tcgen05_launches": len(tc)}
+    roof = gemm_roofline(kb, pk, ms * K * 1e-3)
     tr = ncu_traffic(w.name)
-    if tr:
+    if tr and roof:
         roof["traffic"] = tr["traffic_bytes"]
         roof["traffic_kernel"] = tr["kernel"]
-        roof["traffic_algorithmic_bytes"] = tr["algorithmic_bytes"]
         roof["traffic_source"] = tr["source"]
+    step_flops = sum(r["flops"] for r in kb)
     launches = (f.num_launches(1) + (sgd_info["launches"] if sgd_info else 0)) * K
-    # end to end: H2D of this step's batch (pinned host) + step + D2H of the loss
-    e2e = None
-    if not args.no_e2e:
-        # Every step copies its own batch (x, t) from pinned host memory and
-        # reads the loss back.  Two device copies of the batch arguments
-        # alternate: step k's upload runs on a copy stream while step k-1
-        # computes (the copy of step k must finish before step k starts).
+    detail = {"n_gpus": world, "workload": w.name,
+              "kernels": [{"desc": r["desc"][:120], "kernel": r.get("kernel"), "ms": round(r["ms"], 4),
+                           "excl_ms": round(r["excl_ms"], 4), "flops": r["flops"], "bytes": r["bytes"],
+                           "timing": r["timing"]} for r in kb]}
+
+    def e2e_leg(f32_inputs: bool):
+        """End to end through the public API: every step copies its own batch
+        (x, t) from pinned host memory and reads the loss back.  Two device
+        copies of the batch arguments alternate: step k+1's upload runs on a
+        copy stream while step k computes.  `f32_inputs`: x is uploaded in
+        the IR's f32 type (the library casts it for the bf16 dots) instead of
+        the bf16 storage form dlvm.h allows."""
         xi = [i for i, a in enumerate(w.args) if a.batched]
         pinned = []
+        bufs = [list(dev_in), list(dev_in)]
         for i in xi:
             t = torch.from_numpy(host[i])
-            if dev_in[i].dtype == torch.bfloat16:
+            if dev_in[i].dtype == torch.bfloat16 and not f32_inputs:
                 t = t.to(torch.bfloat16)
             elif dev_in[i].dtype == torch.bool:
                 t = t != 0
             pinned.append(t.pin_memory())
+            bufs[0][i] = torch.empty(t.shape, dtype=t.dtype, device=dev)
+            bufs[1][i] = torch.empty(t.shape, dtype=t.dtype, device=dev)
         loss_h = torch.empty((), dtype=torch.float32).pin_memory()
         h2d = sum(p.numel() * p.element_size() for p in pinned)
-        bufs = [list(dev_in), list(dev_in)]
-        for i in xi:
-            bufs[1][i] = torch.empty_like(dev_in[i])
         copy_st = torch.cuda.Stream(device=dev)
         main_st = torch.cuda.current_stream(dev)
         ready = [torch.cuda.Event(), torch.cuda.Event()]
@@ -549,13 +648,20 @@ def main():
             e2e_step()
         ms_e2e = time_steps(e2e_step, max(3, K // 2), dev, world)
         torch.cuda.synchronize(dev)
-        e2e = {"value": w.global_batch / (ms_e2e * 1e-3), "unit": "samples/s", "ms_per_step": ms_e2e,
-               "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * world,
-               "api": "paper_1711_03016_b200.Function.grad_run (dlvm_grad_run) + DataParallelStep",
-               "overlap": "batch upload of step k+1 on a copy stream during step k (double buffer)"}
-    out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W_,
-           "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "bf16" if w.dot_precision == "bf16" else "f32",
+        del bufs
+        return {"value": round(w.global_batch / (ms_e2e * 1e-3), 1), "unit": "samples/s",
+                "ms_per_step": round(ms_e2e, 4), "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 4 * world,
+                "x_host_dtype": "f32" if f32_inputs else str(dev_in[0].dtype).replace("torch.", "")}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(False)
+        e2e["api"] = "Function.grad_run (dlvm_grad_run) + DataParallelStep; batch upload of step k+1 overlaps step k"
+        if not args.no_e2e_f32 and w.dot_precision == "bf16":
+            e2e["f32_inputs"] = e2e_leg(True)
+    out = {"metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": K,
+           "warmup": W_, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "bf16" if w.dot_precision == "bf16" else "f32",
            "data": "synthetic (seeded PCG64 per workloads.py; Glorot weights)",
            "config": {"workload": w.name, "global_batch": w.global_batch, "per_rank_batch": w.batch,
                       "layers": [list(l) for l in w.layers], "parallelism": f"dp{world}",
@@ -564,8 +670,8 @@ def main():
                       "l2": ("inputs larger than L2 (x is %d MiB per rank)" % (w.batch * w.layers[0][0] * 2 >> 20))
                       if w.cfg != 1 else "L2-resident (whole c1 working set < 1 MiB; latency-bound config)",
                       "cuda_graph": use_graph},
-           "roofline": roof, "gpu_launches": launches, "clocks": clocks,
-           "kernels": [{"desc": r["desc"][:100], "ms": round(r["ms"], 4)} for r in kb]}
+           "step_tflops": round(step_flops / (ms * 1e-3) / 1e12, 1),
+           "roofline": roof, "gpu_launches": launches, "clocks": clocks}
     if e2e:
         out["e2e"] = e2e
     if sgd_info:
@@ -576,30 +682,35 @@ def main():
         except Exception as ex:  # noqa: BLE001
             out["cpu_baseline"] = {"error": repr(ex)}
         if not args.no_elementwise:
-            ew = bench_chain(dev, K, W_)
+            ew, ew_detail = bench_chain(dev, K, W_)
             out["fused_elementwise"] = ew
+            detail["fused_elementwise"] = ew_detail
             out["gpu_launches"] += (1 + ew["launches_fwd_adj"]) * K
             try:
                 ew["cpu_baseline"] = cpu_baseline_chain(256)
             except Exception as ex:  # noqa: BLE001
                 ew["cpu_baseline"] = {"error": repr(ex)}
-        if not args.no_next:
-            legs = {}
-            rnn = WL.rnn()
-            legs["rnn"] = bench_grad_leg(rnn, lambda r: WL.rnn(8, r, 2048, 2048), dev, K, W_,
-                                         {"W", "U", "h0"} | {f"x{t}" for t in range(1, 9)}, 16)
-            hv = WL.mlp_hvp()
-            legs["mlp_hvp"] = bench_grad_leg(hv, lambda r: WL.mlp_hvp(r), dev, K, W_, {"x", "W1", "W2"}, 16)
-            for v in legs.values():
-                out["gpu_launches"] += v["launches"] * K
-            out["next_rows"] = legs
         if not args.no_configs and args.workload == "c4":
             # BASELINE config 3 (the same MLP at batch 1024; target >= 975.5 TFLOP/s,
             # BASELINE.md §3) through dlvm_grad_run, x and W as bf16 storage
-            c3 = bench_grad_leg(WL.c3(), lambda r: WL.c3(r), dev, K, W_, {"x", "w1", "w2", "w3"}, 64)
+            c3, detail["c3"] = bench_grad_leg(WL.c3(), lambda r: WL.c3(r), dev, K, W_, {"x", "w1", "w2", "w3"}, 64)
             out["gpu_launches"] += c3["launches"] * K
             out["other_configs"] = {"c3": c3}
+        if not args.no_next:
+            legs = {}
+            rnn = WL.rnn()
+            legs["rnn"], detail["rnn"] = bench_grad_leg(rnn, lambda r: WL.rnn(8, r, 2048, 2048), dev, K, W_,
+                                                        {"W", "U", "h0"} | {f"x{t}" for t in range(1, 9)}, 16)
+            hv = WL.mlp_hvp()
+            legs["mlp_hvp"], detail["mlp_hvp"] = bench_grad_leg(hv, lambda r: WL.mlp_hvp(r), dev, K, W_,
+                                                                {"x", "W1", "W2"}, 16)
+            for v in legs.values():
+                out["gpu_launches"] += v["launches"] * K
+            out["next_rows"] = legs
     if rank == 0:
+        dp_ = write_detail(args, detail)
+        if dp_:
+            out["detail_file"] = os.path.relpath(dp_, ROOT)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -60,7 +60,7 @@ typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3 } dlvm_d
 
 #define DLVM_MAX_RANK 8
 typedef struct {
-  void* data;                    /* device pointer (host pointer for dlvm_*_host) */
+  void* data;                    /* device pointer (caller-owned) */
   int32_t dtype;                 /* dlvm_dtype */
   int32_t rank;                  /* 0..DLVM_MAX_RANK; 0 = scalar */
   int64_t shape[DLVM_MAX_RANK];
@@ -81,7 +81,10 @@ typedef struct {
 
 typedef struct {
   int32_t dot_precision; /* DLVM_DOT_F32 | DLVM_DOT_BF16 */
-  int32_t device;        /* CUDA device ordinal the handle launches on */
+  int32_t device;        /* -1: launch on the caller's current device (the default);
+                            >= 0: create loads its kernels into, and run/grad_run launch on,
+                            that device (made current for the call, then restored).  The
+                            tensors and stream passed to run must live on that device. */
   uint32_t flags;        /* DLVM_PLAN_ONLY | DLVM_NO_FUSION | DLVM_NO_SPECIALIZE | DLVM_NO_OPT | DLVM_NO_JIT */
 } dlvm_options;
 
@@ -91,19 +94,33 @@ typedef struct dlvm_fn_s* dlvm_fn;
 #define DLVM_PRIMAL 0
 #define DLVM_GRADIENT 1
 
-/* Parse `module_text` (len bytes, need not be NUL-terminated), verify the
+/* Defined by: the module/function/gradient-declaration structure of Fig. 3
+ * (P:L246-272), the canonicalisation of a gradient declaration into a
+ * function -- "first copies basic blocks and instructions from the original
+ * function to the new function body, and then applies adjoint code
+ * generation" (§3.1.3) -- and NNKit's shape-specialised lowering and
+ * "function reification" (§3.4): a handle is that reified,
+ * shape-specialised callable.
+ * Parse `module_text` (len bytes, need not be NUL-terminated), verify the
  * whole module, and build a handle for function `fn_name` and, if
  * `grad_name` is non-NULL, the gradient declaration of that name (which must
  * be a `[gradient @fn_name ...]` declaration); with grad_name NULL the unique
  * gradient declaration of fn_name is used if there is exactly one.
  * Errors: DLVM_ERR_PARSE, DLVM_ERR_VERIFY (incl. non-differentiable),
  * DLVM_ERR_UNSUPPORTED (e.g. f64/integer tensors on the GPU path),
- * DLVM_ERR_USAGE (NULL pointers, unknown function names). `opts` may be NULL
- * (defaults: DLVM_DOT_F32, device 0, no flags). */
+ * DLVM_ERR_USAGE (NULL pointers, unknown function names, device < -1),
+ * DLVM_ERR_CUDA (cudaSetDevice for opts->device failed).  `opts` may be NULL
+ * (defaults: DLVM_DOT_F32, device -1 = current, no flags).  Ownership: *out
+ * is a host-side object owned by the caller until dlvm_fn_destroy; *out is
+ * NULL on failure. */
 dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_name,
                            const char* grad_name, const dlvm_options* opts, dlvm_fn* out);
 
-/* Inferred signature of the primal (which=0) or gradient (which=1) function.
+/* Defined by: the function types of Fig. 3 -- `@foo: (<1x784>, <784x10>,
+ * <1x10>) -> <1x10>`, `@foo_grad` and the seedable
+ * `@foo_grad_3` with its seed appended and results (dW, db, kept)
+ * -- and Table 1's type rules.
+ * Inferred signature of the primal (which=0) or gradient (which=1) function.
  * On entry *n_in / *n_out hold the capacity of in_types / out_types (either
  * array may be NULL with capacity 0 to query counts); on exit they hold the
  * counts.  Returned tensors have data=NULL and dtype DLVM_F32/DLVM_F64/
@@ -127,7 +144,10 @@ dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_
 dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);
 
 /* Device workspace bytes dlvm_fn_run (which=0) / dlvm_grad_run (which=1)
- * need; the caller passes a buffer at least this large (256-byte aligned). */
+ * need; the caller passes a buffer at least this large (256-byte aligned).
+ * The workspace holds intermediates of one run: concurrent runs (e.g. on
+ * different streams) need separate workspaces.  Errors: DLVM_ERR_USAGE
+ * (NULL handle/pointer, which not 0/1, which=1 without a gradient). */
 dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes);
 
 /* Number of kernel launches one run (which=0) / grad run (which=1) issues
@@ -136,19 +156,35 @@ dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes);
  * covered by dlvm_fn_launch_events). */
 dlvm_status dlvm_fn_num_launches(dlvm_fn fn, int which, int* launches);
 
-/* Execute the primal function on `cuda_stream` (a cudaStream_t; NULL = the
- * legacy default stream).  in[n_in] / out[n_out] follow the signature. */
+/* Defined by: the instruction semantics of §3.1.1 and Table 1
+ * (P:L164-189), evaluated in program order ("straight-line" function).
+ * Execute the primal function on `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  in[n_in] / out[n_out] follow the signature; the
+ * caller owns every buffer and keeps it alive until the stream's work is
+ * done.  Errors (returned before anything is queued): DLVM_ERR_USAGE for
+ * arity, shape, dtype, alignment or NULL-workspace mismatches;
+ * DLVM_ERR_UNSUPPORTED if the function could not be planned; DLVM_ERR_CUDA
+ * if a launch fails (earlier launches of the call may already be queued).
+ * Device faults surface asynchronously at the caller's next sync. */
 dlvm_status dlvm_fn_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, dlvm_tensor* out, int n_out,
                         void* workspace, void* cuda_stream);
 
-/* Execute the gradient function.  `in` holds the primal arguments; `seed`
+/* Defined by: the gradient declaration (§3.1.3): a function
+ * that "takes original inputs and produces a tuple of partial derivatives
+ * with respect to the inputs", i.e. the vector-Jacobian product
+ * seed^T J_f restricted to `wrt` (reading A6), configurable by
+ * `wrt`, `keeping`, `from` and `seedable`, with unused
+ * operations removed by dead-code elimination.
+ * Execute the gradient function.  `in` holds the primal arguments; `seed`
  * is non-NULL iff the declaration is `seedable` (it is the last parameter of
  * the gradient function).  out[n_out]: gradients in `wrt` order, then kept
  * outputs.  If `grad_ready_events` is non-NULL it points to n_grads
  * cudaEvent_t (n_grads = number of `wrt` gradients), each recorded on
  * `cuda_stream` as soon as that gradient is final -- a communication stream
  * can wait on them to overlap a gradient all-reduce with the rest of the
- * adjoint (data-parallel path). */
+ * adjoint (data-parallel path).  Ownership and errors as
+ * for dlvm_fn_run; events are caller-owned and must be real (created)
+ * cudaEvent_t handles. */
 dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlvm_tensor* seed,
                           dlvm_tensor* out, int n_out, void* workspace, void* cuda_stream,
                           void* const* grad_ready_events);
@@ -168,10 +204,16 @@ dlvm_status dlvm_fn_launch_events(dlvm_fn fn, int which, void* const* events, in
 dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t cap, double* flops,
                                 double* bytes);
 
-/* Thread-local text of the last error on this thread ("" if none). */
+/* Defined by: SPEC.md's diagnostics format "line:col: severity: message"
+ * (S:L284).  Thread-local text of the last error on this thread ("" if
+ * none); the pointer stays valid until the next failing call on this
+ * thread.  Never NULL. */
 const char* dlvm_last_error(void);
 
-/* Release the host-side plan.  NULL is ignored. */
+/* Release the host-side plan.  NULL is ignored.  Work already queued by the
+ * handle is unaffected (its launches hold their parameters by value, and
+ * create-time NVRTC kernels stay loaded in a per-process cache); any later
+ * call with the handle is invalid. */
 void dlvm_fn_destroy(dlvm_fn fn);
 
 /* Library version string, e.g. "dlvm-b200 0.1 sm_100a". */

@@ -134,6 +134,22 @@ int epi_vec(const EwParams& e) {
   return 4;
 }
 
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t set(int dev) {
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e != cudaSuccess) return e;
+    if (prev == dev) {
+      prev = -1;
+      return cudaSuccess;
+    }
+    return cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, const dlvm_tensor* seed,
                     dlvm_tensor* out, int n_out, void* workspace, void* stream_v, void* const* events) {
   if (!fn) return fail(DLVM_ERR_USAGE, "NULL handle");
@@ -174,6 +190,13 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " NULL or not 16-byte aligned");
   }
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  // dlvm_options.device >= 0: the launches go to that device (made current
+  // for the duration of the call, then restored); -1: the caller's current one
+  DeviceGuard dg;
+  if (fn->opts.device >= 0) {
+    cudaError_t e = dg.set(fn->opts.device);
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
   // parameter i of the function: an input, or the seed (last parameter of a
   // seedable gradient, passed separately; it may feed a dot and need a cast)
   auto param = [&](int i) -> const dlvm_tensor& { return i < n_in ? in[i] : *seed; };
@@ -317,9 +340,18 @@ double step_bytes(const Plan& P, const Step& st) {
     SType t = buf >= 0 ? P.bufs[buf].st : fallback;
     return t == SType::F32 ? 4.0 : t == SType::BF16 ? 2.0 : 1.0;
   };
+  double b = 0;
+  if (st.kind == Step::EW && st.ew.finalize) {
+    // a merged finalize: input q is the [nchunks, dims[q]] partials of
+    // reduction q (dims[q] its own length); store o writes dims[store_slot[o]]
+    for (size_t q = 0; q < g.inputs.size(); ++q)
+      b += (double)g.inputs[q].nchunks * (double)g.dims[q] * 4.0;
+    for (size_t o = 0; o < g.stores.size(); ++o)
+      b += (double)g.dims[g.prog.store_slot[o]] * esz(g.stores[o].buf, g.stores[o].st);
+    return b;
+  }
   int64_t n = 1;
   for (int d = 0; d < g.ndims; ++d) n *= g.dims[d];
-  double b = 0;
   for (auto& r : g.inputs) {
     if (r.buf < 0) continue;
     int64_t cnt = r.nchunks;  // elements touched: product of dims with a nonzero stride
@@ -401,9 +433,11 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
   *out = nullptr;
   dlvm_options o{};
   o.dot_precision = DLVM_DOT_F32;
+  o.device = -1;
   if (opts) o = *opts;
   if (o.dot_precision != DLVM_DOT_F32 && o.dot_precision != DLVM_DOT_BF16)
     return fail(DLVM_ERR_USAGE, "unknown dot precision");
+  if (o.device < -1) return fail(DLVM_ERR_USAGE, "device must be -1 (current) or a device ordinal");
   try {
     Module m = parse_module(std::string(module_text, len));
     verify_module(m);
@@ -461,7 +495,15 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
         }
       }
     }
-    if (!(o.flags & (DLVM_PLAN_ONLY | DLVM_NO_SPECIALIZE | DLVM_NO_JIT)) && jit_available()) jit_specialise(h);
+    if (!(o.flags & (DLVM_PLAN_ONLY | DLVM_NO_SPECIALIZE | DLVM_NO_JIT)) && jit_available()) {
+      // create-time kernels are loaded into the context of the run device
+      DeviceGuard dg;
+      if (o.device >= 0 && dg.set(o.device) != cudaSuccess) {
+        delete h;
+        return fail(DLVM_ERR_CUDA, "cudaSetDevice failed for dlvm_options.device");
+      }
+      jit_specialise(h);
+    }
     *out = h;
     return DLVM_OK;
   } catch (const Error& e) {
@@ -553,6 +595,7 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
 
 dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes) {
   if (!fn || !bytes) return fail(DLVM_ERR_USAGE, "NULL argument");
+  if (which != 0 && which != 1) return fail(DLVM_ERR_USAGE, "which must be 0 or 1");
   if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
   if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
   *bytes = fn->plan[which].workspace_bytes;
@@ -561,6 +604,7 @@ dlvm_status dlvm_fn_workspace_bytes(dlvm_fn fn, int which, size_t* bytes) {
 
 dlvm_status dlvm_fn_num_launches(dlvm_fn fn, int which, int* launches) {
   if (!fn || !launches) return fail(DLVM_ERR_USAGE, "NULL argument");
+  if (which != 0 && which != 1) return fail(DLVM_ERR_USAGE, "which must be 0 or 1");
   if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
   if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
   *launches = fn->plan[which].launches();
@@ -588,6 +632,7 @@ dlvm_status dlvm_grad_run(dlvm_fn fn, const dlvm_tensor* in, int n_in, const dlv
 
 dlvm_status dlvm_fn_launch_events(dlvm_fn fn, int which, void* const* events, int n_events) {
   if (!fn || (which != 0 && which != 1)) return fail(DLVM_ERR_USAGE, "bad handle or which");
+  if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
   if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
   if (!events || n_events == 0) {
     fn->launch_events[which].clear();
@@ -600,6 +645,7 @@ dlvm_status dlvm_fn_launch_events(dlvm_fn fn, int which, void* const* events, in
 
 dlvm_status dlvm_fn_launch_info(dlvm_fn fn, int which, int i, char* buf, size_t cap, double* flops, double* bytes) {
   if (!fn || (which != 0 && which != 1)) return fail(DLVM_ERR_USAGE, "bad handle or which");
+  if (which == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
   if (!fn->planned[which]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[which]);
   const Plan& P = fn->plan[which];
   int li = 0;

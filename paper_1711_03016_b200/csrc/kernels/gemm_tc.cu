@@ -39,8 +39,8 @@ cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStrea
   TcParams tp;
   if (!make_params(p, &tp, ctas)) return cudaErrorInvalidValue;
   const int smem = ctas == 2 ? smem_bytes<256, 2>() : (p.bn == 256 ? smem_bytes<256, 1>() : smem_bytes<128, 1>());
-  const int tiles = tp.tiles_m * tp.tiles_n;
-  const int grid = ctas * std::min(tiles, num_sms() / ctas);
+  const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);  // work items (tile x K split)
+  const int grid = ctas * std::min(items, num_sms() / ctas);
   LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), smem, stream, (unsigned)ctas, 1);
   void* args[] = {&tp};
   return launch_jit(fn, L, args);

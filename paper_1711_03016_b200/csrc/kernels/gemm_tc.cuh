@@ -19,6 +19,7 @@
 //   warps 4-11: epilogue (TMEM lanes 32*(warp%4) .. +31 = tile rows; two
 //               warps per lane quarter split the tile's column chunks)
 // Host side: tensor maps, launch configuration, registry entry points.
+#include <atomic>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -142,18 +143,25 @@ bool use_cta_pair(const GemmParams& p) {
 
 template <int BN, class PROG, int CTAS>
 cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
-  static bool configured = false;
+  // the max-dynamic-smem attribute is per device: one bit per device ordinal
+  static std::atomic<uint64_t> configured{0};
   constexpr int SMEM = smem_bytes<BN, CTAS>();
   auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
-  if (!configured) {
+  int dev = 0;
+  cudaError_t e0 = cudaGetDevice(&dev);
+  if (e0 != cudaSuccess) return e0;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_relaxed) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit);
   }
   TcParams tp;
   if (!make_params(p, &tp, CTAS)) return cudaErrorInvalidValue;
-  const int tiles = tp.tiles_m * tp.tiles_n;
-  const int grid = CTAS * std::min(tiles, num_sms() / CTAS);  // persistent: one CTA (pair) per SM (pair)
+  // persistent: one CTA (pair) per SM (pair), up to one per work item
+  // (tile x K split)
+  const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);
+  const int grid = CTAS * std::min(items, num_sms() / CTAS);
   LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), SMEM, stream, CTAS, 1);
   cudaError_t e = cudaLaunchKernelEx(&L.cfg, kern, tp);
   return e != cudaSuccess ? e : cudaGetLastError();

@@ -9,6 +9,7 @@
 // `return (%a: T, %b: T)` (reading A22).  Names are resolved later by the
 // verifier, so a malformed text is always reported as a parse error (2)
 // before any type error (1).
+#include <cerrno>
 #include <cctype>
 #include <cmath>
 #include <cstdlib>
@@ -153,7 +154,19 @@ struct Parser {
     for (size_t k = 0; ok && k < x.text.size(); ++k)
       ok = std::isdigit((unsigned char)x.text[k]) || (k == 0 && x.text[k] == '-' && x.text.size() > 1);
     if (!ok) fail(x, "expected integer, found '" + x.text + "'");
-    return std::strtoll(x.text.c_str(), nullptr, 10);
+    errno = 0;
+    const long long v = std::strtoll(x.text.c_str(), nullptr, 10);
+    if (errno == ERANGE) fail(x, "integer '" + x.text + "' out of range");
+    return v;
+  }
+  // element count of a shape; rejects shapes of more than 2^59 elements
+  // (2^62 bytes at 8 bytes per element), so numel() and every byte size
+  // derived from it stay far from int64 overflow
+  void check_numel(const Token& at, const std::vector<int64_t>& shape) {
+    int64_t n = 1;
+    for (int64_t d : shape)
+      if (__builtin_mul_overflow(n, d, &n) || n > (int64_t(1) << 59))
+        fail(at, "tensor has too many elements (more than 2^59)");
   }
   DType dtype() {
     const Token& x = next();
@@ -169,6 +182,7 @@ struct Parser {
     Type ty;
     if (peek().text == "<" && peek().kind == Tk::Punct) {
       next();
+      const Token& first = peek();
       while (!peek_dtype()) {
         const Token& u = peek();
         int64_t d = integer();
@@ -176,6 +190,7 @@ struct Parser {
         ty.shape.push_back(d);
         expect("x");
       }
+      check_numel(first, ty.shape);
       ty.dtype = dtype();
       expect(">");
       return ty;
@@ -262,11 +277,13 @@ struct Parser {
     } else if (op == Op::ShapeCast) {
       in.ops.push_back(operand());
       expect("to");
+      const Token& first = peek();
       in.shape.push_back(integer());
       while (peek().text == "x" && peek().kind == Tk::Ident) {
         next();
         in.shape.push_back(integer());
       }
+      check_numel(first, in.shape);
     } else if (op == Op::DataTypeCast) {
       in.ops.push_back(operand());
       expect("to");

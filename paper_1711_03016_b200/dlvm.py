@@ -129,7 +129,7 @@ class Function:
     dlvm_grad_run."""
 
     def __init__(self, text: str, fn: str, grad: Optional[str] = None, dot_precision: str = "f32",
-                 device: int = 0, flags: int = 0):
+                 device: int = -1, flags: int = 0):
         L = lib()
         o = dlvm_options(DLVM_DOT_BF16 if dot_precision == "bf16" else DLVM_DOT_F32, device, flags)
         h = ctypes.c_void_p()
@@ -193,13 +193,17 @@ class Function:
         _check(lib().dlvm_fn_launch_events(self._h, which, arr, len(events)))
 
     # ----------------------------------------------------------- execution
-    def _workspace(self, which: int, device):
+    def _workspace(self, which: int, device, stream=None):
+        """The cached workspace of (which, stream): runs on different streams
+        get different workspaces, so concurrent runs of one handle do not
+        share intermediates (dlvm.h: a workspace serves one run at a time)."""
         import torch
         n = self.workspace_bytes(which)
-        ws = self._ws.get(which)
+        key = (which, int(stream or 0))
+        ws = self._ws.get(key)
         if ws is None or ws.numel() < n:
             ws = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
-            self._ws[which] = ws
+            self._ws[key] = ws
         return ws
 
     def _outputs(self, which: int, device, outputs):
@@ -215,8 +219,8 @@ class Function:
         _require_cuda(inputs)
         dev = inputs[0].device if inputs else torch.device("cuda")
         outs = self._outputs(0, dev, outputs)
-        ws = self._workspace(0, dev) if workspace is None else workspace
         st = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        ws = self._workspace(0, dev, st) if workspace is None else workspace
         _check(lib().dlvm_fn_run(self._h, _tarray(inputs), len(inputs), _tarray(outs), len(outs),
                                  ws.data_ptr(), st))
         return outs
@@ -226,8 +230,8 @@ class Function:
         _require_cuda(list(inputs) + ([seed] if seed is not None else []))
         dev = inputs[0].device if inputs else torch.device("cuda")
         outs = self._outputs(1, dev, outputs)
-        ws = self._workspace(1, dev) if workspace is None else workspace
         st = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        ws = self._workspace(1, dev, st) if workspace is None else workspace
         seed_t = ctypes.byref(_tensor(seed)) if seed is not None else None
         ev = None
         if events is not None:

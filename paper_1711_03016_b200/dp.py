@@ -62,23 +62,58 @@ class GradBuffer:
         return self.flat[lo:self.offsets[last] + k]
 
 
+class CudaStreams:
+    """The stream/event operations DataParallelStep needs, on CUDA (the
+    product configuration).  Tests on CPU substitute an object with the same
+    methods to observe bucket order and event gating (tests/test_dp_gloo.py)."""
+
+    def __init__(self, device):
+        import torch
+        self.torch = torch
+        self.device = device
+
+    def new_event(self):
+        e = self.torch.cuda.Event()
+        e.record()  # torch creates CUDA events lazily; the C ABI needs real handles
+        return e
+
+    def new_stream(self):
+        return self.torch.cuda.Stream(device=self.device)
+
+    def current(self):
+        return self.torch.cuda.current_stream(self.device)
+
+    def use(self, stream):
+        return self.torch.cuda.stream(stream)
+
+    def wait_event(self, stream, event):
+        stream.wait_event(event)
+
+    def wait_stream(self, stream, other):
+        stream.wait_stream(other)
+
+    def handle(self, stream):
+        return stream.cuda_stream
+
+
 def allreduce_buckets(buf: GradBuffer, buckets: Sequence[Sequence[int]], group=None, order=None,
-                      comm_stream=None, ready_events=None):
+                      comm_stream=None, ready_events=None, streams=None):
     """All-reduce (SUM) each bucket.  With `comm_stream` and `ready_events`
-    (one torch.cuda.Event per gradient), bucket b is issued on the comm
-    stream after waiting for the events of its gradients.  Returns the async
-    work handles (the caller makes its stream wait on them)."""
+    (one event per gradient), bucket b is issued on the comm stream after
+    waiting for the events of its gradients.  Returns the async work handles
+    (the caller makes its stream wait on them)."""
     import torch.distributed as dist
     works = []
     seq = order if order is not None else range(len(buckets))
     for b in seq:
         bucket = buckets[b]
         if comm_stream is not None:
-            import torch
-            with torch.cuda.stream(comm_stream):
+            if streams is None:
+                streams = CudaStreams(None)
+            with streams.use(comm_stream):
                 if ready_events is not None:
                     for g in bucket:
-                        comm_stream.wait_event(ready_events[g])
+                        streams.wait_event(comm_stream, ready_events[g])
                 works.append(dist.all_reduce(buf.bucket_slice(bucket), op=dist.ReduceOp.SUM, group=group,
                                              async_op=True))
         else:
@@ -89,36 +124,40 @@ def allreduce_buckets(buf: GradBuffer, buckets: Sequence[Sequence[int]], group=N
 
 class DataParallelStep:
     """One fwd+adjoint step of a gradient handle on this rank's batch shard,
-    then the bucketed gradient all-reduce (NCCL), overlapped with the adjoint."""
+    then the bucketed gradient all-reduce (NCCL), overlapped with the adjoint:
+    dlvm_grad_run records gradient g's ready event on the compute stream as
+    soon as g is final; bucket b's all-reduce is issued on a communication
+    stream that first waits for the events of b's gradients, in reverse
+    bucket order (the last layer's gradients are final first)."""
 
-    def __init__(self, fn, n_grads: int, device, group=None, per_bucket: int = 2, world_size: int = 1):
+    def __init__(self, fn, n_grads: int, device, group=None, per_bucket: int = 2, world_size: int = 1,
+                 streams=None, grads_dtype=None):
         import torch
         self.fn = fn
         self.n_grads = n_grads
         self.device = device
         self.group = group
         self.world_size = world_size
+        self.streams = streams if streams is not None else CudaStreams(device)
         _, outs = fn.signature(1)
-        self.grads = GradBuffer([s for s, _ in outs[:n_grads]], device)
-        self.kept = [torch.empty(s, dtype=torch.float32, device=device) for s, _ in outs[n_grads:]]
+        self.grads = GradBuffer([s for s, _ in outs[:n_grads]], device, dtype=grads_dtype)
+        self.kept = [torch.empty(s, dtype=grads_dtype or torch.float32, device=device) for s, _ in outs[n_grads:]]
         self.outputs = self.grads.views + self.kept
         self.buckets = layer_buckets(n_grads, per_bucket)
         # gradients become ready in reverse layer order: issue the last bucket first
         self.order = list(reversed(range(len(self.buckets))))
-        self.events = [torch.cuda.Event() for _ in range(n_grads)]
-        for e in self.events:
-            e.record()  # torch creates CUDA events lazily; the C ABI needs real handles
-        self.comm = torch.cuda.Stream(device=device) if world_size > 1 else None
+        self.events = [self.streams.new_event() for _ in range(n_grads)]
+        self.comm = self.streams.new_stream() if world_size > 1 else None
 
     def step(self, inputs, seed, stream=None):
-        import torch
-        st = stream or torch.cuda.current_stream(self.device)
-        self.fn.grad_run(inputs, seed=seed, outputs=self.outputs, stream=st.cuda_stream,
+        st = stream or self.streams.current()
+        self.fn.grad_run(inputs, seed=seed, outputs=self.outputs, stream=self.streams.handle(st),
                          events=self.events if self.comm is not None else None)
         if self.comm is None:
             return self.outputs
-        works = allreduce_buckets(self.grads, self.buckets, self.group, self.order, self.comm, self.events)
+        works = allreduce_buckets(self.grads, self.buckets, self.group, self.order, self.comm, self.events,
+                                  self.streams)
         for w in works:
             w.wait()  # makes the current stream wait for the collective
-        st.wait_stream(self.comm)
+        self.streams.wait_stream(st, self.comm)
         return self.outputs

@@ -538,3 +538,57 @@ def test_binding_refuses_host_tensors():
     f = _plan_only(w.text, w.fn, w.grad)
     with pytest.raises(ValueError, match="CUDA tensors"):
         f.run([torch.from_numpy(x) for x in w.inputs()])
+
+
+def test_launch_info_bytes_of_merged_finalize():
+    """dlvm_fn_launch_info's minimum bytes for a merged finalize count each
+    reduction's partials at its own length: 250x1000 + 4x3000 + 1000x1 f32
+    partials read, 1000 + 3000 + 1 f32 results written."""
+    from merged_reductions import merged_reduction_program
+    f = _plan_only(merged_reduction_program(3000, 1000), "f")
+    desc, flops, nbytes = f.launch_info(0, 1)
+    assert desc.startswith("finalize"), desc
+    assert flops == 0
+    assert nbytes == 4 * (250 * 1000 + 4 * 3000 + 1000 * 1) + 4 * (1000 + 3000 + 1)
+
+
+def test_overflowing_dimensions_are_parse_errors():
+    """Shapes whose element count overflows int64 (or exceeds 2^59, so byte
+    sizes stay representable) and out-of-range integers are rejected at parse
+    time (class 2) instead of wrapping numel / workspace sizes."""
+    big = 1 << 31
+    for dims in (f"{big} x {big} x {big}", "99999999999999999999999", f"{1 << 30} x {1 << 30}"):
+        t = (f'module "m"\nstage raw\nfunc @f: (<{dims} x f32>) -> <{dims} x f32> {{\n'
+             f"'entry(%x: <{dims} x f32>):\n    %y = tanh %x: <{dims} x f32>\n    return %y: <{dims} x f32>\n}}\n")
+        with pytest.raises(P.DlvmError) as e:
+            P.Function(t, "f", None, flags=P.DLVM_PLAN_ONLY)
+        assert e.value.status == 2, (dims, e.value)
+    X = "<4 x 4 x f32>"
+    t = (f'module "m"\nstage raw\nfunc @f: ({X}) -> <{1 << 31} x {1 << 31} x f32> {{\n'
+         f"'entry(%x: {X}):\n    %y = shapeCast %x: {X} to {1 << 31} x {1 << 31} x {1 << 31}\n"
+         f"    return %y: {X}\n}}\n")
+    with pytest.raises(P.DlvmError) as e:
+        P.Function(t, "f", None, flags=P.DLVM_PLAN_ONLY)
+    assert e.value.status == 2
+
+
+def test_which_is_range_checked_in_every_entry_point():
+    w = W.c1()
+    f = _plan_only(w.text, w.fn, w.grad)
+    L = P.dlvm.lib()
+    n = ctypes.c_size_t(0)
+    k = ctypes.c_int(0)
+    for which in (-1, 2, 7):
+        assert L.dlvm_fn_workspace_bytes(f._h, which, ctypes.byref(n)) == 3
+        assert L.dlvm_fn_num_launches(f._h, which, ctypes.byref(k)) == 3
+        assert L.dlvm_fn_launch_events(f._h, which, None, 0) == 3
+    g = _plan_only(W.FIG3, "foo", None)  # no gradient: which=1 is a usage error
+    assert L.dlvm_fn_workspace_bytes(g._h, 1, ctypes.byref(n)) == 3
+    assert L.dlvm_fn_num_launches(g._h, 1, ctypes.byref(k)) == 3
+
+
+def test_device_option_validated():
+    o = P.dlvm.dlvm_options(P.dlvm.DLVM_DOT_F32, -2, P.DLVM_PLAN_ONLY)
+    h = ctypes.c_void_p()
+    b = W.FIG3.encode()
+    assert P.dlvm.lib().dlvm_fn_create(b, len(b), b"foo", None, ctypes.byref(o), ctypes.byref(h)) == 3

@@ -1158,9 +1158,11 @@ def test_op_sweep_every_vm_opcode():
 
 def test_concurrent_runs_on_separate_streams_bit_identical():
     """dlvm_fn_run / dlvm_grad_run keep no mutable state in the handle (the
-    caller owns workspace and outputs): the same handle run concurrently on
-    two streams, and a second handle on a third, give bit-identical results
-    to sequential runs."""
+    caller owns workspace and outputs; the binding keeps one workspace per
+    stream): the same handle run concurrently on two streams with DIFFERENT
+    input values, and a second handle on a third, give bit-identical results
+    to sequential runs of each input set (a shared workspace would mix the
+    two runs' intermediates)."""
     import torch
     import paper_1711_03016_b200 as P
     dev = torch.device("cuda:0")
@@ -1168,13 +1170,17 @@ def test_concurrent_runs_on_separate_streams_bit_identical():
     f3 = P.Function(w3.text, w3.fn, w3.grad, dot_precision="bf16")
     w2 = W.c2(512, 4096)
     f2 = P.Function(w2.text, w2.fn, w2.grad)
-    ins3 = [torch.from_numpy(x).to(dev) for x in w3.inputs()]
+    ins3a = [torch.from_numpy(x).to(dev) for x in w3.inputs()]
+    ins3b = [torch.from_numpy(x).to(dev) for x in w3.inputs(row_offset=256)]  # other rows of the batch
+    ins3b[1] = ins3b[1] * 0.5  # and other weights
     ins2 = [torch.from_numpy(x).to(dev) for x in w2.inputs()]
     s3 = torch.tensor(np.float32(w3.seed()), device=dev)
     s2 = torch.from_numpy(w2.seed()).to(dev)
-    ref3 = [o.cpu() for o in f3.grad_run(ins3, seed=s3)]
+    ref3a = [o.cpu() for o in f3.grad_run(ins3a, seed=s3)]
+    ref3b = [o.cpu() for o in f3.grad_run(ins3b, seed=s3)]
     ref2 = [o.cpu() for o in f2.grad_run(ins2, seed=s2)]
     torch.cuda.synchronize()
+    assert not torch.equal(ref3a[0], ref3b[0])
     streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
     outs = []
     for rep in range(4):
@@ -1182,14 +1188,14 @@ def test_concurrent_runs_on_separate_streams_bit_identical():
         for k, st in enumerate(streams):
             with torch.cuda.stream(st):
                 if k < 2:
-                    res.append(f3.grad_run(ins3, seed=s3, stream=st.cuda_stream))
+                    res.append(f3.grad_run(ins3a if k == 0 else ins3b, seed=s3, stream=st.cuda_stream))
                 else:
                     res.append(f2.grad_run(ins2, seed=s2, stream=st.cuda_stream))
         torch.cuda.synchronize()
         outs.append(res)
     for res in outs:
         for k, r in enumerate(res):
-            ref = ref3 if k < 2 else ref2
+            ref = (ref3a, ref3b, ref2)[k]
             for a, b in zip(r, ref):
                 assert torch.equal(a.cpu(), b), f"stream {k}"
 
