@@ -200,9 +200,11 @@ def kernel_breakdown(f, which, step, K, dev):
                 step()
             torch.cuda.synchronize(dev)
         ks = [e for e in prof.profiler.kineto_results.events()
-              if e.device_type() == DeviceType.CUDA and "memcpy" not in e.name().lower()
-              and "memset" not in e.name().lower()]
+              if e.device_type() == DeviceType.CUDA and any(k in e.name() for k in OWN_KERNELS)]
         ks.sort(key=lambda e: e.start_ns())
+        ks = ks[-K * n:] if len(ks) >= K * n else ks  # the K steps end the session
+        if len(ks) != K * n:
+            raise RuntimeError(f"CUPTI saw {len(ks)} library kernels, plan has {K} x {n}")
         if len(ks) == K * n:
             dur = [[0.0] * K for _ in range(n)]
             exc = [[0.0] * K for _ in range(n)]
@@ -220,8 +222,9 @@ def kernel_breakdown(f, which, step, K, dev):
                 desc, flops, nbytes = f.launch_info(which, i)
                 out.append({"desc": desc, "kernel": names[i][:60], "ms": statistics.mean(dur[i]),
                             "excl_ms": statistics.mean(exc[i]), "flops": flops, "bytes": nbytes, "timing": "cupti"})
-    except Exception:  # noqa: BLE001
+    except Exception as ex:  # noqa: BLE001
         out = None
+        why = repr(ex)[:200]
     if out is not None:
         return out
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(K)]
@@ -238,8 +241,14 @@ def kernel_breakdown(f, which, step, K, dev):
     for i in range(n):
         desc, flops, nbytes = f.launch_info(which, i)
         ms = statistics.mean(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(K))
-        out.append({"desc": desc, "ms": ms, "excl_ms": ms, "flops": flops, "bytes": nbytes, "timing": "events"})
+        out.append({"desc": desc, "ms": ms, "excl_ms": ms, "flops": flops, "bytes": nbytes, "timing": "events",
+                    "cupti_failed": why})
     return out
+
+
+# kernel-name fragments of this library's kernels (ahead-of-time and NVRTC)
+OWN_KERNELS = ("gemm_tc_kernel", "gemm_simt_kernel", "ew_kernel", "ew2d_kernel", "ew_tma_kernel",
+               "finalize_kernel", "cast_bf16_kernel", "pack_bf16_kernel")
 
 
 def gemm_roofline(kb, pk, region_s):
@@ -428,6 +437,51 @@ def spawn_ranks(n: int) -> int:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd)
+
+
+def _pick(d, keys):
+    return {k: d[k] for k in keys if d is not None and k in d}
+
+
+def compact_line(out):
+    """The one JSON line: every contract key, and of each sub-measurement
+    only its headline numbers (the full records go to the detail file), so
+    the line stays short enough for the driver's stdout tail."""
+    line = _pick(out, ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                       "scaling", "vs_baseline", "dtype", "data", "config", "step_tflops", "gpu_launches", "clocks"])
+    line["config"] = _pick(out["config"], ["workload", "global_batch", "per_rank_batch", "parallelism", "l2",
+                                           "cuda_graph", "step"])
+    r = out.get("roofline")
+    if r:
+        line["roofline"] = _pick(r, ["bound", "achieved", "peak", "unit", "frac", "traffic", "kernel_ms", "timing",
+                                     "frac_of_sustained"])
+        line["roofline"]["kernel"] = r["kernel"][:60]
+        line["roofline"]["peak_kind"] = r["peak_kind"].split(" (")[0]
+        line["roofline"]["gemm_class"] = _pick(r["gemm_class"], ["tflops", "frac_of_burst", "share_of_step"])
+    if "e2e" in out:
+        e = out["e2e"]
+        line["e2e"] = _pick(e, ["value", "unit", "ms_per_step", "h2d_bytes_per_step", "d2h_bytes_per_step",
+                                "x_host_dtype"])
+        if "f32_inputs" in e:
+            line["e2e"]["f32_inputs"] = _pick(e["f32_inputs"], ["value", "ms_per_step", "h2d_bytes_per_step"])
+    if "cpu_baseline" in out:
+        line["cpu_baseline"] = out["cpu_baseline"]
+    if "fused_elementwise" in out:
+        ew = out["fused_elementwise"]
+        line["fused_elementwise"] = _pick(ew, ["fwd_gbs", "fwd_frac", "fwd_adj_gbs", "fwd_adj_frac"])
+        line["fused_elementwise"]["roofline"] = _pick(ew["roofline"], ["bound", "achieved", "peak", "unit", "frac",
+                                                                        "traffic", "timing"])
+        line["fused_elementwise"]["cpu_gbs"] = (ew.get("cpu_baseline") or {}).get("value")
+    legs = dict(out.get("other_configs", {}))
+    legs.update(out.get("next_rows", {}))
+    for name, leg in legs.items():
+        c = _pick(leg, ["value", "ms_per_step", "step_tflops", "step_frac_of_burst"])
+        if leg.get("roofline"):
+            c["gemm_frac_of_burst"] = leg["roofline"]["gemm_class"]["frac_of_burst"]
+            c["top_kernel_frac"] = leg["roofline"]["frac"]
+        c["cpu_samples_s"] = (leg.get("cpu_baseline") or {}).get("value")
+        line.setdefault("other_configs" if name in out.get("other_configs", {}) else "next_rows", {})[name] = c
+    return line
 
 
 def write_detail(args, detail):
@@ -708,10 +762,12 @@ def main():
                 out["gpu_launches"] += v["launches"] * K
             out["next_rows"] = legs
     if rank == 0:
+        detail["line_full"] = out
         dp_ = write_detail(args, detail)
+        line = compact_line(out)
         if dp_:
-            out["detail_file"] = os.path.relpath(dp_, ROOT)
-        print(json.dumps(out))
+            line["detail_file"] = os.path.relpath(dp_, ROOT)
+        print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 

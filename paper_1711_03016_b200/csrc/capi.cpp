@@ -7,6 +7,7 @@
 // elimination (L304-305) -> plan fused sm_100a launches.  dlvm_fn_run /
 // dlvm_grad_run bind caller pointers and enqueue the planned launches on the
 // caller's stream: no allocation, no host synchronisation (graph-capturable).
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -134,6 +135,11 @@ int epi_vec(const EwParams& e) {
   return 4;
 }
 
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct DeviceGuard {
   int prev = -1;
   cudaError_t set(int dev) {
@@ -241,6 +247,9 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       continue;  // the producer wrote the single partial into the f32 home
     if (st.counted_launch() && (e = mark(li++)) != cudaSuccess)
       return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+    // one NVTX range per launch group, named by the plan step
+    // ("gemm tcgen05 bf16 %z1 M=..."); a no-op unless a tool is attached
+    NvtxRange nvtx_range(st.desc.c_str());
     if (st.kind == Step::EW) {
       EwParams p;
       to_dev(st.ew, b, &p);

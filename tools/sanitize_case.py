@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Small fwd+adjoint cases for compute-sanitizer (memcheck / racecheck):
-c1 (SIMT GEMMs), c2 (EW kernels), a small bf16 MLP (tcgen05 GEMMs with
-fused epilogues and reductions), and an SGD update."""
+c1 (SIMT GEMMs), c2 (EW kernels), small bf16 MLPs (tcgen05 GEMMs with
+fused epilogues and reductions, CTA pairs, split-K dW with its sum step),
+and an RNN (multi-K-segment GEMMs).  Run under
+`compute-sanitizer --tool memcheck|racecheck|synccheck`; summaries in
+profiles/r2_sanitizer.txt."""
 import os
 import sys
 
@@ -30,4 +33,12 @@ if __name__ == "__main__":
     run(W.c3(256, layers=[(256, 256, "relu"), (256, 200, None)]), "bf16")
     run(W._mlp_workload(5, "c5s", 128, [(256, 256, "tanh")] * 2, ("normal",), ("uniform", -0.5, 0.5),
                         1.0 / 128, "bf16", 128), "bf16")
+    # split-K dW GEMMs (K = batch 8192 split 2) with CTA pairs, and the
+    # deferred-epilogue sum step
+    w = W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)])
+    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16", flags=P.DLVM_PLAN_ONLY)
+    assert "K split" in f.print(3), f.print(3)
+    run(w, "bf16")
+    # rnn: multi-segment GEMMs
+    run(W.rnn(3, 256, 128, 128), "bf16")
     print("sanitize cases done")
