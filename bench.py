@@ -369,8 +369,7 @@ def bench_chain(dev, K, W_):
     hb = pk["hbm_gbs"]
     gbs_k = ba / (main["ms"] * 1e-3) / 1e9
     gbs_f, gbs_a = bf / (ms_f * 1e-3) / 1e9, ba / (ms_a * 1e-3) / 1e9
-    detail = {"fwd_adj_kernels": [{"desc": r["desc"][:100], "ms": round(r["ms"], 4), "excl_ms": round(r["excl_ms"], 4)}
-                                  for r in kb]}
+    detail = {"fwd_adj_kernels": [dict(r, desc=r["desc"][:100]) for r in kb]}
     return {"workload": "c2_chain [16384,16384] f32", "fwd_ms": round(ms_f, 4), "fwd_gbs": round(gbs_f, 1),
             "fwd_frac": round(gbs_f / hb, 4), "fwd_adj_ms": round(ms_a, 4), "fwd_adj_gbs": round(gbs_a, 1),
             "fwd_adj_frac": round(gbs_a / hb, 4),
@@ -407,7 +406,7 @@ def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
            "ms_per_step": round(ms, 4), "step_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
            "step_frac_of_burst": round(flops / (ms * 1e-3) / 1e12 / pk["bf16_tflops"], 4),
            "launches": f.num_launches(1), "roofline": gemm_roofline(kb, pk, ms * K * 1e-3)}
-    detail = [{"desc": r["desc"][:110], "ms": round(r["ms"], 4), "excl_ms": round(r["excl_ms"], 4)} for r in kb]
+    detail = [dict(r, desc=r["desc"][:110]) for r in kb]
     try:
         cores = oracle_threads()
         ws_ = small(cpu_rows)

@@ -14,12 +14,16 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OUT = os.path.join(PKG, "libdlvm.so")
-OBJ = os.path.join(PKG, "build")
+# DLVM_BUILD_VARIANT=trace: a separate libdlvm_trace.so with -DDLVM_GEMM_TRACE
+# (GEMM phase stamps, tools/gemm_trace.py); the product library is unchanged
+VARIANT = os.environ.get("DLVM_BUILD_VARIANT", "")
+OUT = os.path.join(PKG, "libdlvm.so" if not VARIANT else f"libdlvm_{VARIANT}.so")
+OBJ = os.path.join(PKG, "build" if not VARIANT else f"build_{VARIANT}")
+VARIANT_FLAGS = {"": [], "trace": ["-DDLVM_GEMM_TRACE"]}[VARIANT]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", os.path.join(ROOT, "include")] + VARIANT_FLAGS
 
 
 def sources():
@@ -42,7 +46,7 @@ def _compile(src: str, is_cu: bool, newest_header: float) -> str:
         if os.environ.get("DLVM_PTXAS_V"):
             cmd += ["-Xptxas", "-v"]
     else:  # host-only C++ (front end, planner, C ABI)
-        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", "-I", CSRC,
+        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function"] + VARIANT_FLAGS + ["-I", CSRC,
                "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -65,3 +65,21 @@ int num_gemm_specs() {
 }
 
 }  // namespace dlvm
+
+#ifdef DLVM_GEMM_TRACE
+// Trace builds only (not part of dlvm.h): tcgen05 GEMM launches k = 0, 1, ...
+// after this call write their phase stamps to slice k % slots of `dev`
+// ([slots][148][8] u64, caller-owned device memory); NULL stops tracing.
+// Used by tools/gemm_trace.py.
+namespace dlvm {
+namespace kern {
+unsigned long long* g_gemm_trace_ptr = nullptr;
+int g_gemm_trace_slots = 1, g_gemm_trace_next = 0;
+}  // namespace kern
+}  // namespace dlvm
+extern "C" void dlvm_debug_gemm_trace(void* dev, int slots) {
+  dlvm::kern::g_gemm_trace_ptr = static_cast<unsigned long long*>(dev);
+  dlvm::kern::g_gemm_trace_slots = slots > 0 ? slots : 1;
+  dlvm::kern::g_gemm_trace_next = 0;
+}
+#endif

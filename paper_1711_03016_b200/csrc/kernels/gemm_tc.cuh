@@ -30,6 +30,15 @@
 #include "gemm_tc_kernel.cuh"
 #include "spec_registry.h"
 
+#ifdef DLVM_GEMM_TRACE
+namespace dlvm {
+namespace kern {
+extern unsigned long long* g_gemm_trace_ptr;  // gemm_tc.cu (trace builds)
+extern int g_gemm_trace_slots, g_gemm_trace_next;
+}  // namespace kern
+}  // namespace dlvm
+#endif
+
 namespace dlvm {
 
 namespace {
@@ -86,6 +95,11 @@ int num_sms() {
 bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
+#ifdef DLVM_GEMM_TRACE
+  // launch k of the traced run writes slice k % slots of [slots][148][8]
+  tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * 8
+                               : nullptr;
+#endif
   const int BN = p.bn;
   if (p.n_seg < 1 || p.n_seg > kMaxSeg) return false;
   for (int q = 0; q < p.n_seg; ++q) {

@@ -44,7 +44,27 @@ struct TcParams {
   GemmParams g;
   int32_t tiles_m, tiles_n;
   int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
+#ifdef DLVM_GEMM_TRACE
+  unsigned long long* trace;   // [gridDim.x][8] %globaltimer stamps (trace builds, tools/gemm_trace.py)
+#endif
 };
+
+// Phase stamps of a trace build (-DDLVM_GEMM_TRACE, build variant "trace"):
+// 0 entry, 1 after the PDL wait, 2 first TMA issued, 3 first stage landed
+// (MMA issuer), 4 last MMA committed, 5 first accumulator ready (epilogue
+// warp 4), 6 last epilogue tile done (warp 4), 7 exit.  No-ops otherwise.
+#ifdef DLVM_GEMM_TRACE
+#define DLVM_GT(P_, slot)                                                           \
+  do {                                                                              \
+    unsigned long long t_;                                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+    if ((P_).trace) (P_).trace[(size_t)blockIdx.x * 8 + (slot)] = t_;               \
+  } while (0)
+#else
+#define DLVM_GT(P_, slot) \
+  do {                    \
+  } while (0)
+#endif
 
 // CTA-pair (cta_group::2) primitives: a shared::cluster address of the same
 // offset in CTA `rank` of the cluster, remote arrive, cluster barrier
@@ -565,6 +585,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) DLVM_GT(P, 0);
   const int base_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
   const int nsplit = g.ksplit > 1 ? g.ksplit : 1;
   const int n_tiles = base_tiles * nsplit;       // work items (tile, K split)
@@ -606,6 +627,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   // previous kernel's results (PDL, launch.cuh)
   pdl_trigger_gemm();
   pdl_wait();
+  if (threadIdx.x == 0) DLVM_GT(P, 1);
 
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
     int s = 0;
@@ -635,6 +657,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           const int kb_lo = split * kbs, kb_hi = kb_lo + kbs < num_kb ? kb_lo + kbs : num_kb;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(empty_bar + 8 * s, ph ^ 1);
+            if (t == tile0 && q == 0 && kb == kb_lo) DLVM_GT(P, 2);
             const uint32_t fb = full_bar + 8 * s;
             const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
             const int k0 = kb * BK;
@@ -701,6 +724,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
             mbar_wait(full_bar + 8 * s, ph);
             tc_fence_after();
+            if (t == tile0 && q == 0 && kb == kb_lo) DLVM_GT(P, 3);
             const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -727,6 +751,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         else
           umma_commit(tfull_bar + 8 * as);
       }
+      DLVM_GT(P, 4);
     }
   } else if (warp >= 4) {  // ---------------- epilogue
     // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (lane = tile row, the
@@ -804,6 +829,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(tfull_bar + 8 * as, aph);
       tc_fence_after();
+      if (it == 0 && ew == 0 && lane == 0) DLVM_GT(P, 5);
       float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
 #pragma unroll
       for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
@@ -939,6 +965,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         epi_bar();
       }
     }
+    if (ew == 0 && lane == 0) DLVM_GT(P, 6);
   }
   tc_fence_before();
   __syncthreads();
@@ -950,6 +977,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
+  if (threadIdx.x == 0) DLVM_GT(P, 7);
 }
 
 }  // namespace kern

@@ -11,7 +11,8 @@ import ctypes
 import os
 from typing import List, Optional, Sequence, Tuple
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdlvm.so")
+# DLVM_LIBRARY: another build of the same ABI (e.g. the trace variant for tools/)
+_LIB_PATH = os.environ.get("DLVM_LIBRARY") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdlvm.so")
 
 DLVM_OK, DLVM_ERR_VERIFY, DLVM_ERR_PARSE, DLVM_ERR_USAGE, DLVM_ERR_RUNTIME, DLVM_ERR_CUDA, \
     DLVM_ERR_UNSUPPORTED = range(7)
