@@ -196,7 +196,7 @@ def kernel_breakdown(f, which, step, K, dev):
         from torch.profiler import ProfilerActivity, profile
         torch.cuda.synchronize(dev)
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
-            for _ in range(K):
+            for _ in range(K + 1):  # the first step primes the tracer (its first kernel can be missed)
                 step()
             torch.cuda.synchronize(dev)
         ks = [e for e in prof.profiler.kineto_results.events()

@@ -19,7 +19,8 @@ CSRC = os.path.join(PKG, "csrc")
 VARIANT = os.environ.get("DLVM_BUILD_VARIANT", "")
 OUT = os.path.join(PKG, "libdlvm.so" if not VARIANT else f"libdlvm_{VARIANT}.so")
 OBJ = os.path.join(PKG, "build" if not VARIANT else f"build_{VARIANT}")
-VARIANT_FLAGS = {"": [], "trace": ["-DDLVM_GEMM_TRACE"]}[VARIANT]
+VARIANT_FLAGS = {"": [], "trace": ["-DDLVM_GEMM_TRACE"], "s4": ["-DDLVM_GEMM_STAGES_PAIR=4"],
+                 "s5": ["-DDLVM_GEMM_STAGES_PAIR=5"]}[VARIANT]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -37,8 +37,8 @@ int gemm_tc_ctas(int64_t M, int bn) {
 
 cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStream_t stream) {
   TcParams tp;
-  if (!make_params(p, &tp, ctas)) return cudaErrorInvalidValue;
-  const int smem = ctas == 2 ? smem_bytes<256, 2>() : (p.bn == 256 ? smem_bytes<256, 1>() : smem_bytes<128, 1>());
+  if (!make_params(p, &tp, ctas, true)) return cudaErrorInvalidValue;  // NVRTC kernels run compile-time programs
+  const int smem = launch_smem(tp, p.bn, ctas);
   const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);  // work items (tile x K split)
   const int grid = ctas * std::min(items, num_sms() / ctas);
   LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), smem, stream, (unsigned)ctas, 1);

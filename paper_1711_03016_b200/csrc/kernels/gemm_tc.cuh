@@ -73,13 +73,142 @@ bool encode(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int
   return r == CUDA_SUCCESS;
 }
 
+constexpr int kMaxDynSmem = 227 * 1024;
+__host__ __device__ constexpr int stage_bytes(int bn, int ctas) { return A_STAGE_BYTES + (bn / ctas) * BK * 2; }
+// bytes after the stages: barriers (256) + the epilogue reduction scratch
+__host__ __device__ constexpr int tail_bytes(int bn) {
+  return 256 + (kEpiReds * 4 * bn + kEpiReds * 2 * BM + kEpiReds * 8) * 4;
+}
+constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
 template <int BN, int CTAS = 1>
 constexpr int smem_bytes() {
-  constexpr int NST = num_stages<CTAS, BN>();
-  return 1024 + NST * (A_STAGE_BYTES + (BN / CTAS) * BK * 2) + 16 * NST + 64 +
-         (kEpiReds * 4 * BN + kEpiReds * 2 * BM + kEpiReds * 8 + 8 * 32 * 17) * 4;
+  return 1024 + num_stages<CTAS, BN>() * stage_bytes(BN, CTAS) + tail_bytes(BN);
 }
-static_assert(smem_bytes<256, 2>() <= 227 * 1024, "CTA-pair stages exceed shared memory");
+static_assert(smem_bytes<256, 2>() <= kMaxDynSmem, "CTA-pair stages exceed shared memory");
+
+// dynamic shared memory of a launch: the default pipeline, or with the TMA
+// epilogue its stage count plus the staging region
+int launch_smem(const TcParams& tp, int bn, int ctas) {
+  if (!tp.et.on) return 1024 + num_stages_rt(ctas) * stage_bytes(bn, ctas) + tail_bytes(bn);
+  return 1024 + tp.et.epi_off + tp.et.n_in_bufs * tp.et.in_buf_bytes + 16 * tp.et.st_slot_bytes;
+}
+
+int es_of(uint8_t st) { return st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1; }
+
+// 2-D (or, with `splits`, 3-D {cols, rows, splits}) tensor map of an
+// epilogue operand: box {16 columns, box_rows rows}, swizzled by row width
+// (64 B: SWIZZLE_64B, 32 B: SWIZZLE_32B, 16 B: none) -- the layout
+// box_addr() reads and writes
+bool encode_epi(CUtensorMap* map, const void* ptr, uint8_t st, int64_t cols, int64_t rows, int64_t pitch_bytes,
+                int box_rows, int64_t splits = 0, int64_t split_bytes = 0) {
+  auto fn = get_encode();
+  if (!fn) return false;
+  const int es = es_of(st);
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 || pitch_bytes % 16 || pitch_bytes <= 0 || rows < 1 || cols < 1)
+    return false;
+  if (splits > 1 && split_bytes % 16) return false;
+  const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const CUtensorMapSwizzle sw = es == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : es == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)(splits > 1 ? splits : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch_bytes, (cuuint64_t)split_bytes};
+  cuuint32_t box[3] = {16u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t esd[3] = {1u, 1u, 1u};
+  const cuuint32_t rank = splits > 1 ? 3 : 2;
+  CUresult r = fn(map, dt, rank, const_cast<void*>(ptr), dims, strides, box, esd, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// TMA epilogue set-up (see EpiTma): stores, staged inputs, stage count.
+// `spec_prog`: the kernel runs a compile-time program (ahead-of-time or
+// NVRTC), whose chunk width follows from its slot count.
+void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_prog) {
+  EpiTma& et = tp->et;
+  et.on = 0;
+  static const bool enabled = [] {
+    const char* e = std::getenv("DLVM_GEMM_TMA_EPI");
+    return !(e && e[0] == '0');
+  }();
+  const EwParams& E = p.epi;
+  const EwProgram& Pg = E.prog;
+  if (!enabled || !spec_prog || epi_chunk_width(Pg.n_in + Pg.n_lits + Pg.n_ins) != 16 || Pg.n_stores < 1) return;
+  const int BN = p.bn;
+  // stores: every one TMA-legal, else the direct path for all
+  int off = 0;
+  for (int o = 0; o < Pg.n_stores; ++o) {
+    const EwDevOut& r = E.out[o];
+    const int es = es_of(r.st);
+    if (r.s[1] != 1) return;
+    const bool split = o == 0 && p.ksplit > 1;
+    if (!encode_epi(&tp->tma_st[o], r.ptr, r.st, p.N, p.M, r.s[0] * es, 32, split ? p.ksplit : 0,
+                    split ? p.split_bytes : 0))
+      return;
+    const int al = es == 4 ? 512 : es == 2 ? 256 : 128;
+    off = round_up(off, al);
+    et.st_off[o] = off;
+    off += 32 * 16 * es;
+  }
+  et.split3d = p.ksplit > 1;
+  et.st_slot_bytes = round_up(off, 512);
+  // staged inputs: [M, N] rows (kind 1, TMA boxes) and [1, N] f32 row vectors (kind 2)
+  int nmap = 0, in_bytes = 0, in1_bytes = 0;
+  int8_t kind[kMaxIn] = {0};
+  for (int s2 = 1; s2 < Pg.n_in; ++s2) {
+    const EwDevIn& in = E.in[s2];
+    if (in.nchunks != 1 || in.chunk_mul) continue;
+    const int es = es_of(in.st);
+    if (in.s[1] == 1 && in.s[0] != 0 && nmap < kEpiTmaIn &&
+        encode_epi(&tp->tma_in[nmap], in.ptr, in.st, p.N, p.M, in.s[0] * es, BM)) {
+      kind[s2] = 1;
+      et.in_map[s2] = (int8_t)nmap++;
+      et.in_chunk_bytes[s2] = BM * 16 * es;
+      in_bytes = round_up(in_bytes, 1024);
+      et.in_off[s2] = in_bytes;
+      in_bytes += (BN / 16) * BM * 16 * es;
+      in1_bytes += (BN / 16) * BM * 16 * es;
+    } else if (in.s[0] == 0 && in.s[1] == 1 && in.st == (uint8_t)SType::F32 && p.N % 4 == 0 &&
+               reinterpret_cast<uintptr_t>(in.ptr) % 16 == 0) {
+      kind[s2] = 2;
+      in_bytes = round_up(in_bytes, 16);
+      et.in_off[s2] = in_bytes;
+      in_bytes += BN * 4;
+    }
+  }
+  const int stage = stage_bytes(BN, ctas), tail = tail_bytes(BN);
+  const int nst_max = num_stages_rt(ctas), nst_min = ctas == 2 ? 4 : 3;
+  auto total = [&](int nst, int nbufs, int ibytes) {
+    return 1024 + round_up(nst * stage + tail, 1024) + nbufs * round_up(ibytes, 1024) + 16 * et.st_slot_bytes;
+  };
+  // prefer more pipeline stages, then two input buffers; drop the [M, N]
+  // inputs back to direct loads if even one buffer does not fit
+  for (int pass = 0; pass < 2; ++pass) {
+    const int ib = pass == 0 ? in_bytes : in_bytes - in1_bytes;  // pass 1: row vectors only
+    if (pass == 1) {
+      int o2 = 0;
+      for (int s2 = 1; s2 < kMaxIn; ++s2) {
+        if (kind[s2] == 1) kind[s2] = 0;
+        if (kind[s2] == 2) {
+          et.in_off[s2] = o2;
+          o2 += BN * 4;
+        }
+      }
+    }
+    for (int nst = nst_max; nst >= nst_min; --nst)
+      for (int nb = ib > 0 ? 2 : 0; nb >= (ib > 0 ? 1 : 0); --nb)
+        if (total(nst, nb, ib) <= kMaxDynSmem) {
+          for (int s2 = 0; s2 < kMaxIn; ++s2) et.in_kind[s2] = kind[s2];
+          et.nst = nst;
+          et.n_in_bufs = nb;
+          et.in_buf_bytes = round_up(ib, 1024);
+          et.epi_off = round_up(nst * stage + tail, 1024);
+          et.on = 1;
+          return;
+        }
+  }
+}
 
 int num_sms() {
   static int n = 0;
@@ -92,7 +221,7 @@ int num_sms() {
   return n;
 }
 
-bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1) {
+bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog = false) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
 #ifdef DLVM_GEMM_TRACE
@@ -143,6 +272,7 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1) {
       tp->hint_b = stream;
     }
   }
+  setup_tma_epilogue(p, tp, ctas, spec_prog);
   return true;
 }
 
@@ -159,7 +289,7 @@ template <int BN, class PROG, int CTAS>
 cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
   // the max-dynamic-smem attribute is per device: one bit per device ordinal
   static std::atomic<uint64_t> configured{0};
-  constexpr int SMEM = smem_bytes<BN, CTAS>();
+  constexpr int SMEM = kMaxDynSmem;  // the attribute allows every launch's size
   auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
   int dev = 0;
   cudaError_t e0 = cudaGetDevice(&dev);
@@ -171,12 +301,12 @@ cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
     configured.fetch_or(bit);
   }
   TcParams tp;
-  if (!make_params(p, &tp, CTAS)) return cudaErrorInvalidValue;
+  if (!make_params(p, &tp, CTAS, vm_cw<PROG>::value == 0)) return cudaErrorInvalidValue;
   // persistent: one CTA (pair) per SM (pair), up to one per work item
   // (tile x K split)
   const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);
   const int grid = CTAS * std::min(items, num_sms() / CTAS);
-  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), SMEM, stream, CTAS, 1);
+  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), launch_smem(tp, BN, CTAS), stream, CTAS, 1);
   cudaError_t e = cudaLaunchKernelEx(&L.cfg, kern, tp);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

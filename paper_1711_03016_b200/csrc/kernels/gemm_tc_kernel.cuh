@@ -38,9 +38,40 @@ namespace kern {
 constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 384;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
+// TMA epilogue (set up by make_params when the program is compile-time
+// specialised with 16-column chunks and its operands are TMA-legal):
+//  * stores: each epilogue warp writes its 32-row x 16-column chunk of every
+//    stored value into a per-warp shared-memory staging slot (two slots,
+//    swizzled like the TMA box so the row-per-lane writes are conflict-free)
+//    and one lane issues cp.async.bulk.tensor stores (bulk groups);
+//  * row-contiguous inputs ([M, N] operands such as the saved ReLU mask) and
+//    row-vector inputs ([1, N] biases) of a tile are loaded by warp 3 into a
+//    per-tile input buffer (TMA boxes of 16 columns x 128 rows; a 1-D bulk
+//    copy for row vectors) while the tile's MMAs run, completing on
+//    in_full[b]; the epilogue warps release it on in_empty[b].
+// The pipeline then runs with `nst` stages so everything fits in 227 KB.
+constexpr int kEpiTmaIn = 4;  // staged row-contiguous epilogue inputs (tensor maps)
+struct EpiTma {
+  int32_t on;                   // stores through staging + TMA
+  int32_t nst;                  // pipeline stages
+  int32_t n_in_bufs;            // 0 (no staged inputs), 1 or 2 per-tile input buffers
+  int32_t in_buf_bytes;         // one input buffer
+  int8_t in_kind[kMaxIn];       // per input slot: 0 direct, 1 staged [M,N] (map in_map), 2 staged [1,N] row vector
+  int8_t in_map[kMaxIn];
+  int32_t in_off[kMaxIn];       // byte offset of the slot's data in an input buffer
+  int32_t in_chunk_bytes[kMaxIn];  // one 16 x 128 box (kind 1)
+  int32_t st_off[kMaxStores];   // byte offset of store o in a warp's staging slot
+  int32_t st_slot_bytes;        // one staging slot
+  int32_t split3d;              // store 0 is the split-K partial: 3-D map {N, M, S}
+  int32_t epi_off;              // byte offset of the staging region from the aligned base
+};
+
 struct TcParams {
   CUtensorMap tma_a[kMaxSeg];  // per K segment (sums of products share one accumulator)
   CUtensorMap tma_b[kMaxSeg];
+  CUtensorMap tma_st[kMaxStores];  // TMA epilogue stores
+  CUtensorMap tma_in[kEpiTmaIn];   // TMA epilogue staged inputs
+  EpiTma et;
   GemmParams g;
   int32_t tiles_m, tiles_n;
   int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
@@ -117,6 +148,104 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "[%2], %5;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
+}
+
+// TMA epilogue primitives: smem -> global tensor stores in bulk groups
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1,
+                                             int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// Row r (0..), 16-byte chunk c of a staged 16-column box whose rows are
+// 16 * es bytes: the TMA swizzle of that row width (64 B rows: SWIZZLE_64B,
+// 32 B rows: SWIZZLE_32B, 16 B rows: none), so a warp's row-per-lane
+// 16-byte accesses hit distinct bank groups.
+__device__ __forceinline__ uint32_t box_addr(uint32_t base, int r, int c, int es) {
+  if (es == 4) return base + r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+  if (es == 2) return base + r * 32 + ((c ^ ((r >> 2) & 1)) << 4);
+  return base + r * 16;
+}
+
+// The 16 values of row r of a staged box -> float (stored type st)
+__device__ __forceinline__ void box_read16(uint32_t base, int r, uint8_t st, float* v) {
+  if (st == (uint8_t)SType::F32) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 x = lds128(box_addr(base, r, c, 4));
+      v[4 * c] = __uint_as_float(x.x); v[4 * c + 1] = __uint_as_float(x.y);
+      v[4 * c + 2] = __uint_as_float(x.z); v[4 * c + 3] = __uint_as_float(x.w);
+    }
+  } else if (st == (uint8_t)SType::BF16) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const uint4 x = lds128(box_addr(base, r, c, 2));
+      const unsigned w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[8 * c + 2 * k] = __uint_as_float(w[k] << 16);
+        v[8 * c + 2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+      }
+    }
+  } else {
+    const uint4 x = lds128(box_addr(base, r, 0, 1));
+    const unsigned w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[4 * k] = (w[k] & 0xffu) ? 1.f : 0.f;
+      v[4 * k + 1] = (w[k] & 0xff00u) ? 1.f : 0.f;
+      v[4 * k + 2] = (w[k] & 0xff0000u) ? 1.f : 0.f;
+      v[4 * k + 3] = (w[k] & 0xff000000u) ? 1.f : 0.f;
+    }
+  }
+}
+
+// Row r of a staged store box from 16 floats (stored as type st)
+__device__ __forceinline__ void box_write16(uint32_t base, int r, uint8_t st, const float* v) {
+  if (st == (uint8_t)SType::F32) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      sts128(box_addr(base, r, c, 4), __float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+             __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
+  } else if (st == (uint8_t)SType::BF16) {
+    unsigned w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = (unsigned)f2bf(v[2 * k]) | ((unsigned)f2bf(v[2 * k + 1]) << 16);
+    sts128(box_addr(base, r, 0, 2), w[0], w[1], w[2], w[3]);
+    sts128(box_addr(base, r, 1, 2), w[4], w[5], w[6], w[7]);
+  } else {
+    unsigned w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (v[4 * k] != 0.f ? 1u : 0u) | (v[4 * k + 1] != 0.f ? 0x100u : 0u) |
+             (v[4 * k + 2] != 0.f ? 0x10000u : 0u) | (v[4 * k + 3] != 0.f ? 0x1000000u : 0u);
+    sts128(box_addr(base, r, 0, 1), w[0], w[1], w[2], w[3]);
+  }
 }
 
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1
@@ -551,10 +680,14 @@ __host__ __device__ constexpr int epi_chunk_width(int slots) { return slots <= 6
 // of B's columns, the leader issues cta_group::2 MMAs over both CTAs' smem
 // into both CTAs' TMEM (per-SM smem traffic per MMA drops by a third), and
 // each CTA runs the epilogue of its own 128 rows.
+#ifndef DLVM_GEMM_STAGES_PAIR
+#define DLVM_GEMM_STAGES_PAIR 6
+#endif
 template <int CTAS, int BN>
 __host__ __device__ constexpr int num_stages() {
-  return CTAS == 2 ? 6 : STAGES;
+  return CTAS == 2 ? DLVM_GEMM_STAGES_PAIR : STAGES;
 }
+__host__ __device__ constexpr int num_stages_rt(int ctas) { return ctas == 2 ? DLVM_GEMM_STAGES_PAIR : STAGES; }
 
 template <int BN, class PROG, int CTAS = 1>
 __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ TcParams P) {
@@ -573,13 +706,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
+  const EpiTma& xt = P.et;
+  const int nst = xt.on ? xt.nst : NST;  // pipeline stages (fewer when the TMA epilogue stages)
   const uint32_t sA = base;
-  const uint32_t sB = base + NST * A_STAGE_BYTES;
-  const uint32_t sBar = sB + NST * B_STAGE_BYTES;  // full[S], empty[S], tfull[2], tempty[2]
-  const uint32_t full_bar = sBar, empty_bar = sBar + 8 * NST, tfull_bar = sBar + 16 * NST,
-                 tempty_bar = tfull_bar + 16;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 16 * NST + 32);
-  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 16 * NST + 64);  // [kEpiReds][4][BN]
+  const uint32_t sB = base + nst * A_STAGE_BYTES;
+  // barriers: full[<=6] @0, empty[<=6] @48, tfull[2] @96, tempty[2] @112,
+  // in_full[2] @128, in_empty[2] @144; TMEM address @192; reductions @256
+  const uint32_t sBar = sB + nst * B_STAGE_BYTES;
+  const uint32_t full_bar = sBar, empty_bar = sBar + 48, tfull_bar = sBar + 96, tempty_bar = sBar + 112,
+                 in_full_bar = sBar + 128, in_empty_bar = sBar + 144;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 192);
+  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 256);  // [kEpiReds][4][BN]
   float* rowred = colred + kEpiReds * 4 * BN;                                          // [kEpiReds][2][BM]
   float* allred = rowred + kEpiReds * 2 * BM;                                          // [kEpiReds][8]
 
@@ -593,13 +730,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(full_bar + 8 * s, 1);
       mbar_init(empty_bar + 8 * s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + 8 * s, 1);
       mbar_init(tempty_bar + 8 * s, 8 * CTAS);  // one arrival per epilogue warp of the pair
+      mbar_init(in_full_bar + 8 * s, 1);        // the loader's arrive + the staged bytes
+      mbar_init(in_empty_bar + 8 * s, 8);       // one arrival per epilogue warp of this CTA
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < g.n_seg; ++q) {
@@ -693,7 +832,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                 for (int c = 0; c < BNC / 64; ++c) tma_load_2d(b_dst + c * 8192, mb, fb, nb + 64 * c, k0, pol_b);
               }
             }
-            if (++s == NST) {
+            if (++s == nst) {
               s = 0;
               ph ^= 1;
             }
@@ -740,7 +879,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
               umma_commit_pair(empty_bar + 8 * s);  // both CTAs' slots are free
             else
               umma_commit(empty_bar + 8 * s);
-            if (++s == NST) {
+            if (++s == nst) {
               s = 0;
               ph ^= 1;
             }
@@ -752,6 +891,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           umma_commit(tfull_bar + 8 * as);
       }
       DLVM_GT(P, 4);
+    }
+  } else if (warp == 3) {  // ---------------- epilogue input loader (TMA epilogue)
+    if (xt.on && xt.n_in_bufs > 0 && lane == 0) {
+      const uint32_t in_base = base + (uint32_t)xt.epi_off;
+      const EwParams& E = g.epi;
+      int it = 0;
+      for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+        int tm, tn;
+        tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
+        const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
+        const int b = xt.n_in_bufs == 2 ? (it & 1) : 0;
+        const uint32_t ph = xt.n_in_bufs == 2 ? ((it >> 1) & 1) : (it & 1);
+        mbar_wait(in_empty_bar + 8 * b, ph ^ 1);
+        const uint32_t fb = in_full_bar + 8 * b;
+        const uint32_t buf = in_base + (uint32_t)(b * xt.in_buf_bytes);
+        const int cols = (int)min((int64_t)BN, g.N - n0);
+        uint32_t tx = 0;
+        for (int s2 = 1; s2 < kMaxIn; ++s2) {
+          if (xt.in_kind[s2] == 1) tx += (uint32_t)(BN / 16) * (uint32_t)xt.in_chunk_bytes[s2];
+          else if (xt.in_kind[s2] == 2) tx += (uint32_t)((cols * 4 + 15) & ~15);
+        }
+        mbar_expect_tx(fb, tx);
+        for (int s2 = 1; s2 < kMaxIn; ++s2) {
+          if (xt.in_kind[s2] == 1) {
+            const CUtensorMap* mp = &P.tma_in[xt.in_map[s2]];
+#pragma unroll 1
+            for (int c = 0; c < BN / 16; ++c)
+              tma_load_2d(buf + xt.in_off[s2] + c * xt.in_chunk_bytes[s2], mp, fb, n0 + 16 * c, m0, l2_policy(0));
+          } else if (xt.in_kind[s2] == 2) {
+            const float* src = reinterpret_cast<const float*>(E.in[s2].ptr) + n0;
+            bulk_load(buf + xt.in_off[s2], src, (uint32_t)((cols * 4 + 15) & ~15), fb);
+          }
+        }
+      }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
     // 8 warps: warp (q, h) owns TMEM lanes 32q..32q+31 (lane = tile row, the
@@ -792,6 +965,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         has_all |= red_kind(r) == RED_ALL;
       }
     const bool vec_ok = E.vec == 4;
+    // TMA epilogue (compile-time specialised programs with 16-column chunks)
+    constexpr bool TMA_EPI = SPEC && CW == 16;
+    const bool tma_on = TMA_EPI && xt.on;
+    const bool staged_in = tma_on && xt.n_in_bufs > 0;
+    const uint32_t in_base = base + (uint32_t)xt.epi_off;
+    const uint32_t st_base = in_base + (uint32_t)(xt.n_in_bufs * xt.in_buf_bytes) +
+                             (uint32_t)(ew * 2 * xt.st_slot_bytes);  // this warp's two staging slots
+    int kc = 0;  // this warp's chunk count (staging slot = kc & 1)
     int it = 0;
     for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
       int tm, tn;
@@ -830,6 +1011,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       mbar_wait(tfull_bar + 8 * as, aph);
       tc_fence_after();
       if (it == 0 && ew == 0 && lane == 0) DLVM_GT(P, 5);
+      const int ib = xt.n_in_bufs == 2 ? (it & 1) : 0;
+      const uint32_t in_buf = in_base + (uint32_t)(ib * xt.in_buf_bytes);
+      if (staged_in) mbar_wait(in_full_bar + 8 * ib, xt.n_in_bufs == 2 ? ((it >> 1) & 1) : (it & 1));
       float rowacc[NRS > 0 ? NRS : 1], allacc[NRS > 0 ? NRS : 1];
 #pragma unroll
       for (int r = 0; r < (NRS > 0 ? NRS : 1); ++r) rowacc[r] = allacc[r] = 0.f;
@@ -848,11 +1032,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       constexpr int SUB = 16 / CW;                 // chunks per 16-column block
       constexpr int NIT = BN / CW / 2;             // chunks per warp per tile
       auto chunk_of = [&](int i) { return (h + 2 * (i / SUB)) * SUB + i % SUB; };
+      auto staged = [&](int s2) { return staged_in && xt.in_kind[s2] != 0; };
       if constexpr (SPEC) {
         if (seg_full(chunk_of(0)))
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2)
-            if (seg_vector(E.in[s2]))
+            if (seg_vector(E.in[s2]) && !staged(s2))
               epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + chunk_of(0) * CW, pf[s2 - 1]);
       }
       for (int it = 0; it < NIT; ++it) {
@@ -868,7 +1053,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           if (it + 1 < NIT && seg_full(nx))
 #pragma unroll
             for (int s2 = 1; s2 < T::kIn; ++s2)
-              if (seg_vector(E.in[s2])) epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + nx * CW, pf[s2 - 1]);
+              if (seg_vector(E.in[s2]) && !staged(s2))
+                epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + nx * CW, pf[s2 - 1]);
           // row segments three chunks further on into L1 (no registers)
           const int nx3 = it + 3 < NIT ? chunk_of(it + 3) : 0;
           if (kEpiL1Prefetch && it + 3 < NIT && seg_full(nx3))
@@ -880,15 +1066,61 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         if constexpr (SPEC) {
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2) {
+            if constexpr (TMA_EPI) {
+              if (staged(s2)) {
+                if (xt.in_kind[s2] == 1) {  // [M, N]: row 32q+lane of chunk box ch
+                  box_read16(in_buf + xt.in_off[s2] + ch * xt.in_chunk_bytes[s2], 32 * q + lane, E.in[s2].st,
+                             reinterpret_cast<float*>(v[s2]));
+                } else {  // [1, N] row vector: the chunk's 16 values, same for every lane
+                  const uint32_t a0 = in_buf + xt.in_off[s2] + ch * 64;
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) {
+                    const uint4 x = lds128(a0 + 16 * c);
+                    v[s2][4 * c] = __uint_as_float(x.x); v[s2][4 * c + 1] = __uint_as_float(x.y);
+                    v[s2][4 * c + 2] = __uint_as_float(x.z); v[s2][4 * c + 3] = __uint_as_float(x.w);
+                  }
+                }
+                continue;
+              }
+            }
             if (full && seg_vector(E.in[s2]))
               epi_row_decode<CW>(E.in[s2], cur[s2 - 1], v[s2]);
             else
               epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
           }
           T::template exec<CW>(v);
+          if (tma_on) {
+            if constexpr (TMA_EPI) {
+              // stage this chunk's stores (slot kc & 1) and hand them to TMA;
+              // the group that last used the slot (two chunks ago) must have
+              // finished reading it
+              const uint32_t slot = st_base + (uint32_t)((kc & 1) * xt.st_slot_bytes);
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
 #pragma unroll
-          for (int s2 = 0; s2 < T::Stores::n; ++s2)
-            epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
+              for (int s2 = 0; s2 < T::Stores::n; ++s2)
+                box_write16(slot + xt.st_off[s2], lane, (s2 == 0 ? out0 : E.out[s2]).st,
+                            reinterpret_cast<const float*>(v[T::Stores::at(s2)]));
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                const int32_t r0 = tm * BM + 32 * q;
+#pragma unroll
+                for (int s2 = 0; s2 < T::Stores::n; ++s2) {
+                  if (s2 == 0 && xt.split3d)
+                    tma_store_3d(&P.tma_st[0], slot + xt.st_off[0], (int32_t)n0, r0, split);
+                  else
+                    tma_store_2d(&P.tma_st[s2], slot + xt.st_off[s2], (int32_t)n0, r0);
+                }
+                bulk_commit();
+              }
+              ++kc;
+            }
+          } else {
+#pragma unroll
+            for (int s2 = 0; s2 < T::Stores::n; ++s2)
+              epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
+          }
         } else {
           for (int s2 = 1; s2 < Pg.n_in; ++s2) epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
           vm_exec<CW>(Pg, v);
@@ -914,6 +1146,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             for (int j = 0; j < CW; ++j) allacc[r] = __fadd_rn(allacc[r], x[j]);
           }
         }
+      }
+      // this warp is done with the tile's staged inputs
+      if (staged_in) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(in_empty_bar + 8 * ib);
       }
       // accumulator buffer free for the next tile's MMAs (one arrival per warp,
       // on the leader's barrier for a pair)
@@ -965,6 +1202,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         epi_bar();
       }
     }
+    if (tma_on && lane == 0) bulk_wait_all();  // this warp's TMA stores are complete
     if (ew == 0 && lane == 0) DLVM_GT(P, 6);
   }
   tc_fence_before();
