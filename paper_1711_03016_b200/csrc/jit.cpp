@@ -148,8 +148,17 @@ const char* kSource =
     "#include \"gemm_simt_kernel.cuh\"\n";
 
 std::vector<std::string> options() {
-  return {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-I" + kernel_dir(),
-          "-I" + cuda_include()};
+  std::vector<std::string> o = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device", "-lineinfo",
+                                "-I" + kernel_dir(), "-I" + cuda_include()};
+  // a build variant's kernel-layout defines apply to create-time kernels too
+  // (they are part of the cache key below)
+#ifdef DLVM_GEMM_TRACE
+  o.push_back("-DDLVM_GEMM_TRACE");
+#endif
+#ifdef DLVM_GEMM_STAGES_PAIR
+  o.push_back("-DDLVM_GEMM_STAGES_PAIR=" + std::to_string(DLVM_GEMM_STAGES_PAIR));
+#endif
+  return o;
 }
 
 // NVRTC compile of one instantiation -> (lowered name, cubin)

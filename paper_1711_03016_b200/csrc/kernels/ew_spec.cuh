@@ -15,7 +15,9 @@ namespace dlvm {
 namespace spec {
 
 template <int OP, int D, int A, int B, int C>
-struct Ins {};
+struct Ins {
+  static constexpr int op = OP, dst = D;
+};
 template <int... S>
 struct St {};
 template <int... R>  // flattened (slot, kind) pairs
@@ -62,6 +64,14 @@ struct Traits<Prog<NIN, NLIT, St<S...>, Rd<R...>, Is...>> {
   template <int VEC>
   __device__ __forceinline__ static void exec(float (&v)[kSlots][VEC]) {
     (one<VEC>(v, Is{}), ...);
+  }
+  // slot d holds only 0.0f / 1.0f: written by a compare or a cast to bool
+  __host__ __device__ static constexpr bool is01(int d) {
+    constexpr int ops[] = {Is::op..., -1};
+    constexpr int dst[] = {Is::dst..., -1};
+    for (int k = 0; k < (int)sizeof...(Is); ++k)
+      if (dst[k] == d) return (ops[k] >= VM_LT && ops[k] <= VM_NE) || ops[k] == VM_TOBOOL;
+    return false;
   }
 };
 

@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -91,30 +92,31 @@ static_assert(smem_bytes<256, 2>() <= kMaxDynSmem, "CTA-pair stages exceed share
 // epilogue its stage count plus the staging region
 int launch_smem(const TcParams& tp, int bn, int ctas) {
   if (!tp.et.on) return 1024 + num_stages_rt(ctas) * stage_bytes(bn, ctas) + tail_bytes(bn);
-  return 1024 + tp.et.epi_off + tp.et.n_in_bufs * tp.et.in_buf_bytes + 16 * tp.et.st_slot_bytes;
+  return 1024 + tp.et.epi_off + tp.et.n_in_bufs * tp.et.in_buf_bytes + 8 * tp.et.st_slot_bytes;
 }
 
 int es_of(uint8_t st) { return st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1; }
 
 // 2-D (or, with `splits`, 3-D {cols, rows, splits}) tensor map of an
-// epilogue operand: box {16 columns, box_rows rows}, swizzled by row width
-// (64 B: SWIZZLE_64B, 32 B: SWIZZLE_32B, 16 B: none) -- the layout
-// box_addr() reads and writes
+// epilogue operand with box {box_cols, box_rows}; box rows of 128 bytes use
+// SWIZZLE_128B, of 64 bytes SWIZZLE_64B (the layouts sw128 / sw64 read and
+// write)
 bool encode_epi(CUtensorMap* map, const void* ptr, uint8_t st, int64_t cols, int64_t rows, int64_t pitch_bytes,
-                int box_rows, int64_t splits = 0, int64_t split_bytes = 0) {
+                int box_cols, int box_rows, int64_t splits = 0, int64_t split_bytes = 0) {
   auto fn = get_encode();
   if (!fn) return false;
   const int es = es_of(st);
+  const int row_bytes = box_cols * es;
   if (reinterpret_cast<uintptr_t>(ptr) % 16 || pitch_bytes % 16 || pitch_bytes <= 0 || rows < 1 || cols < 1)
     return false;
   if (splits > 1 && split_bytes % 16) return false;
+  if (row_bytes != 128 && row_bytes != 64) return false;
   const CUtensorMapDataType dt = es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
-  const CUtensorMapSwizzle sw = es == 4 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                : es == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)(splits > 1 ? splits : 1)};
   cuuint64_t strides[2] = {(cuuint64_t)pitch_bytes, (cuuint64_t)split_bytes};
-  cuuint32_t box[3] = {16u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1u};
   cuuint32_t esd[3] = {1u, 1u, 1u};
   const cuuint32_t rank = splits > 1 ? 3 : 2;
   CUresult r = fn(map, dt, rank, const_cast<void*>(ptr), dims, strides, box, esd, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
@@ -125,7 +127,24 @@ bool encode_epi(CUtensorMap* map, const void* ptr, uint8_t st, int64_t cols, int
 // TMA epilogue set-up (see EpiTma): stores, staged inputs, stage count.
 // `spec_prog`: the kernel runs a compile-time program (ahead-of-time or
 // NVRTC), whose chunk width follows from its slot count.
+void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool spec_prog);
+// DLVM_EPI_VERBOSE=1: one stderr line per launch set-up (TMA epilogue on/off, stages, buffers)
 void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_prog) {
+  setup_tma_epilogue_impl(p, tp, ctas, spec_prog);
+  static const bool verbose = [] {
+    const char* e = std::getenv("DLVM_EPI_VERBOSE");
+    return e && e[0] == '1';
+  }();
+  if (verbose) {
+    const EpiTma& et = tp->et;
+    fprintf(stderr, "dlvm gemm M=%lld N=%lld bn=%d ctas=%d spec=%d slots=%d stores=%d: tma_epi=%d nst=%d in_bufs=%d "
+            "in_buf=%d st_region=%d\n", (long long)p.M, (long long)p.N, p.bn, ctas, (int)spec_prog,
+            p.epi.prog.n_in + p.epi.prog.n_lits + p.epi.prog.n_ins, p.epi.prog.n_stores, et.on, et.nst,
+            et.n_in_bufs, et.in_buf_bytes, et.st_slot_bytes);
+  }
+}
+
+void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool spec_prog) {
   EpiTma& et = tp->et;
   et.on = 0;
   static const bool enabled = [] {
@@ -136,39 +155,42 @@ void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_p
   const EwProgram& Pg = E.prog;
   if (!enabled || !spec_prog || epi_chunk_width(Pg.n_in + Pg.n_lits + Pg.n_ins) != 16 || Pg.n_stores < 1) return;
   const int BN = p.bn;
-  // stores: every one TMA-legal, else the direct path for all
+  // stores: every one TMA-legal, else the direct path for all.  A warp's
+  // staging region holds one 32-row x 64-column group of every store: f32 as
+  // two 32-column boxes (4 KB each), bf16 one box of 128-byte rows (4 KB),
+  // bytes one box of 64-byte rows (2 KB)
   int off = 0;
   for (int o = 0; o < Pg.n_stores; ++o) {
     const EwDevOut& r = E.out[o];
     const int es = es_of(r.st);
     if (r.s[1] != 1) return;
     const bool split = o == 0 && p.ksplit > 1;
-    if (!encode_epi(&tp->tma_st[o], r.ptr, r.st, p.N, p.M, r.s[0] * es, 32, split ? p.ksplit : 0,
-                    split ? p.split_bytes : 0))
+    if (!encode_epi(&tp->tma_st[o], r.ptr, r.st, p.N, p.M, r.s[0] * es, es == 4 ? 32 : 64, 32,
+                    split ? p.ksplit : 0, split ? p.split_bytes : 0))
       return;
-    const int al = es == 4 ? 512 : es == 2 ? 256 : 128;
-    off = round_up(off, al);
+    off = round_up(off, es == 1 ? 512 : 1024);
     et.st_off[o] = off;
-    off += 32 * 16 * es;
+    off += es == 4 ? 8192 : es == 2 ? 4096 : 2048;
   }
   et.split3d = p.ksplit > 1;
-  et.st_slot_bytes = round_up(off, 512);
-  // staged inputs: [M, N] rows (kind 1, TMA boxes) and [1, N] f32 row vectors (kind 2)
+  et.st_slot_bytes = round_up(off, 1024);
+  // staged inputs: [M, N] rows (kind 1: boxes of 128 rows x 128 bytes) and
+  // [1, N] f32 row vectors (kind 2)
   int nmap = 0, in_bytes = 0, in1_bytes = 0;
   int8_t kind[kMaxIn] = {0};
   for (int s2 = 1; s2 < Pg.n_in; ++s2) {
     const EwDevIn& in = E.in[s2];
     if (in.nchunks != 1 || in.chunk_mul) continue;
     const int es = es_of(in.st);
-    if (in.s[1] == 1 && in.s[0] != 0 && nmap < kEpiTmaIn &&
-        encode_epi(&tp->tma_in[nmap], in.ptr, in.st, p.N, p.M, in.s[0] * es, BM)) {
+    if (in.s[1] == 1 && in.s[0] != 0 && nmap < kEpiTmaIn && BN % (128 / es) == 0 &&
+        encode_epi(&tp->tma_in[nmap], in.ptr, in.st, p.N, p.M, in.s[0] * es, 128 / es, BM)) {
       kind[s2] = 1;
       et.in_map[s2] = (int8_t)nmap++;
-      et.in_chunk_bytes[s2] = BM * 16 * es;
+      et.in_cols[s2] = 128 / es;
       in_bytes = round_up(in_bytes, 1024);
       et.in_off[s2] = in_bytes;
-      in_bytes += (BN / 16) * BM * 16 * es;
-      in1_bytes += (BN / 16) * BM * 16 * es;
+      in_bytes += BN * es * BM;
+      in1_bytes += BN * es * BM;
     } else if (in.s[0] == 0 && in.s[1] == 1 && in.st == (uint8_t)SType::F32 && p.N % 4 == 0 &&
                reinterpret_cast<uintptr_t>(in.ptr) % 16 == 0) {
       kind[s2] = 2;
@@ -180,7 +202,7 @@ void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_p
   const int stage = stage_bytes(BN, ctas), tail = tail_bytes(BN);
   const int nst_max = num_stages_rt(ctas), nst_min = ctas == 2 ? 4 : 3;
   auto total = [&](int nst, int nbufs, int ibytes) {
-    return 1024 + round_up(nst * stage + tail, 1024) + nbufs * round_up(ibytes, 1024) + 16 * et.st_slot_bytes;
+    return 1024 + round_up(nst * stage + tail, 1024) + nbufs * round_up(ibytes, 1024) + 8 * et.st_slot_bytes;
   };
   // prefer more pipeline stages, then two input buffers; drop the [M, N]
   // inputs back to direct loads if even one buffer does not fit
@@ -205,6 +227,11 @@ void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_p
           et.in_buf_bytes = round_up(ib, 1024);
           et.epi_off = round_up(nst * stage + tail, 1024);
           et.on = 1;
+          static const int dbg = [] {
+            const char* e = std::getenv("DLVM_EPI_DBG");
+            return e ? std::atoi(e) : 0;
+          }();
+          et.dbg = dbg;
           return;
         }
   }

@@ -40,13 +40,16 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
 // TMA epilogue (set up by make_params when the program is compile-time
 // specialised with 16-column chunks and its operands are TMA-legal):
-//  * stores: each epilogue warp writes its 32-row x 16-column chunk of every
-//    stored value into a per-warp shared-memory staging slot (two slots,
-//    swizzled like the TMA box so the row-per-lane writes are conflict-free)
-//    and one lane issues cp.async.bulk.tensor stores (bulk groups);
+//  * stores: each epilogue warp writes its 32-row x 64-column column group of
+//    every stored value (four 16-column chunks) into its shared-memory
+//    staging region, swizzled like the TMA box so the row-per-lane writes
+//    are conflict-free, and one lane issues cp.async.bulk.tensor stores
+//    (bulk groups) of 64-byte or 128-byte rows.  The TMA unit's cost grows
+//    with the number of box rows, so wide rows matter (measured: 16-column
+//    boxes cost ~2.3 us per stored value per 128x256 tile);
 //  * row-contiguous inputs ([M, N] operands such as the saved ReLU mask) and
 //    row-vector inputs ([1, N] biases) of a tile are loaded by warp 3 into a
-//    per-tile input buffer (TMA boxes of 16 columns x 128 rows; a 1-D bulk
+//    per-tile input buffer (TMA boxes of 128 rows x 128 bytes; a 1-D bulk
 //    copy for row vectors) while the tile's MMAs run, completing on
 //    in_full[b]; the epilogue warps release it on in_empty[b].
 // The pipeline then runs with `nst` stages so everything fits in 227 KB.
@@ -59,11 +62,12 @@ struct EpiTma {
   int8_t in_kind[kMaxIn];       // per input slot: 0 direct, 1 staged [M,N] (map in_map), 2 staged [1,N] row vector
   int8_t in_map[kMaxIn];
   int32_t in_off[kMaxIn];       // byte offset of the slot's data in an input buffer
-  int32_t in_chunk_bytes[kMaxIn];  // one 16 x 128 box (kind 1)
-  int32_t st_off[kMaxStores];   // byte offset of store o in a warp's staging slot
-  int32_t st_slot_bytes;        // one staging slot
+  int32_t in_cols[kMaxIn];      // kind 1: columns per 128-row box (128-byte rows: 128 / element size)
+  int32_t st_off[kMaxStores];   // byte offset of store o in a warp's staging region
+  int32_t st_slot_bytes;        // one warp's staging region (one 32 x 64 group of every store)
   int32_t split3d;              // store 0 is the split-K partial: 3-D map {N, M, S}
   int32_t epi_off;              // byte offset of the staging region from the aligned base
+  int32_t dbg;                  // DLVM_EPI_DBG & 8 (trace builds): per-section cycles of epilogue warp 4
 };
 
 struct TcParams {
@@ -91,7 +95,16 @@ struct TcParams {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
     if ((P_).trace) (P_).trace[(size_t)blockIdx.x * 8 + (slot)] = t_;               \
   } while (0)
+#define DLVM_SECT(var)                                                  \
+  do {                                                                  \
+    long long c_ = clock64();                                           \
+    var += c_ - sect_t0;                                                \
+    sect_t0 = c_;                                                       \
+  } while (0)
 #else
+#define DLVM_SECT(var) \
+  do {                 \
+  } while (0)
 #define DLVM_GT(P_, slot) \
   do {                    \
   } while (0)
@@ -182,29 +195,31 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   return v;
 }
 
-// Row r (0..), 16-byte chunk c of a staged 16-column box whose rows are
-// 16 * es bytes: the TMA swizzle of that row width (64 B rows: SWIZZLE_64B,
-// 32 B rows: SWIZZLE_32B, 16 B rows: none), so a warp's row-per-lane
-// 16-byte accesses hit distinct bank groups.
-__device__ __forceinline__ uint32_t box_addr(uint32_t base, int r, int c, int es) {
-  if (es == 4) return base + r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
-  if (es == 2) return base + r * 32 + ((c ^ ((r >> 2) & 1)) << 4);
-  return base + r * 16;
+// Staged epilogue boxes.  Every box row is 128 bytes (SWIZZLE_128B: the
+// 16-byte unit u of row r sits at unit u ^ (r & 7)) or, for byte stores of
+// a 64-column group, 64 bytes (SWIZZLE_64B: unit u at u ^ ((r >> 1) & 3)),
+// so the row-per-lane 16-byte accesses of a warp hit distinct bank groups.
+__device__ __forceinline__ uint32_t sw128(uint32_t base, int r, int u) {
+  return base + r * 128 + ((u ^ (r & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t sw64(uint32_t base, int r, int u) {
+  return base + r * 64 + ((u ^ ((r >> 1) & 3)) << 4);
 }
 
-// The 16 values of row r of a staged box -> float (stored type st)
-__device__ __forceinline__ void box_read16(uint32_t base, int r, uint8_t st, float* v) {
+// 16 values of row r starting at 16-byte unit u0 of a 128-byte-row staged
+// input box (stored type st) -> float
+__device__ __forceinline__ void box_read16(uint32_t base, int r, int u0, uint8_t st, float* v) {
   if (st == (uint8_t)SType::F32) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const uint4 x = lds128(box_addr(base, r, c, 4));
+      const uint4 x = lds128(sw128(base, r, u0 + c));
       v[4 * c] = __uint_as_float(x.x); v[4 * c + 1] = __uint_as_float(x.y);
       v[4 * c + 2] = __uint_as_float(x.z); v[4 * c + 3] = __uint_as_float(x.w);
     }
   } else if (st == (uint8_t)SType::BF16) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const uint4 x = lds128(box_addr(base, r, c, 2));
+      const uint4 x = lds128(sw128(base, r, u0 + c));
       const unsigned w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -213,7 +228,7 @@ __device__ __forceinline__ void box_read16(uint32_t base, int r, uint8_t st, flo
       }
     }
   } else {
-    const uint4 x = lds128(box_addr(base, r, 0, 1));
+    const uint4 x = lds128(sw128(base, r, u0));
     const unsigned w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -225,26 +240,48 @@ __device__ __forceinline__ void box_read16(uint32_t base, int r, uint8_t st, flo
   }
 }
 
-// Row r of a staged store box from 16 floats (stored as type st)
-__device__ __forceinline__ void box_write16(uint32_t base, int r, uint8_t st, const float* v) {
+__device__ __forceinline__ unsigned pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // one cvt.rn.bf16x2.f32, RNE like f2bf
+  return *reinterpret_cast<const unsigned*>(&h);
+}
+// four values known to be exactly 0.0f / 1.0f -> bytes 0 / 1: byte 3 of 1.0f
+// is 0x3f, of 0.0f 0x00, so the low bit of that byte is the value
+__device__ __forceinline__ unsigned pack01x4(float a, float b, float c, float d) {
+  const unsigned ab = __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0073);
+  const unsigned cd = __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0073);
+  return __byte_perm(ab, cd, 0x5410) & 0x01010101u;
+}
+
+// Chunk gi (16 columns) of row r of a warp's staged 32-row x 64-column store
+// group, stored as type st: f32 in two 32-column boxes of 128-byte rows
+// (4 KB apart), bf16 one box of 128-byte rows, bytes one box of 64-byte
+// rows.  `is01`: the values are 0.0f / 1.0f (a compare result), which pack
+// to bytes without per-element compares.
+__device__ __forceinline__ void grp_write16(uint32_t base, int r, int gi, uint8_t st, const float* v, bool is01) {
   if (st == (uint8_t)SType::F32) {
+    const uint32_t b = base + (gi >> 1) * 4096;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      sts128(box_addr(base, r, c, 4), __float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+      sts128(sw128(b, r, (gi & 1) * 4 + c), __float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
              __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
   } else if (st == (uint8_t)SType::BF16) {
     unsigned w[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = (unsigned)f2bf(v[2 * k]) | ((unsigned)f2bf(v[2 * k + 1]) << 16);
-    sts128(box_addr(base, r, 0, 2), w[0], w[1], w[2], w[3]);
-    sts128(box_addr(base, r, 1, 2), w[4], w[5], w[6], w[7]);
+    for (int k = 0; k < 8; ++k) w[k] = pack_bf16x2(v[2 * k], v[2 * k + 1]);
+    sts128(sw128(base, r, 2 * gi), w[0], w[1], w[2], w[3]);
+    sts128(sw128(base, r, 2 * gi + 1), w[4], w[5], w[6], w[7]);
   } else {
     unsigned w[4];
+    if (is01) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      w[k] = (v[4 * k] != 0.f ? 1u : 0u) | (v[4 * k + 1] != 0.f ? 0x100u : 0u) |
-             (v[4 * k + 2] != 0.f ? 0x10000u : 0u) | (v[4 * k + 3] != 0.f ? 0x1000000u : 0u);
-    sts128(box_addr(base, r, 0, 1), w[0], w[1], w[2], w[3]);
+      for (int k = 0; k < 4; ++k) w[k] = pack01x4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        w[k] = (v[4 * k] != 0.f ? 1u : 0u) | (v[4 * k + 1] != 0.f ? 0x100u : 0u) |
+               (v[4 * k + 2] != 0.f ? 0x10000u : 0u) | (v[4 * k + 3] != 0.f ? 0x1000000u : 0u);
+    }
+    sts128(sw64(base, r, gi), w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -909,16 +946,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const int cols = (int)min((int64_t)BN, g.N - n0);
         uint32_t tx = 0;
         for (int s2 = 1; s2 < kMaxIn; ++s2) {
-          if (xt.in_kind[s2] == 1) tx += (uint32_t)(BN / 16) * (uint32_t)xt.in_chunk_bytes[s2];
+          if (xt.in_kind[s2] == 1) tx += (uint32_t)(BN / xt.in_cols[s2]) * (uint32_t)(BM * 128);
           else if (xt.in_kind[s2] == 2) tx += (uint32_t)((cols * 4 + 15) & ~15);
         }
         mbar_expect_tx(fb, tx);
         for (int s2 = 1; s2 < kMaxIn; ++s2) {
           if (xt.in_kind[s2] == 1) {
             const CUtensorMap* mp = &P.tma_in[xt.in_map[s2]];
+            const int ic = xt.in_cols[s2];
 #pragma unroll 1
-            for (int c = 0; c < BN / 16; ++c)
-              tma_load_2d(buf + xt.in_off[s2] + c * xt.in_chunk_bytes[s2], mp, fb, n0 + 16 * c, m0, l2_policy(0));
+            for (int c = 0; c < BN / ic; ++c)
+              tma_load_2d(buf + xt.in_off[s2] + c * (BM * 128), mp, fb, n0 + ic * c, m0, l2_policy(0));
           } else if (xt.in_kind[s2] == 2) {
             const float* src = reinterpret_cast<const float*>(E.in[s2].ptr) + n0;
             bulk_load(buf + xt.in_off[s2], src, (uint32_t)((cols * 4 + 15) & ~15), fb);
@@ -971,8 +1009,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     const bool staged_in = tma_on && xt.n_in_bufs > 0;
     const uint32_t in_base = base + (uint32_t)xt.epi_off;
     const uint32_t st_base = in_base + (uint32_t)(xt.n_in_bufs * xt.in_buf_bytes) +
-                             (uint32_t)(ew * 2 * xt.st_slot_bytes);  // this warp's two staging slots
-    int kc = 0;  // this warp's chunk count (staging slot = kc & 1)
+                             (uint32_t)(ew * xt.st_slot_bytes);  // this warp's staging region
+#ifdef DLVM_GEMM_TRACE
+    long long sect[6] = {0, 0, 0, 0, 0, 0}, sect_t0 = clock64();
+#endif
     int it = 0;
     for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
       int tm, tn;
@@ -983,6 +1023,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       EwDevOut out0 = E.out[0];
       out0.ptr = static_cast<char*>(out0.ptr) + (int64_t)split * g.split_bytes;
       const bool block_live = (int64_t)tm * BM < g.M;
+      const bool tile_full = (int64_t)tm * BM + BM <= g.M && (int64_t)tn * BN + BN <= g.N;
       const int64_t m = (int64_t)tm * BM + 32 * q + lane;
       const bool mval = m < g.M;
       // this row's segments take the vector path only if every row-contiguous
@@ -1029,12 +1070,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       // not depend on the chunk width: a kept loss computed by the gradient's
       // epilogue equals the primal's bit for bit (reading A20) even when the
       // two programs get different chunk widths
-      constexpr int SUB = 16 / CW;                 // chunks per 16-column block
+      constexpr int GCH = 64 / CW;                 // chunks per 64-column group
       constexpr int NIT = BN / CW / 2;             // chunks per warp per tile
-      auto chunk_of = [&](int i) { return (h + 2 * (i / SUB)) * SUB + i % SUB; };
+      auto chunk_of = [&](int i) { return (h + 2 * (i / GCH)) * GCH + i % GCH; };
       auto staged = [&](int s2) { return staged_in && xt.in_kind[s2] != 0; };
+      // fast TMA tile: every input is staged or constant along the row
+      // (column vector / scalar: loaded once per tile) -- no per-chunk
+      // global loads, prefetch registers or bounds checks
+      bool fast = false;
+      float rowc[SPEC && T::kIn > 1 ? T::kIn : 1];
+      if constexpr (TMA_EPI) {
+        fast = tma_on;
+#pragma unroll
+        for (int s2 = 1; s2 < T::kIn; ++s2) {
+          const bool st_ = staged(s2);
+          fast = fast && (st_ || E.in[s2].s[1] == 0);
+          rowc[s2] = (!st_ && E.in[s2].s[1] == 0 && mval) ? ld1(E.in[s2].ptr, m * E.in[s2].s[0], E.in[s2].st) : 0.f;
+        }
+      }
       if constexpr (SPEC) {
-        if (seg_full(chunk_of(0)))
+        if (!fast && seg_full(chunk_of(0)))
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2)
             if (seg_vector(E.in[s2]) && !staged(s2))
@@ -1043,10 +1098,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       for (int it = 0; it < NIT; ++it) {
         const int ch = chunk_of(it);
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
-        const int ncol = (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
+        const int ncol = tile_full ? CW : (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
         const bool full = mval && ncol == CW && row_vec;
         RawSeg<CW> cur[NPF];
-        if constexpr (SPEC) {
+        if constexpr (SPEC) if (!fast) {
 #pragma unroll
           for (int s2 = 0; s2 < NPF; ++s2) cur[s2] = pf[s2];
           const int nx = it + 1 < NIT ? chunk_of(it + 1) : 0;
@@ -1062,15 +1117,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             for (int s2 = 1; s2 < T::kIn; ++s2)
               if (seg_vector(E.in[s2])) epi_row_prefetch_l1(E.in[s2], m, (int64_t)tn * BN + nx3 * CW);
         }
+        DLVM_SECT(sect[0]);  // prefetch / loop overhead
         tmem_ldn<CW>(tmem_base + ((uint32_t)(32 * q) << 16) + as * BN + ch * CW, v[0]);
+        DLVM_SECT(sect[1]);  // TMEM load
         if constexpr (SPEC) {
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2) {
             if constexpr (TMA_EPI) {
+              if (fast && !staged(s2)) {
+#pragma unroll
+                for (int j = 0; j < CW; ++j) v[s2][j] = rowc[s2];
+                continue;
+              }
               if (staged(s2)) {
-                if (xt.in_kind[s2] == 1) {  // [M, N]: row 32q+lane of chunk box ch
-                  box_read16(in_buf + xt.in_off[s2] + ch * xt.in_chunk_bytes[s2], 32 * q + lane, E.in[s2].st,
-                             reinterpret_cast<float*>(v[s2]));
+                if (xt.in_kind[s2] == 1) {  // [M, N]: row 32q+lane, columns ch*16.. of the tile
+                  const int ic = xt.in_cols[s2], col = ch * CW;
+                  const int es = 128 / ic;
+                  box_read16(in_buf + xt.in_off[s2] + (col / ic) * (BM * 128), 32 * q + lane, ((col % ic) * es) >> 4,
+                             E.in[s2].st, reinterpret_cast<float*>(v[s2]));
                 } else {  // [1, N] row vector: the chunk's 16 values, same for every lane
                   const uint32_t a0 = in_buf + xt.in_off[s2] + ch * 64;
 #pragma unroll
@@ -1088,33 +1152,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             else
               epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
           }
+          DLVM_SECT(sect[2]);  // inputs
           T::template exec<CW>(v);
+          DLVM_SECT(sect[3]);  // program
           if (tma_on) {
             if constexpr (TMA_EPI) {
-              // stage this chunk's stores (slot kc & 1) and hand them to TMA;
-              // the group that last used the slot (two chunks ago) must have
-              // finished reading it
-              const uint32_t slot = st_base + (uint32_t)((kc & 1) * xt.st_slot_bytes);
-              if (lane == 0) bulk_wait_read<1>();
-              __syncwarp();
+              // stage this chunk into the warp's 32 x 64 group boxes; the
+              // group's first chunk waits until the TMA has read the
+              // previous group, its last one hands the boxes to TMA
+              const int gi = it % GCH;
+              if (gi == 0) {
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+              }
 #pragma unroll
               for (int s2 = 0; s2 < T::Stores::n; ++s2)
-                box_write16(slot + xt.st_off[s2], lane, (s2 == 0 ? out0 : E.out[s2]).st,
-                            reinterpret_cast<const float*>(v[T::Stores::at(s2)]));
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                const int32_t r0 = tm * BM + 32 * q;
+                grp_write16(st_base + xt.st_off[s2], lane, gi, (s2 == 0 ? out0 : E.out[s2]).st,
+                            reinterpret_cast<const float*>(v[T::Stores::at(s2)]), T::is01(T::Stores::at(s2)));
+              if (gi == GCH - 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  const int32_t r0 = tm * BM + 32 * q;
+                  const int32_t c0 = (int32_t)((int64_t)tn * BN + (ch - gi) * CW);  // the group's first column
 #pragma unroll
-                for (int s2 = 0; s2 < T::Stores::n; ++s2) {
-                  if (s2 == 0 && xt.split3d)
-                    tma_store_3d(&P.tma_st[0], slot + xt.st_off[0], (int32_t)n0, r0, split);
-                  else
-                    tma_store_2d(&P.tma_st[s2], slot + xt.st_off[s2], (int32_t)n0, r0);
+                  for (int s2 = 0; s2 < T::Stores::n; ++s2) {
+                    const uint32_t b = st_base + xt.st_off[s2];
+                    const bool f32 = (s2 == 0 ? out0 : E.out[s2]).st == (uint8_t)SType::F32;
+                    if (s2 == 0 && xt.split3d) {
+                      tma_store_3d(&P.tma_st[0], b, c0, r0, split);
+                      tma_store_3d(&P.tma_st[0], b + 4096, c0 + 32, r0, split);
+                    } else {
+                      tma_store_2d(&P.tma_st[s2], b, c0, r0);
+                      if (f32) tma_store_2d(&P.tma_st[s2], b + 4096, c0 + 32, r0);
+                    }
+                  }
+                  bulk_commit();
                 }
-                bulk_commit();
               }
-              ++kc;
             }
           } else {
 #pragma unroll
@@ -1127,13 +1202,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           for (int s2 = 0; s2 < Pg.n_stores; ++s2)
             epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[Pg.store_slot[s2]]);
         }
+        DLVM_SECT(sect[4]);  // stores
 #pragma unroll
         for (int r = 0; r < NRS; ++r) {
           if (r >= nred) break;
           const int kind = red_kind(r);
           float x[CW];
+          if (tile_full) {  // interior tile: every row and column is in range
 #pragma unroll
-          for (int j = 0; j < CW; ++j) x[j] = (mval && j < ncol) ? v[red_slot(r)][j] : 0.f;
+            for (int j = 0; j < CW; ++j) x[j] = v[red_slot(r)][j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) x[j] = (mval && j < ncol) ? v[red_slot(r)][j] : 0.f;
+          }
           if (kind == RED_COL) {
             int col;
             const float cs = col_butterfly<CW>(x, lane, &col);
@@ -1146,6 +1227,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             for (int j = 0; j < CW; ++j) allacc[r] = __fadd_rn(allacc[r], x[j]);
           }
         }
+        DLVM_SECT(sect[5]);  // reductions
       }
       // this warp is done with the tile's staged inputs
       if (staged_in) {
@@ -1204,6 +1286,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     }
     if (tma_on && lane == 0) bulk_wait_all();  // this warp's TMA stores are complete
     if (ew == 0 && lane == 0) DLVM_GT(P, 6);
+#ifdef DLVM_GEMM_TRACE
+    // epilogue section cycles of warp 4 (DLVM_EPI_DBG & 8): slots 0..4 =
+    // reductions, TMEM loads, inputs, program, stores
+    if ((xt.dbg & 8) && ew == 0 && lane == 0 && P.trace) {
+      long long c_ = clock64();
+      (void)c_;
+      P.trace[(size_t)blockIdx.x * 8 + 0] = (unsigned long long)sect[5];
+      for (int k = 1; k < 5; ++k) P.trace[(size_t)blockIdx.x * 8 + k] = (unsigned long long)sect[k];
+    }
+#endif
   }
   tc_fence_before();
   __syncthreads();

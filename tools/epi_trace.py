@@ -46,7 +46,7 @@ def main():
         rt = rtypes[0] if len(rtypes) == 1 else "(" + ", ".join(rtypes) + ")"
         params = f"{A}, {B}" + (f", {V}" if "%v" in extra else "") + (f", {BL}" if "%m" in extra else "")
         text = f'module "e"\nstage raw\nfunc @f: ({params}) -> {rt} {{\n' + HEAD.replace("%EXTRA", extra) + body + "}\n"
-        f = P.Function(text, "f", None, dot_precision="bf16", flags=P.DLVM_NO_JIT)
+        f = P.Function(text, "f", None, dot_precision="bf16")
         ins = [a, b] + ([v] if "%v" in extra else []) + ([m] if "%m" in extra else [])
         outs = f.run(ins)
         outs = [o.to(torch.bfloat16) if (k < len(odt) and odt[k] == "bf16") else o for k, o in enumerate(outs)]
@@ -64,7 +64,12 @@ def main():
             t = buf.cpu().numpy().reshape(148, 8).astype(np.float64)
             live = t[t[:, 5] > 0]
             res.append(np.median(live[:, 6] - live[:, 5]) / 1e3)
-        print(f"{name:28s} epilogue {np.median(res):6.2f} us  (plan: {f.print(2).splitlines()[-1][:70]})", flush=True)
+            if int(os.environ.get("DLVM_EPI_DBG", "0")) & 8:  # section cycles of epilogue warp 4
+                sec = [int(np.median(live[:, k])) for k in range(5)]
+        extra = ""
+        if int(os.environ.get("DLVM_EPI_DBG", "0")) & 8:
+            extra = " cycles: red %d tmem %d in %d prog %d st %d" % tuple(sec)
+        print(f"{name:28s} epilogue {np.median(res):6.2f} us{extra}", flush=True)
 
 
 if __name__ == "__main__":

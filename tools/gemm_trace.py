@@ -29,7 +29,7 @@ def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
     w = W.c3() if cfg == "c3" else W.c4(8)
     dev = torch.device("cuda:0")
-    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16", flags=P.DLVM_NO_JIT)
+    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
     ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
     for i, a in enumerate(w.args):
         if a.name == "x" or a.name.startswith("w"):
