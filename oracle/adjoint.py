@@ -151,6 +151,16 @@ def _rules(G: _Gen, ins: Inst, g: Operand, y: Operand, ops: List[Operand], activ
         return out
     if op == "transpose":
         return [(0, E("transpose", [g]))]
+    if op == "reduce" and ins.attrs["op"] == "max":
+        # reading A26: g / (number of tied maxima) at every position equal to the max
+        a = ops[0]
+        keep = list(a.type.shape)
+        keep[ins.attrs["axis"]] = 1
+        yk = E("shapeCast", [y], {"shape": tuple(keep)})
+        at = E("eq", [a, yk])
+        cnt = E("reduce", [E("dataTypeCast", [at], {"dtype": a.type.dtype})], {"op": "add", "axis": ins.attrs["axis"]})
+        q = E("divide", [E("shapeCast", [g], {"shape": tuple(keep)}), E("shapeCast", [cnt], {"shape": tuple(keep)})])
+        return [(0, E("select", [at, q, _lit(0.0, _scalar(a.type))]))]
     if op == "reduce":
         if ins.attrs["op"] != "add":
             raise VerifyError(ins.line, ins.col, "'reduce by multiply' is not differentiable")

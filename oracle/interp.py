@@ -7,7 +7,8 @@ Op definitions (Table 1):
   lt/le/gt/ge/eq/ne                  pointwise -> bool
   select(c, a, b)                    where(c, a, b) after broadcasting
   dot(a, b)                          a @ b, rank 2
-  reduce(a, add|multiply, d)         sum / prod over axis d (axis removed, A2)
+  reduce(a, add|multiply|max, d)     sum / prod / max over axis d (axis removed, A2;
+                                     max: extension, reading A26)
   transpose(a)                       all axes reversed (A3)
   shapeCast(a, s)                    row-major reshape
   dataTypeCast(a, t)                 value conversion (floats stay float64)
@@ -107,7 +108,7 @@ def eval_inst(ins: Inst, args: List[np.ndarray], rt: TensorType, dot_policy=None
         else:
             r = args[0] @ args[1]
     elif op == "reduce":
-        f = np.sum if ins.attrs["op"] == "add" else np.prod
+        f = {"add": np.sum, "multiply": np.prod, "max": np.max}[ins.attrs["op"]]
         r = f(args[0], axis=ins.attrs["axis"])
     elif op == "transpose":
         r = np.transpose(args[0], tuple(reversed(range(args[0].ndim))))

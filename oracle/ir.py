@@ -316,7 +316,7 @@ class _Parser:
             ops = [self.operand()]
             self.expect("by")
             r = self.next()
-            if r.text not in ("add", "multiply"):
+            if r.text not in ("add", "multiply", "max"):  # max: extension (reading A26)
                 self.err(r, f"unknown reduction '{r.text}'")
             self.expect("along")
             attrs = {"op": r.text, "axis": self.int_()}

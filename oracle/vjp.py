@@ -84,9 +84,16 @@ def vjp_rule(ins: Inst, g: np.ndarray, y: np.ndarray, args: List[np.ndarray], do
     if op == "transpose":
         return [(0, np.transpose(g, tuple(reversed(range(g.ndim)))))]
     if op == "reduce":
+        d = ins.attrs["axis"]
+        if ins.attrs["op"] == "max":
+            # reading A26: the adjoint goes to the positions attaining the
+            # max, split equally among ties (each of k tied positions gets g/k)
+            x = args[0]
+            at = x == np.expand_dims(y, d)
+            k = at.sum(axis=d, keepdims=True)
+            return [(0, np.where(at, np.expand_dims(g, d) / k, 0.0))]
         if ins.attrs["op"] != "add":
             raise ValueError("'reduce by multiply' is not differentiable")
-        d = ins.attrs["axis"]
         return [(0, np.broadcast_to(np.expand_dims(g, d), args[0].shape))]
     if op == "shapeCast":
         return [(0, np.reshape(g, args[0].shape))]

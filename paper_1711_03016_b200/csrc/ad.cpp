@@ -290,6 +290,14 @@ Function differentiate(const Function& src, const GradConfig& cfg, const std::st
       case Op::Reduce: {  // broadcast g back along the reduced axis
         std::vector<int64_t> s = a.type.shape;
         s[in.axis] = 1;
+        if (in.reduce_max) {
+          // reading A26: g / k at the k positions equal to the max, else 0
+          Operand at = b.op2(Op::Eq, a, b.shape_cast(b.V(in.result), s));
+          Operand cnt = b.reduce_add(b.dtype_cast(at, a.type.dtype), in.axis);
+          Operand q = b.op2(Op::Divide, b.shape_cast(gr, s), b.shape_cast(cnt, s));
+          acc(a, b.select(at, q, Builder::L(0.0, Builder::scalar(a.type.dtype))));
+          break;
+        }
         Operand e = b.shape_cast(gr, s);
         acc(a, b.op2(Op::Multiply, e, Builder::L(1.0, a.type)));
         break;
@@ -387,7 +395,9 @@ std::string print_function(const Function& f) {
   for (auto& in : f.insts) {
     s += "    %" + f.names[in.result] + " = " + op_name(in.op) + " ";
     for (size_t k = 0; k < in.ops.size(); ++k) s += (k ? ", " : "") + opnd(f, in.ops[k]);
-    if (in.op == Op::Reduce) s += std::string(" by ") + (in.reduce_mul ? "multiply" : "add") + " along " + std::to_string(in.axis);
+    if (in.op == Op::Reduce)
+      s += std::string(" by ") + (in.reduce_mul ? "multiply" : in.reduce_max ? "max" : "add") + " along " +
+           std::to_string(in.axis);
     if (in.op == Op::ShapeCast) {
       s += " to ";
       for (size_t k = 0; k < in.shape.size(); ++k) s += (k ? " x " : "") + std::to_string(in.shape[k]);

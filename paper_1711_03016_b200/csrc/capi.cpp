@@ -97,7 +97,7 @@ void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
     for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
     d.nchunks = r.nchunks;
     d.chunk_stride = r.chunk_stride;
-    d.chunk_mul = r.chunk_mul ? 1 : 0;
+    d.chunk_op = r.chunk_op;
     d.st = st;
   }
   for (size_t i = 0; i < g.stores.size(); ++i) {

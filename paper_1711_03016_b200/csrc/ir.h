@@ -81,6 +81,7 @@ struct Inst {
   // attributes
   int axis = 0;               // reduce
   bool reduce_mul = false;    // reduce by multiply (else add)
+  bool reduce_max = false;    // reduce by max (extension, reading A26)
   std::vector<int64_t> shape; // shapeCast target
   DType cast_to = DType::F32; // dataTypeCast target
   int64_t from = 0, upto = 0; // slice

@@ -118,9 +118,15 @@ __device__ __forceinline__ void vm_load(const EwDevIn& in, int64_t off, int64_t 
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
       float s;
-      if (in.chunk_mul) {  // product over the reduced axis, in index order
+      if (in.chunk_op == 1) {  // product over the reduced axis, in index order
         s = 1.f;
         for (int k = 0; k < in.nchunks; ++k) s = __fmul_rn(s, ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st));
+      } else if (in.chunk_op == 2) {  // maximum over the reduced axis (a NaN wins, like numpy)
+        s = ld1(in.ptr, off + j * cs, in.st);
+        for (int k = 1; k < in.nchunks; ++k) {
+          const float x = ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st);
+          s = (x > s || x != x) ? x : s;
+        }
       } else {
         s = 0.f;
         for (int k = 0; k < in.nchunks; ++k) s = __fadd_rn(s, ld1(in.ptr, off + j * cs + k * in.chunk_stride, in.st));

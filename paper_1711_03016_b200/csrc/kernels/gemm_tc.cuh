@@ -180,7 +180,7 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
   int8_t kind[kMaxIn] = {0};
   for (int s2 = 1; s2 < Pg.n_in; ++s2) {
     const EwDevIn& in = E.in[s2];
-    if (in.nchunks != 1 || in.chunk_mul) continue;
+    if (in.nchunks != 1 || in.chunk_op) continue;
     const int es = es_of(in.st);
     if (in.s[1] == 1 && in.s[0] != 0 && nmap < kEpiTmaIn && BN % (128 / es) == 0 &&
         encode_epi(&tp->tma_in[nmap], in.ptr, in.st, p.N, p.M, in.s[0] * es, 128 / es, BM)) {

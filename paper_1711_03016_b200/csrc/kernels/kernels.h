@@ -11,14 +11,15 @@ namespace dlvm {
 
 // one program input: element (i_0..i_{n-1}) at ptr + sum_d i_d * s[d]
 // (+ k * chunk_stride summed over k < nchunks for reduction partials;
-// multiplied in k order instead when chunk_mul: `reduce ... by multiply`)
+// multiplied in k order instead when chunk_op == 1: `reduce ... by multiply`;
+// their maximum when chunk_op == 2: `reduce ... by max`, reading A26)
 struct EwDevIn {
   const void* ptr;
   int64_t s[kMaxIterDims];
   int64_t chunk_stride;
   int32_t nchunks;
   uint8_t st;  // SType
-  uint8_t chunk_mul;
+  uint8_t chunk_op;
 };
 
 struct EwDevOut {

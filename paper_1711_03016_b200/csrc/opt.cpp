@@ -158,9 +158,9 @@ struct Optimizer {
           }
           break;
         case Op::Reduce:
-          if (in.ops[0].is_lit()) {  // sum / product of n copies
+          if (in.ops[0].is_lit()) {  // sum / product / max of n copies
             const int64_t n = in.ops[0].type.shape[in.axis];
-            double x = in.reduce_mul ? 1.0 : in.ops[0].lit * (double)n;
+            double x = in.reduce_mul ? 1.0 : in.reduce_max ? in.ops[0].lit : in.ops[0].lit * (double)n;
             if (in.reduce_mul)
               for (int64_t k = 0; k < n; ++k) x *= in.ops[0].lit;
             rauw(r, L(x, rt));
@@ -199,7 +199,7 @@ struct Optimizer {
       else
         k << "|v" << o.value;
     }
-    k << "|a" << in.axis << (in.reduce_mul ? "m" : "a") << "|c" << (int)in.cast_to << "|f" << in.from << ":" << in.upto
+    k << "|a" << in.axis << (in.reduce_mul ? "m" : in.reduce_max ? "x" : "a") << "|c" << (int)in.cast_to << "|f" << in.from << ":" << in.upto
       << "|s";
     for (auto s : in.shape) k << s << ",";
     return k.str();

@@ -270,8 +270,9 @@ struct Parser {
       in.ops.push_back(operand());
       expect("by");
       const Token& r = next();
-      if (r.text != "add" && r.text != "multiply") fail(r, "unknown reduction '" + r.text + "'");
+      if (r.text != "add" && r.text != "multiply" && r.text != "max") fail(r, "unknown reduction '" + r.text + "'");
       in.reduce_mul = r.text == "multiply";
+      in.reduce_max = r.text == "max";  // extension (reading A26)
       expect("along");
       in.axis = (int)integer();
     } else if (op == Op::ShapeCast) {

@@ -78,7 +78,7 @@ void print_group(std::ostringstream& o, const EwGroup& g) {
     o << "    " << what << k << ": buf " << r.buf << " +" << r.offset << " strides [";
     for (int d = 0; d < g.ndims; ++d) o << (d ? "," : "") << r.strides[d];
     o << "] st " << (int)r.st;
-    if (r.nchunks != 1) o << " chunks " << r.nchunks << "x" << r.chunk_stride << (r.chunk_mul ? " (product)" : "");
+    if (r.nchunks != 1) o << " chunks " << r.nchunks << "x" << r.chunk_stride << (r.chunk_op == 1 ? " (product)" : r.chunk_op == 2 ? " (max)" : "");
     if (r.direct_buf >= 0) o << " direct buf " << r.direct_buf;
     o << "\n";
   };
@@ -224,7 +224,8 @@ struct Planner {
     return in && (in->op == Op::Transpose || in->op == Op::ShapeCast || in->op == Op::Slice);
   }
   static bool is_dotlike(Op op) { return op == Op::Dot || op == Op::DotSum; }
-  static bool is_prod(const Inst* in) { return in && in->op == Op::Reduce && in->reduce_mul; }
+  // reductions by multiply or max: one element-wise step of their own (emit_prod)
+  static bool is_prod(const Inst* in) { return in && in->op == Op::Reduce && (in->reduce_mul || in->reduce_max); }
   static bool is_ew(const Inst* in) {
     return in && (is_elementwise(in->op) || in->op == Op::Sech2 || in->op == Op::DataTypeCast);
   }
@@ -364,7 +365,7 @@ struct Planner {
     for (auto& in : f.insts) {
       if (in.op != Op::Reduce) continue;
       if (in.ops[0].is_lit()) unsupported("reduce of a literal");
-      if (in.reduce_mul) continue;  // its own step (emit_prod), never chained into a sum
+      if (in.reduce_mul || in.reduce_max) continue;  // its own step (emit_prod), never chained into a sum
       int x = in.ops[0].value;
       auto it = red_root.find(x);
       if (it != red_root.end() && vi[x].users.size() == 1 && vi[x].outs.empty()) {
@@ -1656,7 +1657,8 @@ struct Planner {
   // `reduce %x by multiply along a` (Table 1; forward only):
   // an element-wise step over the result's index space whose one input walks
   // the reduced axis as nchunks = shape[a] chunks at the axis stride,
-  // multiplied in index order by the load (chunk_mul), then stored to every
+  // multiplied in index order by the load (chunk_op 1; `by max`: chunk_op 2,
+  // the maximum, reading A26), then stored to every
   // home of the result.  Its consumers read those homes.
   void emit_prod(Node& n) {
     const Inst& in = f.insts[n.dot_inst];
@@ -1673,7 +1675,7 @@ struct Planner {
     it.st = r.st;
     it.nchunks = (int)r.shape[in.axis];
     it.chunk_stride = r.strides[in.axis];
-    it.chunk_mul = true;
+    it.chunk_op = in.reduce_max ? 2 : 1;
     for (int d = 0, j = 0; d < rx; ++d)
       if (d != in.axis) it.strides[j++] = r.strides[d];
     g.inputs.push_back(it);
@@ -1696,8 +1698,8 @@ struct Planner {
     std::ostringstream d;
     d << "ew [";
     for (int k = 0; k < g.ndims; ++k) d << (k ? "," : "") << g.dims[k];
-    d << "] vec" << g.vec << " product of %" << f.names[x] << " along " << in.axis << " (" << it.nchunks
-      << " factors) -> %" << f.names[v];
+    d << "] vec" << g.vec << (in.reduce_max ? " max of %" : " product of %") << f.names[x] << " along " << in.axis
+      << " (" << it.nchunks << (in.reduce_max ? " values" : " factors") << ") -> %" << f.names[v];
     s.desc = d.str();
     g.desc = s.desc;
     plan.steps.push_back(s);

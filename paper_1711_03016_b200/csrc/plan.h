@@ -59,7 +59,7 @@ struct IterRef {
   int64_t strides[kPlanDims] = {0, 0, 0, 0, 0, 0, 0, 0};  // per iteration dim
   int nchunks = 1;
   int64_t chunk_stride = 0;
-  bool chunk_mul = false;        // chunks multiplied in order (`reduce ... by multiply`), else summed
+  uint8_t chunk_op = 0;          // chunks summed (0), multiplied in order (1, `reduce ... by multiply`) or maxed (2, `by max`)
   SType st = SType::F32;
   // reductions with a single partial: the value's f32 home, which the
   // producer writes directly when that buffer is bound as f32 at run time

@@ -592,3 +592,24 @@ def test_device_option_validated():
     h = ctypes.c_void_p()
     b = W.FIG3.encode()
     assert P.dlvm.lib().dlvm_fn_create(b, len(b), b"foo", None, ctypes.byref(o), ctypes.byref(h)) == 3
+
+
+def test_reduce_max_and_softmax_ce_through_cpp_ad():
+    """`reduce ... by max` (reading A26) through the C++ front end: types,
+    the generated adjoint (ties split equally) interpreted by the oracle in
+    f64 == the oracle's reverse sweep, on a softmax-CE MLP and on a program
+    with exact ties; the planner gives each max its own element-wise step."""
+    w = W.ce_mlp(6, layers=[(7, 5, "relu"), (5, 4, None)], dot_precision="f32")
+    ins = [x.astype(np.float64) for x in w.inputs()]
+    f = _ad_cross_check(w.text, w.fn, w.grad, ins, np.float64(w.seed()))
+    assert " by max along 1" in f.print(0)
+    assert "max of %" in f.print(3), f.print(3)
+    T = "<3 x 4 x f32>"
+    t = (f'module "m"\nstage raw\nfunc @f: ({T}) -> <3 x f32> {{\n\'entry(%a: {T}):\n'
+         f"    %s = multiply %a: {T}, %a: {T}\n    %r = reduce %s: {T} by max along 1\n"
+         f"    return %r: <3 x f32>\n}}\n\n[gradient @f wrt 0 seedable]\nfunc @g: ({T}, <3 x f32>) -> {T}\n")
+    a = np.array([[1.0, -1.0, 0.5, 0.0], [2.0, 2.0, -2.0, 1.0], [0.0, 0.0, 0.0, 0.0]])
+    _ad_cross_check(t, "f", "g", [a], np.array([1.0, 3.0, 4.0]))
+    with pytest.raises(P.DlvmError) as e:
+        P.Function(t.replace("by max", "by min"), "f", "g", flags=P.DLVM_PLAN_ONLY)
+    assert e.value.status == 2

@@ -1362,3 +1362,40 @@ def test_merged_finalize_outputs_bound_as_bf16():
         got = o.cpu().to(torch.float32).numpy()
         want = bf16_round(r) if k in bf else r
         assert np.array_equal(got.reshape(-1).view(np.uint32), np.asarray(want, np.float32).reshape(-1).view(np.uint32)), k
+
+
+def test_softmax_ce_mlp_f32():
+    """Softmax cross-entropy MLP (`reduce ... by max`,
+    reading A26) under the fp32 dot policy, ragged shapes: loss and every
+    gradient against the oracle (A16/A17 bounds from the oracle's adjoint)."""
+    w = W.ce_mlp(37, layers=[(70, 52, "tanh"), (52, 13, None)], dot_precision="f32")
+    _check_f32(w, w.inputs(), w.seed())
+
+
+def test_softmax_ce_mlp_bf16():
+    """The same loss on tcgen05 GEMMs (bf16 policy): normwise 2e-2 against the
+    oracle under the same operand rounding (A18'), and the loss and
+    last-layer gradients against the unrounded oracle."""
+    w = W.ce_mlp(256, layers=[(256, 256, "relu"), (256, 100, None)])
+    _check_c3(w)
+
+
+def test_reduce_max_ties_bit_exact():
+    """Exact ties (dyadic data): the adjoint splits the seed equally among the
+    tied maxima, bit for bit as the oracle (values and counts are exact)."""
+    T = "<64 x 40 x f32>"
+    text = (f'module "m"\nstage raw\nfunc @f: ({T}) -> <64 x f32> {{\n\'entry(%a: {T}):\n'
+            f"    %r = reduce %a: {T} by max along 1\n    return %r: <64 x f32>\n}}\n\n"
+            f"[gradient @f wrt 0 seedable]\nfunc @g: ({T}, <64 x f32>) -> {T}\n")
+    rng = np.random.default_rng(31)
+    a = rng.integers(-3, 4, size=(64, 40)).astype(np.float32)  # many ties
+    seed = rng.choice([0.5, 1.0, 2.0, -4.0], size=64).astype(np.float32)
+    res = gpu_run(text, "f", "g", [a], seed=seed)
+    m = oracle.parse(text)
+    np.testing.assert_array_equal(res["primal"][0], oracle.run(m, "f", [a.astype(np.float64)])[0])
+    ref = oracle.run(m, "g", [a.astype(np.float64), seed.astype(np.float64)])[0]
+    # g / k with k in 1..40: exact only when k is a power of two; otherwise one rounding
+    assert_f32_parity(res["grad"][0], ref, what="max ties grad")
+    k = (a == a.max(axis=1, keepdims=True)).sum(axis=1)
+    pow2 = (k & (k - 1)) == 0
+    np.testing.assert_array_equal(res["grad"][0][pow2], ref[pow2])

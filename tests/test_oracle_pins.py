@@ -605,3 +605,82 @@ def test_F14_fd_dataTypeCast_f32_to_f64():
     src = oracle.parse(text).functions["f"]
     (g,) = oracle.grad(src, [a], wrt=[0])
     np.testing.assert_allclose(g, 2 * np.tanh(a) * (1 - np.tanh(a) ** 2), rtol=1e-14)
+
+
+# --- `reduce ... by max` (extension, reading A26) and softmax cross-entropy --
+
+def _max_module(shape, axis, grad=True):
+    rt = [d for k, d in enumerate(shape) if k != axis]
+    T = lambda s: "<" + " x ".join(str(d) for d in s) + " x f32>" if s else "f32"
+    text = (f'module "m"\nstage raw\nfunc @f: ({T(shape)}) -> {T(rt)} {{\n'
+            f"'entry(%a: {T(shape)}):\n    %r = reduce %a: {T(shape)} by max along {axis}\n"
+            f"    return %r: {T(rt)}\n}}\n")
+    if grad:
+        text += f"\n[gradient @f wrt 0 seedable]\nfunc @g: ({T(shape)}, {T(rt)}) -> {T(shape)}\n"
+    return oracle.parse(text)
+
+
+def test_reduce_max_forward_pins():
+    """max over the axis, axis removed: hand values and brute force."""
+    a = np.array([[1.0, -2.0, 3.0], [4.0, 5.0, -6.0]])
+    np.testing.assert_array_equal(oracle.run(_max_module((2, 3), 0), "f", [a])[0], [4.0, 5.0, 3.0])
+    np.testing.assert_array_equal(oracle.run(_max_module((2, 3), 1), "f", [a])[0], [3.0, 5.0])
+    assert float(oracle.run(_max_module((4,), 0), "f", [np.array([-1.5, -2.0, -0.5, -4.0])])[0]) == -0.5
+    x = np.random.default_rng(17).uniform(-1, 1, (3, 4, 5))
+    for ax in range(3):
+        got = oracle.run(_max_module(x.shape, ax), "f", [x])[0]
+        rest = [d for k, d in enumerate(x.shape) if k != ax]
+        for idx in itertools.product(*[range(d) for d in rest]):
+            best = -np.inf
+            for t in range(x.shape[ax]):
+                full = list(idx)
+                full.insert(ax, t)
+                best = x[tuple(full)] if x[tuple(full)] > best else best
+            assert got[idx] == best
+
+
+def test_reduce_max_adjoint_ties_split_and_fd():
+    """Reading A26: the incoming adjoint goes to the position(s) attaining
+    the max, split equally among ties; away from ties it is the derivative
+    (central differences)."""
+    m = _max_module((2, 3), 1)
+    a = np.array([[1.0, 3.0, 3.0], [2.0, 0.0, -1.0]])
+    (g,) = oracle.run(m, "g", [a, np.array([1.0, 4.0])])
+    np.testing.assert_array_equal(g, [[0.0, 0.5, 0.5], [4.0, 0.0, 0.0]])
+    (g2,) = oracle.run(_max_module((2, 3), 0), "g", [a, np.array([1.0, 2.0, 3.0])])
+    np.testing.assert_array_equal(g2, [[0.0, 2.0, 3.0], [1.0, 0.0, 0.0]])
+    x = np.random.default_rng(19).uniform(-1, 1, (4, 5))
+    for ax in (0, 1):
+        mm = _max_module((4, 5), ax)
+        seed = np.random.default_rng(23).uniform(-1, 1, mm.functions["f"].result_types[0].shape)
+        (gx,) = oracle.run(mm, "g", [x, seed])
+        np.testing.assert_allclose(gx, oracle.fd_grad(mm.functions["f"], [x], 0, seed=seed), rtol=1e-5, atol=1e-8)
+        # the IR adjoint (oracle.canonical) equals the value-level sweep, ties included
+        from oracle.interp import run_function
+        xt = x.copy()
+        xt[1] = xt[0] if ax == 0 else xt[1]
+        xt[:, 2] = xt[:, 3] if ax == 1 else xt[:, 2]
+        for inp in (x, xt):
+            np.testing.assert_allclose(run_function(oracle.canonical(mm, "g"), [inp, seed])[0],
+                                       oracle.run(mm, "g", [inp, seed])[0], rtol=1e-15, atol=0)
+
+
+def test_softmax_cross_entropy_gradient_closed_form():
+    """softmax-CE built from primitives with the max shift (workloads.mlp_ir
+    loss="ce"): L = sum_b (logsumexp(y_b) - y_b . t_b) and dL/dy = softmax(y)
+    - t, so for a linear last layer y = h.W + b: dW = h^T (softmax(y) - t),
+    db = sum_b (softmax(y) - t) -- checked against the closed form."""
+    w = W.ce_mlp(5, layers=[(6, 4, None)], dot_precision="f32")
+    m = oracle.parse(w.text)
+    x, W1, b1, t = [a.astype(np.float64) for a in w.inputs()]
+    y = x @ W1 + b1
+    e = np.exp(y - y.max(axis=1, keepdims=True))
+    p = e / e.sum(axis=1, keepdims=True)
+    L_ref = float(np.sum(np.log(np.exp(y).sum(axis=1)) - (y * t).sum(axis=1)))
+    assert abs(float(oracle.run(m, "mlp", [x, W1, b1, t])[0]) - L_ref) <= 1e-12 * abs(L_ref)
+    dW, db, L = oracle.run(m, "mlp_grad", [x, W1, b1, t, np.float64(1.0)])
+    np.testing.assert_allclose(dW, x.T @ (p - t), rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(db, (p - t).sum(axis=0, keepdims=True), rtol=1e-12, atol=1e-14)
+    # large logits: the max shift keeps the forward finite where exp(y) overflows
+    big = [x * 300.0, W1, b1, t]
+    assert np.isfinite(oracle.run(m, "mlp", big)[0])

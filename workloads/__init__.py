@@ -149,10 +149,13 @@ def _act_lines(act: Optional[str], l: int, a: str, shape) -> Tuple[List[str], st
 
 
 def mlp_ir(batch: int, layers: Sequence[Tuple[int, int, Optional[str]]],
-           module: str = "mlp", with_grad: bool = True) -> str:
+           module: str = "mlp", with_grad: bool = True, loss: str = "mse") -> str:
     """Straight-line MLP `@mlp(x, W1, b1, ..., WL, bL, t) -> f32` with MSE
     loss 0.5 * sum((y - t)^2) (reading A9) and the declaration
-    `[gradient @mlp wrt 1..2L keeping 0 seedable]` (Appendix A of SURVEY)."""
+    `[gradient @mlp wrt 1..2L keeping 0 seedable]` (Appendix A of SURVEY).
+    loss="ce": softmax cross-entropy sum_b (logsumexp(y_b) - y_b . t_b),
+    the log-sum-exp shifted by the row max (`reduce ... by max`, reading
+    A26) and built from the paper's primitives otherwise."""
     L = len(layers)
     params = [(f"x", (batch, layers[0][0]))]
     for l, (i, o, _) in enumerate(layers, 1):
@@ -170,12 +173,27 @@ def mlp_ir(batch: int, layers: Sequence[Tuple[int, int, Optional[str]]],
         more, h = _act_lines(act, l, f"a{l}", (batch, o))
         lines += more
     Y = _ty((batch, out_dim))
-    lines += [f"    %r = subtract %{h}: {Y}, %t: {Y}",
-              f"    %s = multiply %r: {Y}, %r: {Y}",
-              f"    %q = reduce %s: {Y} by add along 1",
-              f"    %l = reduce %q: {_ty((batch,))} by add along 0",
-              f"    %L = multiply %l: f32, 0.5: f32",
-              "    return %L: f32", "}"]
+    B1 = _ty((batch,))
+    if loss == "ce":
+        lines += [f"    %mx = reduce %{h}: {Y} by max along 1",
+                  f"    %mk = shapeCast %mx: {B1} to {batch} x 1",
+                  f"    %zs = subtract %{h}: {Y}, %mk: {_ty((batch, 1))}",
+                  f"    %ex = exp %zs: {Y}",
+                  f"    %se = reduce %ex: {Y} by add along 1",
+                  f"    %ls = log %se: {B1}",
+                  f"    %lse = add %ls: {B1}, %mx: {B1}",
+                  f"    %zt = multiply %{h}: {Y}, %t: {Y}",
+                  f"    %zy = reduce %zt: {Y} by add along 1",
+                  f"    %nl = subtract %lse: {B1}, %zy: {B1}",
+                  f"    %L = reduce %nl: {B1} by add along 0",
+                  "    return %L: f32", "}"]
+    else:
+        lines += [f"    %r = subtract %{h}: {Y}, %t: {Y}",
+                  f"    %s = multiply %r: {Y}, %r: {Y}",
+                  f"    %q = reduce %s: {Y} by add along 1",
+                  f"    %l = reduce %q: {B1} by add along 0",
+                  f"    %L = multiply %l: f32, 0.5: f32",
+                  "    return %L: f32", "}"]
     if with_grad:
         wrt = ", ".join(str(k) for k in range(1, 2 * L + 1))
         grads = []
@@ -207,13 +225,13 @@ def chain_ir(R: int, C: int, module: str = "chain") -> str:
 
 
 def _mlp_workload(cfg: int, name: str, batch: int, layers, x_dist, t_dist, seed_value,
-                  dot_precision: str, global_batch: int) -> Workload:
+                  dot_precision: str, global_batch: int, loss: str = "mse") -> Workload:
     args = [ArgSpec("x", (batch, layers[0][0]), x_dist, batched=True)]
     for l, (i, o, _) in enumerate(layers, 1):
         args.append(ArgSpec(f"w{l}", (i, o), ("glorot", i, o)))
         args.append(ArgSpec(f"b{l}", (1, o), ("uniform", -0.1, 0.1)))
     args.append(ArgSpec("t", (batch, layers[-1][1]), t_dist, batched=True))
-    return Workload(cfg, name, mlp_ir(batch, layers, module=name), "mlp", "mlp_grad", args,
+    return Workload(cfg, name, mlp_ir(batch, layers, module=name, loss=loss), "mlp", "mlp_grad", args,
                     seed_value=seed_value, dot_precision=dot_precision, batch=batch,
                     global_batch=global_batch, layers=list(layers))
 
@@ -242,6 +260,15 @@ def c3(batch: int = 1024, global_batch: Optional[int] = None, cfg: int = 3,
     gb = batch if global_batch is None else global_batch
     return _mlp_workload(cfg, "c3_mlp" if cfg == 3 else "c4_mlp", batch, layers or C3_LAYERS,
                          ("normal",), ("onehot",), 1.0 / gb, "bf16", gb)
+
+
+def ce_mlp(batch: int = 1024, layers=None, global_batch: Optional[int] = None,
+           dot_precision: str = "bf16") -> Workload:
+    """The c3 MLP shape with the softmax cross-entropy loss (SURVEY §8(f)
+    rank 4): one-hot targets, seed 1/B (mean over the batch)."""
+    gb = batch if global_batch is None else global_batch
+    return _mlp_workload(8, "ce_mlp", batch, layers or C3_LAYERS, ("normal",), ("onehot",), 1.0 / gb,
+                         dot_precision, gb, loss="ce")
 
 
 def c4(n_ranks: int = 1, global_batch: int = 65536) -> Workload:
