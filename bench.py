@@ -202,9 +202,26 @@ def kernel_breakdown(f, which, step, K, dev):
         ks = [e for e in prof.profiler.kineto_results.events()
               if e.device_type() == DeviceType.CUDA and any(k in e.name() for k in OWN_KERNELS)]
         ks.sort(key=lambda e: e.start_ns())
-        ks = ks[-K * n:] if len(ks) >= K * n else ks  # the K steps end the session
-        if len(ks) != K * n:
-            raise RuntimeError(f"CUPTI saw {len(ks)} library kernels, plan has {K} x {n}")
+        # match the plan's launches to the recorded kernels by kind, walking
+        # back from the last step (a kernel the plan does not count -- e.g.
+        # a conditional finalize -- is skipped instead of shifting the rest)
+        want = [kernel_kind(f.launch_info(which, i)[0]) for i in range(n)]
+        optional = ["skipped when" in f.launch_info(which, i)[0] for i in range(n)]
+        picked, j = [], len(ks) - 1
+        for _ in range(K):
+            step_k = []
+            for i in reversed(range(n)):
+                if optional[i] and (j < 0 or not any(frag in ks[j].name() for frag in want[i])):
+                    step_k.append(None)  # e.g. a cast skipped because the input came as bf16
+                    continue
+                while j >= 0 and not any(frag in ks[j].name() for frag in want[i]):
+                    j -= 1
+                if j < 0:
+                    raise RuntimeError(f"CUPTI kernels do not match the plan (launch {i}: {want[i]})")
+                step_k.append(ks[j])
+                j -= 1
+            picked = list(reversed(step_k)) + picked
+        ks = picked
         if len(ks) == K * n:
             dur = [[0.0] * K for _ in range(n)]
             exc = [[0.0] * K for _ in range(n)]
@@ -212,6 +229,9 @@ def kernel_breakdown(f, which, step, K, dev):
             last_end = None
             for j, e in enumerate(ks):
                 k, i = divmod(j, n)
+                if e is None:
+                    names[i] = "(not launched)"
+                    continue
                 s0, e0 = e.start_ns(), e.start_ns() + e.duration_ns()
                 dur[i][k] = e.duration_ns() * 1e-6
                 exc[i][k] = max(0, e0 - (s0 if last_end is None else max(s0, last_end))) * 1e-6
@@ -244,6 +264,21 @@ def kernel_breakdown(f, which, step, K, dev):
         out.append({"desc": desc, "ms": ms, "excl_ms": ms, "flops": flops, "bytes": nbytes, "timing": "events",
                     "cupti_failed": why})
     return out
+
+
+def kernel_kind(desc):
+    """Kernel-name fragments a plan launch with this description runs as."""
+    if desc.startswith("gemm tcgen05"):
+        return ("gemm_tc_kernel",)
+    if desc.startswith("gemm simt"):
+        return ("gemm_simt_kernel",)
+    if desc.startswith("finalize"):
+        return ("finalize_kernel",)
+    if desc.startswith("pack"):
+        return ("pack_bf16_kernel",)
+    if desc.startswith("cast"):
+        return ("cast_bf16_kernel",)
+    return ("ew2d_kernel", "ew_kernel", "ew_tma_kernel")
 
 
 # kernel-name fragments of this library's kernels (ahead-of-time and NVRTC)
