@@ -77,8 +77,8 @@ bool encode(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int
 constexpr int kMaxDynSmem = 227 * 1024;
 __host__ __device__ constexpr int stage_bytes(int bn, int ctas) { return A_STAGE_BYTES + (bn / ctas) * BK * 2; }
 // bytes after the stages: barriers (256) + the epilogue reduction scratch
-__host__ __device__ constexpr int tail_bytes(int bn) {
-  return 256 + (kEpiReds * 4 * bn + kEpiReds * 2 * BM + kEpiReds * 8) * 4;
+__host__ __device__ constexpr int tail_bytes(int bn, int nred = kEpiReds) {
+  return 256 + (nred * 4 * bn + nred * 2 * BM + nred * 8) * 4;
 }
 constexpr int round_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -199,7 +199,7 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
       in_bytes += BN * 4;
     }
   }
-  const int stage = stage_bytes(BN, ctas), tail = tail_bytes(BN);
+  const int stage = stage_bytes(BN, ctas), tail = tail_bytes(BN, Pg.n_reduces);  // compile-time programs: NRS
   const int nst_max = num_stages_rt(ctas), nst_min = ctas == 2 ? 4 : 3;
   auto total = [&](int nst, int nbufs, int ibytes) {
     return 1024 + round_up(nst * stage + tail, 1024) + nbufs * round_up(ibytes, 1024) + 8 * et.st_slot_bytes;

@@ -753,9 +753,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const uint32_t full_bar = sBar, empty_bar = sBar + 48, tfull_bar = sBar + 96, tempty_bar = sBar + 112,
                  in_full_bar = sBar + 128, in_empty_bar = sBar + 144;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 192);
-  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 256);  // [kEpiReds][4][BN]
-  float* rowred = colred + kEpiReds * 4 * BN;                                          // [kEpiReds][2][BM]
-  float* allred = rowred + kEpiReds * 2 * BM;                                          // [kEpiReds][8]
+  // reduction scratch sized by the program's reduction count (NRS; the
+  // interpreter reserves kEpiReds), so programs without reductions leave
+  // that space to the pipeline / TMA epilogue (host: tail_bytes)
+  float* colred = reinterpret_cast<float*>(gbase + (sBar - base) + 256);  // [NRS][4][BN]
+  float* rowred = colred + NRS * 4 * BN;                                               // [NRS][2][BM]
+  float* allred = rowred + NRS * 2 * BM;                                               // [NRS][8]
 
   const GemmParams& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
