@@ -484,7 +484,7 @@ def compact_line(out):
     line = _pick(out, ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                        "scaling", "vs_baseline", "dtype", "data", "config", "step_tflops", "gpu_launches", "clocks"])
     line["config"] = _pick(out["config"], ["workload", "global_batch", "per_rank_batch", "parallelism", "l2",
-                                           "cuda_graph", "step"])
+                                           "cuda_graph", "step", "gradient_reduction"])
     r = out.get("roofline")
     if r:
         line["roofline"] = _pick(r, ["bound", "achieved", "peak", "unit", "frac", "traffic", "kernel_ms", "timing",
@@ -545,6 +545,9 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the c3 leg (BASELINE config 3, batch 1024)")
     ap.add_argument("--cpu-rows", type=int, default=None)
     ap.add_argument("--detail", default=None, help="write per-kernel detail JSON here")
+    ap.add_argument("--dp", default="nccl", choices=["nccl", "fused"],
+                    help="gradient reduction: bucketed NCCL all-reduce, or fused into the gradient kernels "
+                         "(DLVM_F32_ADD into the owners' symmetric memory, dp.FusedReduceStep)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: on for the launch-bound c1)")
     args = ap.parse_args()
@@ -605,15 +608,25 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.dp == "fused":
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
     pk = peaks()
     w = make_workload()
     f, dev_in, seed, host, n_grads = mlp_setup(w, dev, rank)
-    dps = DataParallelStep(f, n_grads, dev, world_size=world)
-    for e in dps.events:
-        e.record()
+    if args.dp == "fused":
+        from paper_1711_03016_b200.dp import FusedReduceStep
+        dps = FusedReduceStep(f, n_grads, dev)
+        dps.grads = type("G", (), {"views": dps.views})()
+    else:
+        dps = DataParallelStep(f, n_grads, dev, world_size=world)
+        for e in dps.events:
+            e.record()
     train_step = lambda inp: dps.step(inp, seed)
     step = lambda: train_step(dev_in)
     sgd_info = None
@@ -755,6 +768,8 @@ def main():
                       "layers": [list(l) for l in w.layers], "parallelism": f"dp{world}",
                       "dot_precision": "bf16 operands, fp32 accumulate (tcgen05)" if w.dot_precision == "bf16"
                       else "fp32 operands, FFMA (SIMT)",
+                      "gradient_reduction": "fused into the gradient kernels (DLVM_F32_ADD into owners' peer memory)"
+                      if args.dp == "fused" else "bucketed NCCL all-reduce on a comm stream",
                       "l2": ("inputs larger than L2 (x is %d MiB per rank)" % (w.batch * w.layers[0][0] * 2 >> 20))
                       if w.cfg != 1 else "L2-resident (whole c1 working set < 1 MiB; latency-bound config)",
                       "cuda_graph": use_graph},
@@ -802,7 +817,7 @@ def main():
         if dp_:
             line["detail_file"] = os.path.relpath(dp_, ROOT)
         print(json.dumps(line))
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -56,7 +56,17 @@ typedef enum {
  * where the byte is nonzero, else 0.0 (exact for 0/1 data such as one-hot
  * targets or masks).  An f32 output may be requested as bf16 (stored with
  * round-to-nearest-even). */
-typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3 } dlvm_dtype;
+typedef enum { DLVM_BOOL = 0, DLVM_F32 = 1, DLVM_F64 = 2, DLVM_BF16 = 3, DLVM_F32_ADD = 4 } dlvm_dtype;
+/* DLVM_F32_ADD (outputs only): an f32 output the kernels ACCUMULATE into
+ * with red.global.add instead of storing -- the fused gradient reduction of
+ * the data-parallel path: `data` may be a peer
+ * GPU's memory reachable over NVLink (P2P / symmetric memory), so every
+ * rank adds its partial gradient straight into the owner's buffer from the
+ * GEMM epilogue (or the element-wise step that finalises it).  The caller
+ * zeroes the buffer first and orders every contributor's run before reading
+ * it.  Floating-point addition order across concurrent contributors is not
+ * fixed (two contributors into a zeroed buffer are order-independent).
+ * Rejected (DLVM_ERR_USAGE) for outputs a later launch reads back. */
 
 #define DLVM_MAX_RANK 8
 typedef struct {

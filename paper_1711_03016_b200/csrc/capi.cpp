@@ -38,12 +38,34 @@ struct dlvm_fn_s {
   std::vector<void*> launch_events[2];
   bool specialize = true;
   std::vector<void*> jit_fn[2];  // per plan step: create-time specialised kernel (CUfunction) or null
+  std::vector<char> out_read[2]; // per output: some launch reads it back (it cannot be bound as DLVM_F32_ADD)
   std::string jit_report;        // print mode 8
 };
 
 namespace {
 
 thread_local std::string g_last_error;
+
+// outputs whose buffer a later launch of the plan reads (e.g. a kept value
+// feeding more work): their final value must be stored, not accumulated
+std::vector<char> outputs_read(const Plan& P) {
+  std::vector<char> read(P.n_outputs, 0);
+  auto mark = [&](int buf) {
+    if (buf >= 0 && buf < (int)P.bufs.size() && P.bufs[buf].kind == BufferSlot::Output) read[P.bufs[buf].index] = 1;
+  };
+  for (const Step& st : P.steps) {
+    if (st.kind == Step::EW) {
+      for (auto& r : st.ew.inputs) mark(r.buf);
+    } else if (st.kind == Step::GEMM) {
+      for (auto& sg : st.gemm.seg) {
+        mark(sg.a.buf);
+        mark(sg.b.buf);
+      }
+      for (auto& r : st.gemm.epi.inputs) mark(r.buf);
+    }
+  }
+  return read;
+}
 
 dlvm_status fail(dlvm_status st, const std::string& msg) {
   g_last_error = msg;
@@ -70,7 +92,9 @@ bool shape_matches(const dlvm_tensor& t, const Type& ty) {
   return true;
 }
 
-SType stype_of(int32_t dt) { return dt == DLVM_BF16 ? SType::BF16 : dt == DLVM_BOOL ? SType::U8 : SType::F32; }
+SType stype_of(int32_t dt) {
+  return dt == DLVM_BF16 ? SType::BF16 : dt == DLVM_BOOL ? SType::U8 : dt == DLVM_F32_ADD ? SType::F32_ADD : SType::F32;
+}
 
 struct Bound {
   std::vector<void*> ptr;     // per BufferSlot
@@ -92,7 +116,7 @@ void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
     EwDevIn& d = p->in[i];
     if (r.buf < 0) continue;  // accumulator
     const uint8_t st = b.st[r.buf];
-    size_t esz = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+    size_t esz = (size_t)st_bytes(st);
     d.ptr = static_cast<const char*>(b.ptr[r.buf]) + r.offset * esz;
     for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
     d.nchunks = r.nchunks;
@@ -104,7 +128,7 @@ void to_dev(const EwGroup& g, const Bound& b, EwParams* p) {
     const IterRef& r = g.stores[i];
     EwDevOut& d = p->out[i];
     const uint8_t st = b.st[r.buf];
-    size_t esz = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+    size_t esz = (size_t)st_bytes(st);
     d.ptr = static_cast<char*>(b.ptr[r.buf]) + r.offset * esz;
     for (int k = 0; k < kMaxIterDims; ++k) d.s[k] = r.strides[k];
     d.st = st;
@@ -190,8 +214,11 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
   for (int i = 0; i < n_out; ++i) {
     const Type& t = f.results[i];
     if (!shape_matches(out[i], t)) return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " shape mismatch");
-    bool ok = t.dtype == DType::Bool ? out[i].dtype == DLVM_BOOL : (out[i].dtype == DLVM_F32 || out[i].dtype == DLVM_BF16);
+    bool ok = t.dtype == DType::Bool ? out[i].dtype == DLVM_BOOL
+                                     : (out[i].dtype == DLVM_F32 || out[i].dtype == DLVM_BF16 || out[i].dtype == DLVM_F32_ADD);
     if (!ok) return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " dtype mismatch");
+    if (out[i].dtype == DLVM_F32_ADD && fn->out_read[which][i])
+      return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " is read by a later launch: it cannot be accumulated");
     if (!out[i].data || reinterpret_cast<uintptr_t>(out[i].data) % 16)
       return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " NULL or not 16-byte aligned");
   }
@@ -304,7 +331,7 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       for (int i = 1; epi_pf && i < gp.epi.prog.n_in && gp.n_pf < 4; ++i) {  // row-contiguous [M, N] epilogue inputs
         const EwDevIn& r = gp.epi.in[i];
         if (r.nchunks != 1 || r.s[1] != 1 || r.s[0] == 0) continue;
-        const int es = r.st == (uint8_t)SType::F32 ? 4 : r.st == (uint8_t)SType::BF16 ? 2 : 1;
+        const int es = st_bytes(r.st);
         if (reinterpret_cast<uintptr_t>(r.ptr) % 16 || (r.s[0] * es) % 16) continue;
         gp.pf_ptr[gp.n_pf] = r.ptr;
         gp.pf_row_bytes[gp.n_pf] = r.s[0] * es;
@@ -347,7 +374,7 @@ double step_bytes(const Plan& P, const Step& st) {
   const EwGroup& g = st.kind == Step::GEMM ? st.gemm.epi : st.ew;
   auto esz = [&](int buf, SType fallback) {
     SType t = buf >= 0 ? P.bufs[buf].st : fallback;
-    return t == SType::F32 ? 4.0 : t == SType::BF16 ? 2.0 : 1.0;
+    return (double)st_bytes((uint8_t)t);
   };
   double b = 0;
   if (st.kind == Step::EW && st.ew.finalize) {
@@ -495,6 +522,7 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
       try {
         h->plan[which] = make_plan(which ? *h->opt_grad : h->opt_primal, po);
         h->planned[which] = true;
+        h->out_read[which] = outputs_read(h->plan[which]);
       } catch (const Error& e) {
         h->plan_error[which] = e.what();
         if (!(o.flags & DLVM_PLAN_ONLY)) {

@@ -44,7 +44,7 @@ int tma_stages(const EwParams& p, int bx, int by, int n_in, int rows) {
   for (int i = 0; i < n_in; ++i) {
     const EwDevIn& in = p.in[i];
     if (in.s[0] == 0) continue;
-    const int es = in.st == (uint8_t)SType::F32 ? 4 : in.st == (uint8_t)SType::BF16 ? 2 : 1;
+    const int es = st_bytes(in.st);
     if (in.nchunks != 1 || in.s[1] != 1 || reinterpret_cast<uintptr_t>(in.ptr) % 16 || (in.s[0] * es) % 16 ||
         (p.dims[1] * es) % 16)
       return 0;

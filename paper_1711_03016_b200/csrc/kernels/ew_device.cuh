@@ -87,9 +87,17 @@ __device__ __forceinline__ unsigned short f2bf(float f) {
   return *reinterpret_cast<unsigned short*>(&h);
 }
 
+// 4 consecutive f32 (16-byte aligned) added into global memory in one
+// vector reduction (sm_90+ red.global.add.v4.f32), local or peer
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 __device__ __forceinline__ void st1(void* p, int64_t off, uint8_t st, float v) {
   if (st == (uint8_t)SType::F32)
     reinterpret_cast<float*>(p)[off] = v;
+  else if (st == (uint8_t)SType::F32_ADD)  // accumulate (red.global.add; may be peer memory)
+    atomicAdd(reinterpret_cast<float*>(p) + off, v);
   else if (st == (uint8_t)SType::BF16)
     reinterpret_cast<unsigned short*>(p)[off] = f2bf(v);
   else
@@ -99,6 +107,8 @@ __device__ __forceinline__ void st1(void* p, int64_t off, uint8_t st, float v) {
 __device__ __forceinline__ void st4(void* p, int64_t off, uint8_t st, const float* v) {
   if (st == (uint8_t)SType::F32) {
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(p) + off) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if (st == (uint8_t)SType::F32_ADD) {  // one 16-byte vector reduction
+    red_add_v4(reinterpret_cast<float*>(p) + off, v[0], v[1], v[2], v[3]);
   } else if (st == (uint8_t)SType::BF16) {
     uint2 x;
     x.x = (unsigned)f2bf(v[0]) | ((unsigned)f2bf(v[1]) << 16);

@@ -632,7 +632,7 @@ __device__ __forceinline__ void lds4(const unsigned char* p, uint8_t st, float* 
 }
 
 __device__ __forceinline__ int st_size(uint8_t st) {
-  return st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+  return st_bytes(st);
 }
 
 template <class P>

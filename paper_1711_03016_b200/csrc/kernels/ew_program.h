@@ -26,7 +26,18 @@ constexpr int kMaxStores = 6;
 constexpr int kMaxReduces = 4;
 constexpr int kMaxSlots = kMaxIn + kMaxLits + kMaxIns;
 
-enum class SType : uint8_t { F32 = 0, BF16 = 1, U8 = 2 };
+// F32_ADD: an f32 output the kernels ACCUMULATE into (red.global.add) instead
+// of storing -- possibly another GPU's memory over NVLink (dlvm.h DLVM_F32_ADD)
+enum class SType : uint8_t { F32 = 0, BF16 = 1, U8 = 2, F32_ADD = 3 };
+
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+#define DLVM_HD __host__ __device__
+#else
+#define DLVM_HD
+#endif
+DLVM_HD constexpr int st_bytes(uint8_t st) {
+  return st == (uint8_t)SType::F32 || st == (uint8_t)SType::F32_ADD ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+}
 
 enum VmOp : uint8_t {
   VM_NEG = 0, VM_TANH, VM_EXP, VM_LOG, VM_SQRT, VM_ABS, VM_SIGN,

@@ -95,7 +95,7 @@ int launch_smem(const TcParams& tp, int bn, int ctas) {
   return 1024 + tp.et.epi_off + tp.et.n_in_bufs * tp.et.in_buf_bytes + 8 * tp.et.st_slot_bytes;
 }
 
-int es_of(uint8_t st) { return st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1; }
+int es_of(uint8_t st) { return st_bytes(st); }
 
 // 2-D (or, with `splits`, 3-D {cols, rows, splits}) tensor map of an
 // epilogue operand with box {box_cols, box_rows}; box rows of 128 bytes use
@@ -163,7 +163,7 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
   for (int o = 0; o < Pg.n_stores; ++o) {
     const EwDevOut& r = E.out[o];
     const int es = es_of(r.st);
-    if (r.s[1] != 1) return;
+    if (r.s[1] != 1 || r.st == (uint8_t)SType::F32_ADD) return;  // accumulated outputs: direct red path
     const bool split = o == 0 && p.ksplit > 1;
     if (!encode_epi(&tp->tma_st[o], r.ptr, r.st, p.N, p.M, r.s[0] * es, es == 4 ? 32 : 64, 32,
                     split ? p.ksplit : 0, split ? p.split_bytes : 0))

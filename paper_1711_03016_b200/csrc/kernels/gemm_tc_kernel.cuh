@@ -395,6 +395,11 @@ __device__ __forceinline__ void epi_store(const EwDevOut& o, int64_t m0, int64_t
 #pragma unroll
     for (int j = 0; j < RV; ++j)
       if (j < nrow) p[j * rs] = v[j];
+  } else if (o.st == (uint8_t)SType::F32_ADD) {
+    float* p = reinterpret_cast<float*>(o.ptr) + base;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (j < nrow) atomicAdd(p + j * rs, v[j]);
   } else if (o.st == (uint8_t)SType::BF16) {
     unsigned short* p = reinterpret_cast<unsigned short*>(o.ptr) + base;
 #pragma unroll
@@ -523,6 +528,10 @@ __device__ __forceinline__ void epi_row_store(const EwDevOut& o, int64_t m, int6
 #pragma unroll
       for (int k = 0; k < CW / 4; ++k)
         epi_st(reinterpret_cast<float4*>(p + 4 * k), make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+    } else if (o.st == (uint8_t)SType::F32_ADD) {  // accumulate into (possibly peer) memory
+      float* p = reinterpret_cast<float*>(o.ptr) + off;
+#pragma unroll
+      for (int k = 0; k < CW / 4; ++k) red_add_v4(p + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
     } else if (o.st == (uint8_t)SType::BF16) {
       unsigned w[CW / 2];
 #pragma unroll
@@ -574,7 +583,7 @@ __device__ __forceinline__ bool seg_vector(const EwDevIn& in) { return in.s[1] =
 constexpr bool kEpiL1Prefetch = DLVM_EPI_L1_PREFETCH != 0;
 
 __device__ __forceinline__ void epi_row_prefetch_l1(const EwDevIn& in, int64_t m, int64_t n0) {
-  const int es = in.st == (uint8_t)SType::F32 ? 4 : in.st == (uint8_t)SType::BF16 ? 2 : 1;
+  const int es = st_bytes(in.st);
   const char* a = reinterpret_cast<const char*>(in.ptr) + (m * in.s[0] + n0) * es;
   asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
 }
@@ -1034,7 +1043,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       bool row_vec = vec_ok;
       if (row_vec) {
         auto al = [&](const void* p, int64_t s0, uint8_t st) {
-          const int es = st == (uint8_t)SType::F32 ? 4 : st == (uint8_t)SType::BF16 ? 2 : 1;
+          const int es = st_bytes(st);
           const int w = CW * es < 16 ? CW * es : 16;
           return ((reinterpret_cast<uintptr_t>(p) + (uintptr_t)(m * s0 * es)) & (uintptr_t)(w - 1)) == 0;
         };

@@ -118,7 +118,7 @@ std::vector<int64_t> contig_strides(const std::vector<int64_t>& shape) {
   }
   return st;
 }
-size_t stype_size(SType t) { return t == SType::F32 ? 4 : t == SType::BF16 ? 2 : 1; }
+size_t stype_size(SType t) { return (size_t)st_bytes((uint8_t)t); }
 
 [[noreturn]] void unsupported(const std::string& m) { throw Error(kStatusUnsupported, 0, 0, m); }
 

@@ -16,7 +16,7 @@ _LIB_PATH = os.environ.get("DLVM_LIBRARY") or os.path.join(os.path.dirname(os.pa
 
 DLVM_OK, DLVM_ERR_VERIFY, DLVM_ERR_PARSE, DLVM_ERR_USAGE, DLVM_ERR_RUNTIME, DLVM_ERR_CUDA, \
     DLVM_ERR_UNSUPPORTED = range(7)
-DLVM_BOOL, DLVM_F32, DLVM_F64, DLVM_BF16 = range(4)
+DLVM_BOOL, DLVM_F32, DLVM_F64, DLVM_BF16, DLVM_F32_ADD = range(5)
 DLVM_DOT_F32, DLVM_DOT_BF16 = 0, 1
 DLVM_PLAN_ONLY, DLVM_NO_FUSION, DLVM_NO_SPECIALIZE, DLVM_NO_OPT, DLVM_NO_JIT = 1, 2, 4, 8, 16
 DLVM_PRIMAL, DLVM_GRADIENT = 0, 1
@@ -103,7 +103,34 @@ def _require_cuda(ts) -> None:
             raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
 
 
+class AddInto:
+    """Output binding DLVM_F32_ADD (dlvm.h): the kernels accumulate this
+    output into `target` instead of storing it.  `target` is a float32 CUDA
+    tensor, or a raw device address (int) -- e.g. a peer GPU's
+    symmetric-memory buffer reachable over NVLink -- with `shape` given."""
+
+    def __init__(self, target, shape=None):
+        if isinstance(target, int):
+            if shape is None:
+                raise ValueError("AddInto(address) needs a shape")
+            self.ptr, self.shape = target, tuple(shape)
+        else:
+            import torch
+            if target.dtype != torch.float32 or not target.is_cuda or not target.is_contiguous():
+                raise ValueError("AddInto needs a contiguous float32 CUDA tensor")
+            self.ptr, self.shape = target.data_ptr(), tuple(target.shape)
+            self.tensor = target
+
+
 def _tensor(t) -> dlvm_tensor:
+    if isinstance(t, AddInto):
+        d = dlvm_tensor()
+        d.data = t.ptr
+        d.dtype = DLVM_F32_ADD
+        d.rank = len(t.shape)
+        for i, s in enumerate(t.shape):
+            d.shape[i] = s
+        return d
     if not t.is_cuda:
         raise ValueError("dlvm tensors must be CUDA tensors (device memory)")
     if not t.is_contiguous():

@@ -161,3 +161,93 @@ class DataParallelStep:
             w.wait()  # makes the current stream wait for the collective
         self.streams.wait_stream(st, self.comm)
         return self.outputs
+
+
+def assign_owners(sizes: Sequence[int], world: int) -> List[int]:
+    """Owner rank of each gradient: largest first onto the least-loaded rank
+    (deterministic, identical on every rank)."""
+    load = [0] * world
+    owner = [0] * len(sizes)
+    for g in sorted(range(len(sizes)), key=lambda i: (-sizes[i], i)):
+        r = min(range(world), key=lambda k: (load[k], k))
+        owner[g] = r
+        load[r] += sizes[g]
+    return owner
+
+
+class FusedReduceStep:
+    """Data-parallel step with the gradient reduction fused into the kernels
+    that produce the gradients (over NVLink peer
+    memory): the flat gradient buffer is symmetric memory (one copy per rank,
+    every rank can address every copy); each gradient has an owner rank
+    (assign_owners), and every rank's dlvm_grad_run binds each gradient
+    output as DLVM_F32_ADD into the OWNER's copy, so the dW GEMM epilogues /
+    element-wise finalisers add their partial gradients straight into the
+    owner's memory (red.global.add over NVLink) -- no separate all-reduce
+    pass.  Protocol per step: zero this rank's copy, barrier (nobody adds
+    before every copy is zeroed), grad_run, barrier (every contribution has
+    landed); owners then hold the global-batch gradients of their tensors
+    (seed 1/B_global, F15).  With `gather=True` each owner also copies its
+    gradients into every peer's copy (so every rank ends with all of them,
+    as after an all-reduce).  At world size 1 the owner is this rank and the
+    step is a plain run accumulating into zeroed memory."""
+
+    def __init__(self, fn, n_grads: int, device, group=None, gather: bool = True):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        from .dlvm import AddInto
+        self.AddInto = AddInto
+        self.fn, self.n_grads, self.device, self.gather = fn, n_grads, device, gather
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        _, outs = fn.signature(1)
+        self.shapes = [tuple(s) for s, _ in outs[:n_grads]]
+        self.offsets, total = flat_layout(self.shapes)
+        self.flat = symm.empty(max(total, 1), dtype=torch.float32, device=device)
+        self.handle = symm.rendezvous(self.flat, self.group.group_name)
+        self.ptrs = list(self.handle.buffer_ptrs)
+        sizes = []
+        for s in self.shapes:
+            k = 1
+            for d in s:
+                k *= d
+            sizes.append(k)
+        self.sizes = sizes
+        self.owner = assign_owners(sizes, self.world)
+        self.views = [self.flat[o:o + k].view(s) for o, k, s in zip(self.offsets, sizes, self.shapes)]
+        self.kept = [torch.empty(s, dtype=torch.float32, device=device) for s, _ in outs[n_grads:]]
+        self.bindings = [AddInto(self.ptrs[self.owner[g]] + 4 * self.offsets[g], self.shapes[g])
+                         for g in range(n_grads)] + self.kept
+
+    def _barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        if hasattr(self.handle, "barrier"):
+            self.handle.barrier()  # device-side barrier over the symmetric signal pads
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+
+    def step(self, inputs, seed, stream=None):
+        import torch
+        st = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            self.flat.zero_()
+            self._barrier()
+            self.fn.grad_run(inputs, seed=seed, outputs=self.bindings, stream=st.cuda_stream)
+            self._barrier()
+            if self.gather and self.world > 1:
+                for g in range(self.n_grads):
+                    if self.owner[g] != self.rank:
+                        continue
+                    for r in range(self.world):
+                        if r != self.rank:
+                            peer = self.handle.get_buffer(r, self.shapes[g], torch.float32,
+                                                          storage_offset=self.offsets[g])
+                            peer.copy_(self.views[g])
+                self._barrier()
+        return self.views + self.kept

@@ -203,3 +203,15 @@ def test_data_parallel_step_two_ranks_bucket_order_and_event_gating():
         i += 1
     assert issued == [list(b) for b in reversed(buckets)]
     assert log[-1] == ("wait_stream", "compute", "comm")
+
+
+def test_assign_owners_balanced_and_deterministic():
+    from paper_1711_03016_b200.dp import assign_owners
+    sizes = [4096 * 4096, 4096, 4096 * 4096, 4096, 4096 * 1000, 1000]
+    assert assign_owners(sizes, 1) == [0] * 6
+    o2 = assign_owners(sizes, 2)
+    assert o2[0] != o2[2]  # the two big gradients on different ranks
+    load = [sum(s for s, o in zip(sizes, o2) if o == r) for r in range(2)]
+    assert max(load) - min(load) <= 4096 * 1000 + 4096 + 1000
+    assert assign_owners(sizes, 8) == assign_owners(list(sizes), 8)
+    assert sorted(set(assign_owners(sizes, 8))) == list(range(6))
