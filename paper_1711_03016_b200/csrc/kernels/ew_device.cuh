@@ -124,6 +124,26 @@ __device__ __forceinline__ void st4(void* p, int64_t off, uint8_t st, const floa
 // load input `in` at element offset `off` (column stride cs) into v[0..VEC)
 template <int VEC>
 __device__ __forceinline__ void vm_load(const EwDevIn& in, int64_t off, int64_t cs, float* v) {
+  if (in.nchunks > 1 && in.chunk_op == 0 && VEC == 4 && cs == 1 && in.chunk_stride % 4 == 0) {
+    // sum of partials (split-K, reductions), four contiguous columns per
+    // load: one 16-byte load per chunk, several chunks in flight, summed in
+    // chunk order per column (the same order as the scalar path below)
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < in.nchunks; k += 4) {
+      float x[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + u < in.nchunks) ld4(in.ptr, off + (k + u) * in.chunk_stride, in.st, x[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + u < in.nchunks)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) s[j] = __fadd_rn(s[j], x[u][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) v[j] = s[j];
+    return;
+  }
   if (in.nchunks > 1) {
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
