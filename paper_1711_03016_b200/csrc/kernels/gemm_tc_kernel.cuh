@@ -79,6 +79,7 @@ struct TcParams {
   GemmParams g;
   int32_t tiles_m, tiles_n;
   int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
+  int32_t group_m;             // tile raster: tile-rows per group (N-fastest inside a group is M-fastest here)
 #ifdef DLVM_GEMM_TRACE
   unsigned long long* trace;   // [gridDim.x][8] %globaltimer stamps (trace builds, tools/gemm_trace.py)
 #endif
@@ -665,12 +666,12 @@ __device__ __forceinline__ float col_butterfly(float (&x)[CW], int lane, int* co
 // Tile raster: groups of GROUP_M tile-rows, N fastest inside a group, so the
 // ~148 tiles in flight share a few A row-panels and all of B through L2
 // (a plain M-fastest order re-reads A once per N tile).
-constexpr int GROUP_M = 8;
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int* tm, int* tn) {
-  const int per_group = GROUP_M * tiles_n;
+constexpr int GROUP_M = 8;  // default group height (TcParams.group_m, DLVM_GEMM_GROUP_M)
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int* tm, int* tn, int group_m = GROUP_M) {
+  const int per_group = group_m * tiles_n;
   const int grp = t / per_group;
-  const int first = grp * GROUP_M;
-  const int gsz = min(GROUP_M, tiles_m - first);
+  const int first = grp * group_m;
+  const int gsz = min(group_m, tiles_m - first);
   const int r = t - grp * per_group;
   *tm = first + r % gsz;
   *tn = r / gsz;
@@ -823,7 +824,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     for (int t = tile0; t < n_tiles; t += tile_step) {
       int tm, tn;
       const int split = t / base_tiles;
-      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
+      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
       const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
       for (int i = 0; i < g.n_pf; ++i) {
         const int64_t cols = min((int64_t)BN, g.N - n0);
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       int it = 0;
       for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
         int tm, tn;
-        tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
+        tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
         const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
         const int b = xt.n_in_bufs == 2 ? (it & 1) : 0;
         const uint32_t ph = xt.n_in_bufs == 2 ? ((it >> 1) & 1) : (it & 1);
@@ -1029,7 +1030,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
       int tm, tn;
       const int split = t / base_tiles;
-      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn);
+      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
       tm = tm * CTAS + (int)rank;  // this CTA's 128-row block (partials layout)
       // split K: this work item's raw accumulator goes to its split's slice
       EwDevOut out0 = E.out[0];
