@@ -148,7 +148,10 @@ dlvm_status dlvm_fn_signature(dlvm_fn fn, int which, int* n_in, dlvm_tensor* in_
  * (8) the kernels specialised at create time by NVRTC (one line each:
  * plan, step, status, instantiation), or the detailed plan of the primal (9)
  * / gradient (10): buffers, then every step's iteration space, launch shape,
- * program signature and operand refs (buffer, offset, strides, chunks).
+ * program signature and operand refs (buffer, offset, strides, chunks), or
+ * the two-stream schedule of the primal (11) / gradient (12): per step the
+ * stream (the caller's, or the handle's auxiliary stream running an
+ * independent GEMM beside the previous one) and its cross-stream waits.
  * Writes at most `cap` bytes
  * including the NUL; *needed receives the full size including the NUL. */
 dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* needed);

@@ -39,12 +39,129 @@ struct dlvm_fn_s {
   bool specialize = true;
   std::vector<void*> jit_fn[2];  // per plan step: create-time specialised kernel (CUfunction) or null
   std::vector<char> out_read[2]; // per output: some launch reads it back (it cannot be bound as DLVM_F32_ADD)
+  // two-stream schedule (plan_streams): per step the stream (0 = caller's,
+  // 1 = the handle's auxiliary stream), the earlier steps on the other
+  // stream it waits for, and whether an event is recorded after it
+  std::vector<char> step_stream[2];
+  std::vector<std::vector<int>> step_waits[2];
+  std::vector<char> step_signals[2];
+  bool concurrent[2] = {false, false};
+  int device = -1;
+  cudaStream_t aux = nullptr;
+  std::vector<cudaEvent_t> events;  // one per step that signals, plus fork / join
+  ~dlvm_fn_s() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    if (aux) cudaStreamDestroy(aux);
+  }
   std::string jit_report;        // print mode 8
 };
 
 namespace {
 
 thread_local std::string g_last_error;
+
+int64_t numel_of(const dlvm_tensor& t) {
+  int64_t n = 1;
+  for (int d = 0; d < t.rank; ++d) n *= t.shape[d];
+  return n;
+}
+
+// buffers a step reads / writes (buffer ids of the plan)
+void step_buffers(const Step& st, std::vector<int>* rd, std::vector<int>* wr) {
+  auto group = [&](const EwGroup& g) {
+    for (auto& r : g.inputs)
+      if (r.buf >= 0) rd->push_back(r.buf);
+    for (auto& r : g.stores) wr->push_back(r.buf);
+    for (auto& r : g.reduces) {
+      if (r.buf >= 0) wr->push_back(r.buf);
+      if (r.direct_buf >= 0) wr->push_back(r.direct_buf);
+    }
+  };
+  if (st.kind == Step::EW) {
+    group(st.ew);
+  } else if (st.kind == Step::GEMM) {
+    for (auto& sg : st.gemm.seg) {
+      rd->push_back(sg.a.buf);
+      rd->push_back(sg.b.buf);
+    }
+    group(st.gemm.epi);
+  } else if (st.kind == Step::CAST) {
+    wr->push_back(st.cast.dst_buf);
+  }
+}
+
+// Two-stream schedule of a plan: a tensor-core GEMM that does not depend
+// (through any buffer, transitively) on the GEMM launched before it runs on
+// the auxiliary stream beside it -- the independent weight- and activation-
+// gradient GEMMs of a layer (dW_l = H^T dZ_l and dZ_{l-1} = dZ_l W^T) -- and
+// the steps that only need it follow it there; every cross-stream
+// dependency becomes an event wait.  Both GEMMs of such a pair use dynamic
+// tile scheduling, so the one that starts second takes over tiles as the
+// other's SMs free up.
+void plan_streams(dlvm_fn_s* h, int which) {
+  const Plan& P = h->plan[which];
+  const int n = (int)P.steps.size();
+  std::vector<std::vector<int>> rd(n), wr(n), deps(n);
+  for (int i = 0; i < n; ++i) step_buffers(P.steps[i], &rd[i], &wr[i]);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < j; ++i) {
+      bool d = false;
+      for (int b : rd[j])
+        for (int c : wr[i]) d |= b == c;   // RAW
+      for (int b : wr[j]) {
+        for (int c : wr[i]) d |= b == c;   // WAW
+        for (int c : rd[i]) d |= b == c;   // WAR
+      }
+      if (d) deps[j].push_back(i);
+    }
+  // ancestors (transitive dependencies) as bit rows
+  std::vector<std::vector<char>> anc(n, std::vector<char>(n, 0));
+  for (int j = 0; j < n; ++j)
+    for (int i : deps[j]) {
+      anc[j][i] = 1;
+      for (int k = 0; k < n; ++k) anc[j][k] |= anc[i][k];
+    }
+  std::vector<char>& stream = h->step_stream[which];
+  stream.assign(n, 0);
+  int prev_gemm = -1;
+  bool any = false;
+  for (int j = 0; j < n; ++j) {
+    const Step& s = P.steps[j];
+    if (s.kind == Step::GEMM && s.gemm.tensor_core) {
+      if (prev_gemm >= 0 && stream[prev_gemm] == 0 && !anc[j][prev_gemm]) {
+        stream[j] = 1;
+        any = true;
+      }
+      prev_gemm = j;
+    } else if (s.kind == Step::EVENT) {
+      // recorded on the stream of the gradient's last writer (the step before)
+      stream[j] = j > 0 ? stream[j - 1] : 0;
+    } else {
+      // element-wise steps follow their latest dependency
+      int last = -1;
+      for (int i : deps[j]) last = std::max(last, i);
+      stream[j] = last >= 0 ? stream[last] : 0;
+    }
+  }
+  h->concurrent[which] = any;
+  std::vector<std::vector<int>>& waits = h->step_waits[which];
+  std::vector<char>& signals = h->step_signals[which];
+  waits.assign(n, {});
+  signals.assign(n, 0);
+  if (!any) return;
+  for (int j = 0; j < n; ++j) {
+    // wait for the latest dependency on the other stream (earlier ones on it
+    // are ordered by that stream)
+    int last = -1;
+    for (int i : deps[j])
+      if (stream[i] != stream[j]) last = std::max(last, i);
+    if (P.steps[j].kind == Step::EVENT && j > 0 && stream[j - 1] != stream[j]) last = j - 1;
+    if (last >= 0) {
+      waits[j].push_back(last);
+      signals[last] = 1;
+    }
+  }
+}
 
 // outputs whose buffer a later launch of the plan reads (e.g. a kept value
 // feeding more work): their final value must be stored, not accumulated
@@ -222,7 +339,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     if (!out[i].data || reinterpret_cast<uintptr_t>(out[i].data) % 16)
       return fail(DLVM_ERR_USAGE, "output " + std::to_string(i) + " NULL or not 16-byte aligned");
   }
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  cudaStream_t stream_main = static_cast<cudaStream_t>(stream_v);
+  cudaStream_t stream = stream_main;
   // dlvm_options.device >= 0: the launches go to that device (made current
   // for the duration of the call, then restored); -1: the caller's current one
   DeviceGuard dg;
@@ -266,10 +384,79 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     return cudaEventRecord(static_cast<cudaEvent_t>(lev[i]), stream);
   };
   const std::vector<void*>& jit = fn->jit_fn[which];
+  // dynamic tile scheduling of the tcgen05 GEMMs (DLVM_GEMM_DYN=1): their
+  // work counters live in the workspace and start at zero every run
+  static const bool dyn_env = [] {
+    const char* e = std::getenv("DLVM_GEMM_DYN");
+    return e && e[0] == '1';
+  }();
+  // two streams (plan_streams) when enabled (DLVM_CONCURRENT=1), no
+  // profiling hook is set and no output overlaps an input in memory (the
+  // schedule's dependencies are by buffer, not by address).  Off by default:
+  // measured on c3 (tools/gemm_trace.py), the GEMM started second gets only
+  // the SMs the first one leaves idle until that one's single-tile CTAs
+  // exit, so the pair takes as long as the two in sequence (d13 || d11:
+  // 44.5 vs 35.4 us; d20 || d18: 85 vs 81 us) -- each CTA still pays its own
+  // prologue and exposed epilogue.
+  static const bool conc_env = [] {
+    const char* e = std::getenv("DLVM_CONCURRENT");
+    return e && e[0] == '1';
+  }();
+  bool conc = conc_env && fn->concurrent[which] && lev.empty();
+  for (size_t k = 0; conc && k < P.bufs.size(); ++k) {
+    if (P.bufs[k].kind != BufferSlot::Output) continue;
+    const dlvm_tensor& o = out[P.bufs[k].index];
+    const char* o0 = static_cast<const char*>(o.data);
+    const char* o1 = o0 + numel_of(o) * st_bytes((uint8_t)stype_of(o.dtype));
+    for (int i = 0; i < n_in && conc; ++i) {
+      const char* i0 = static_cast<const char*>(in[i].data);
+      const char* i1 = i0 + numel_of(in[i]) * st_bytes((uint8_t)stype_of(in[i].dtype));
+      conc = !(o0 < i1 && i0 < o1);
+    }
+  }
+  const int nsteps = (int)P.steps.size();
+  if (conc) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!fn->aux || fn->device != dev) {
+      if (fn->aux) cudaStreamDestroy(fn->aux);
+      for (cudaEvent_t ev : fn->events) cudaEventDestroy(ev);
+      fn->events.clear();
+      fn->aux = nullptr;
+      if (cudaStreamCreateWithFlags(&fn->aux, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(DLVM_ERR_CUDA, "cudaStreamCreate failed");
+      fn->device = dev;
+    }
+    while ((int)fn->events.size() < nsteps + 1) {
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        return fail(DLVM_ERR_CUDA, "cudaEventCreate failed");
+      fn->events.push_back(ev);
+    }
+    // fork: the auxiliary stream starts after everything queued before this run
+    cudaError_t e = cudaEventRecord(fn->events[nsteps], stream_main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(fn->aux, fn->events[nsteps], 0);
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("fork: ") + cudaGetErrorString(e));
+  }
+  // dynamic tile scheduling (DLVM_GEMM_DYN=1, or every GEMM of a two-stream
+  // run): the work counters live in the workspace and start at zero
+  const bool dyn = (dyn_env || conc) && P.sched_buf >= 0;
+  if (dyn) {
+    cudaError_t e = cudaMemsetAsync(b.ptr[P.sched_buf], 0, (size_t)P.n_sched * 4, stream_main);
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  }
+  bool aux_used = false;
   for (size_t si = 0; si < P.steps.size(); ++si) {
     const Step& st = P.steps[si];
     void* const jf = si < jit.size() ? jit[si] : nullptr;
     cudaError_t e = cudaSuccess;
+    if (conc) {
+      stream = fn->step_stream[which][si] ? fn->aux : stream_main;
+      aux_used |= stream == fn->aux;
+      for (int w : fn->step_waits[which][si])
+        if ((e = cudaStreamWaitEvent(stream, fn->events[w], 0)) != cudaSuccess)
+          return fail(DLVM_ERR_CUDA, std::string("cudaStreamWaitEvent: ") + cudaGetErrorString(e));
+    }
     if (st.kind == Step::EW && st.ew.finalize && st.ew.direct_buf >= 0 && b.st[st.ew.direct_buf] == (uint8_t)SType::F32)
       continue;  // the producer wrote the single partial into the f32 home
     if (st.counted_launch() && (e = mark(li++)) != cudaSuccess)
@@ -317,6 +504,7 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       gp.bm = g.bm;
       gp.bn = g.bn;
       gp.ksplit = g.ksplit;
+      gp.sched = dyn && g.sched_index >= 0 ? static_cast<int*>(b.ptr[P.sched_buf]) + g.sched_index : nullptr;
       gp.split_bytes = g.split_bytes;
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);
@@ -360,6 +548,15 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       if (events && events[st.event_index]) e = cudaEventRecord(static_cast<cudaEvent_t>(events[st.event_index]), stream);
     }
     if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("CUDA error in '") + st.desc + "': " + cudaGetErrorString(e));
+    if (conc && fn->step_signals[which][si] && (e = cudaEventRecord(fn->events[si], stream)) != cudaSuccess)
+      return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+  }
+  if (conc) {  // join: the caller's stream continues after the auxiliary one
+    stream = stream_main;
+    cudaError_t e = cudaEventRecord(fn->events[nsteps], fn->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream_main, fn->events[nsteps], 0);
+    if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("join: ") + cudaGetErrorString(e));
+    (void)aux_used;
   }
   if (!lev.empty()) {
     cudaError_t e = mark(li);
@@ -523,6 +720,7 @@ dlvm_status dlvm_fn_create(const char* module_text, size_t len, const char* fn_n
         h->plan[which] = make_plan(which ? *h->opt_grad : h->opt_primal, po);
         h->planned[which] = true;
         h->out_read[which] = outputs_read(h->plan[which]);
+        plan_streams(h, which);
       } catch (const Error& e) {
         h->plan_error[which] = e.what();
         if (!(o.flags & DLVM_PLAN_ONLY)) {
@@ -615,8 +813,22 @@ dlvm_status dlvm_fn_print(dlvm_fn fn, int which, char* buf, size_t cap, size_t* 
         s = fn->planned[w] ? fn->plan[w].detail() : "unsupported: " + fn->plan_error[w] + "\n";
         break;
       }
+      case 11:
+      case 12: {  // two-stream schedule of the primal (11) / gradient (12)
+        int w = which - 11;
+        if (w == 1 && !fn->grad) return fail(DLVM_ERR_USAGE, "handle has no gradient function");
+        if (!fn->planned[w]) return fail(DLVM_ERR_UNSUPPORTED, fn->plan_error[w]);
+        const Plan& P = fn->plan[w];
+        s = std::string("streams: ") + (fn->concurrent[w] ? "two" : "one") + "\n";
+        for (size_t i = 0; i < P.steps.size(); ++i) {
+          s += "  [" + std::to_string(i) + "] " + (fn->step_stream[w][i] ? "aux " : "main") + " ";
+          for (int k : fn->step_waits[w][i]) s += "wait[" + std::to_string(k) + "] ";
+          s += P.steps[i].desc.substr(0, 60) + "\n";
+        }
+        break;
+      }
       default:
-        return fail(DLVM_ERR_USAGE, "which must be 0..10");
+        return fail(DLVM_ERR_USAGE, "which must be 0..12");
     }
   } catch (const std::exception& e) {
     return fail(DLVM_ERR_RUNTIME, e.what());

@@ -251,6 +251,7 @@ int num_sms() {
 bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog = false) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
+  tp->sched = p.sched;
 #ifdef DLVM_GEMM_TRACE
   // launch k of the traced run writes slice k % slots of [slots][148][8]
   tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * 8

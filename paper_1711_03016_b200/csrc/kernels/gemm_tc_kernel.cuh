@@ -80,6 +80,7 @@ struct TcParams {
   int32_t tiles_m, tiles_n;
   int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
   int32_t group_m;             // tile raster: tile-rows per group (N-fastest inside a group is M-fastest here)
+  int* sched;                  // dynamic tile scheduling: zeroed work counter (nullptr: static round robin)
 #ifdef DLVM_GEMM_TRACE
   unsigned long long* trace;   // [gridDim.x][8] %globaltimer stamps (trace builds, tools/gemm_trace.py)
 #endif
@@ -128,6 +129,29 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 // compiles to MEMBAR.ALL.GPU and stalls the epilogue on its own stores
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_shared_s32(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_s32(uint32_t addr, int v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -758,11 +782,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const uint32_t sA = base;
   const uint32_t sB = base + nst * A_STAGE_BYTES;
   // barriers: full[<=6] @0, empty[<=6] @48, tfull[2] @96, tempty[2] @112,
-  // in_full[2] @128, in_empty[2] @144; TMEM address @192; reductions @256
+  // in_full[2] @128, in_empty[2] @144, tile queue tq_full[4] @160 and
+  // tq_empty[4] @192; TMEM address @224; tile ids tileq[4] @240; reductions @256
   const uint32_t sBar = sB + nst * B_STAGE_BYTES;
   const uint32_t full_bar = sBar, empty_bar = sBar + 48, tfull_bar = sBar + 96, tempty_bar = sBar + 112,
-                 in_full_bar = sBar + 128, in_empty_bar = sBar + 144;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 192);
+                 in_full_bar = sBar + 128, in_empty_bar = sBar + 144, tq_full_bar = sBar + 160,
+                 tq_empty_bar = sBar + 192, tileq = sBar + 240;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (sBar - base) + 224);
   // reduction scratch sized by the program's reduction count (NRS; the
   // interpreter reserves kEpiReds), so programs without reductions leave
   // that space to the pipeline / TMA epilogue (host: tail_bytes)
@@ -778,6 +804,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   const int n_tiles = base_tiles * nsplit;       // work items (tile, K split)
   const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
   const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
+  // Dynamic scheduling (P.sched != nullptr): the first tile of every CTA
+  // (pair) is its static one; later ones come from an atomic counter
+  // (tile_step + counter), fetched by the leader's producer lane one tile
+  // ahead and published through the shared tile queue to every other role
+  // of the pair (the peer through distributed shared memory), so a grid
+  // running beside another kernel takes over tiles as SMs free up.
+  const bool dyn = P.sched != nullptr;
+  auto tq_publish = [&](int k, int t) {  // leader, warp 0, lane 0
+    const int slot = k & 3;
+    mbar_wait(tq_empty_bar + 8 * slot, ((k >> 2) & 1) ^ 1);
+    st_shared_s32(tileq + 4 * slot, t);
+    if constexpr (CTAS == 2) {
+      st_cluster_u32(mapa_rank(tileq + 4 * slot, 1), t);
+      mbar_arrive_release_cluster(mapa_rank(tq_full_bar + 8 * slot, 1));
+    }
+    mbar_arrive(tq_full_bar + 8 * slot);
+  };
+  auto tq_take = [&](int k) -> int {  // one lane of a consumer role
+    const int slot = k & 3;
+    mbar_wait_acq_cluster(tq_full_bar + 8 * slot, (k >> 2) & 1);
+    const int t = ld_shared_s32(tileq + 4 * slot);
+    if constexpr (CTAS == 2) {
+      if (rank != 0) {
+        mbar_arrive_cluster(mapa_rank(tq_empty_bar + 8 * slot, 0));
+        return t;
+      }
+    }
+    mbar_arrive(tq_empty_bar + 8 * slot);
+    return t;
+  };
+  // tile of iteration k for a consumer warp (lane 0 takes, the warp shares)
+  auto warp_tile = [&](int k) -> int {
+    if (!dyn) return tile0 + k * tile_step;
+    int t = 0;
+    if (lane == 0) t = tq_take(k);
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
@@ -789,6 +852,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       mbar_init(tempty_bar + 8 * s, 8 * CTAS);  // one arrival per epilogue warp of the pair
       mbar_init(in_full_bar + 8 * s, 1);        // the loader's arrive + the staged bytes
       mbar_init(in_empty_bar + 8 * s, 8);       // one arrival per epilogue warp of this CTA
+    }
+    // tile queue (dynamic scheduling): one publish per slot use; released by
+    // every consumer of the pair: the peer's producer, the MMA issuer, the
+    // epilogue warps and the input loaders
+    const int n_cons = (CTAS == 2 ? 1 : 0) + 1 + 8 * CTAS + (xt.on && xt.n_in_bufs > 0 ? CTAS : 0);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(tq_full_bar + 8 * s, 1);
+      mbar_init(tq_empty_bar + 8 * s, n_cons);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int q = 0; q < g.n_seg; ++q) {
@@ -821,7 +892,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
     int s = 0;
     uint32_t ph = 0;
-    for (int t = tile0; t < n_tiles; t += tile_step) {
+    int t_next = tile0;  // leader lane 0 (dynamic): the tile published for the next iteration
+    if (dyn && rank == 0 && lane == 0) tq_publish(0, t_next);
+    for (int pit = 0;; ++pit) {
+      int t;
+      if (!dyn) {
+        t = tile0 + pit * tile_step;
+      } else {
+        int tl = 0;
+        if (lane == 0) {
+          if (rank == 0) {
+            tl = t_next;
+            if (tl < n_tiles) {  // fetch and publish the next one ahead of need
+              t_next = tile_step + atomicAdd(P.sched, 1);
+              tq_publish(pit + 1, t_next);
+            }
+          } else {
+            tl = tq_take(pit);
+          }
+        }
+        t = __shfl_sync(0xffffffffu, tl, 0);
+      }
+      if (t >= n_tiles) break;
       int tm, tn;
       const int split = t / base_tiles;
       tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
@@ -895,8 +987,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
       int s = 0;
       uint32_t ph = 0;
-      int it = 0;
-      for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+      for (int it = 0;; ++it) {
+        const int t = dyn ? tq_take(it) : tile0 + it * tile_step;
+        if (t >= n_tiles) break;
         const int split = t / base_tiles;
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
@@ -946,8 +1039,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     if (xt.on && xt.n_in_bufs > 0 && lane == 0) {
       const uint32_t in_base = base + (uint32_t)xt.epi_off;
       const EwParams& E = g.epi;
-      int it = 0;
-      for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+      for (int it = 0;; ++it) {
+        const int t = dyn ? tq_take(it) : tile0 + it * tile_step;
+        if (t >= n_tiles) break;
         int tm, tn;
         tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
         const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
@@ -1026,8 +1120,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #ifdef DLVM_GEMM_TRACE
     long long sect[6] = {0, 0, 0, 0, 0, 0}, sect_t0 = clock64();
 #endif
-    int it = 0;
-    for (int t = tile0; t < n_tiles; t += tile_step, ++it) {
+    for (int it = 0;; ++it) {
+      const int t = warp_tile(it);
+      if (t >= n_tiles) break;
       int tm, tn;
       const int split = t / base_tiles;
       tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);

@@ -73,6 +73,7 @@ struct GemmParams {
   // output at + split * split_bytes (a following EW step sums the splits)
   int32_t ksplit;
   int64_t split_bytes;
+  int* sched;                // tcgen05: zeroed work counter (dynamic tile scheduling) or nullptr
   int32_t n_pf;
   const void* pf_ptr[4];
   int64_t pf_row_bytes[4];  // row stride in bytes

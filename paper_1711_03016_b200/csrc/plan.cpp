@@ -1649,6 +1649,9 @@ struct Planner {
       finalize_reds(reds, (int)plan.steps.size() - 1, s.ew.gx, s.ew.gy, R, C, "ew");
     }
     add_events();
+    for (auto& st : plan.steps)
+      if (st.kind == Step::GEMM && st.gemm.tensor_core) st.gemm.sched_index = plan.n_sched++;
+    if (plan.n_sched) plan.sched_buf = add_buf(BufferSlot::Work, -1, (size_t)plan.n_sched * 4, SType::U8);
     plan.workspace_bytes = (plan.workspace_bytes + 255) / 256 * 256;
     plan.n_inputs = plan.seed_is_input ? f.num_args() - 1 : f.num_args();
     plan.n_outputs = (int)f.ret.size();

@@ -105,6 +105,7 @@ struct GemmStep {
   int64_t split_bytes = 0;       // byte stride between the partial tiles
   int bm = 128, bn = 128;        // tile shape (partials layout of epilogue reductions)
   EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator
+  int sched_index = -1;          // tcgen05: this GEMM's work counter in Plan::sched_buf (dynamic scheduling)
 };
 
 struct CastStep {                // bf16 copy of an input (cast from f32 and/or rows padded to ld)
@@ -138,6 +139,7 @@ struct Plan {
   bool seed_is_input = false;    // gradient plans: last parameter is the seed
   std::vector<int> input_bf16_ok;  // per input: 1 if it may be passed as bf16 (see make_plan)
   std::vector<int> input_u8_ok;    // per input: 1 if it may be passed as bool bytes (0/1 values; not a dot operand)
+  int sched_buf = -1, n_sched = 0;  // work counters of the tcgen05 GEMMs (zeroed at the start of a run)
   int launches() const;
   std::string str() const;
   std::string detail() const;  // str() + buffers and every step's operand refs

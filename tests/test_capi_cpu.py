@@ -613,3 +613,21 @@ def test_reduce_max_and_softmax_ce_through_cpp_ad():
     with pytest.raises(P.DlvmError) as e:
         P.Function(t.replace("by max", "by min"), "f", "g", flags=P.DLVM_PLAN_ONLY)
     assert e.value.status == 2
+
+
+def test_two_stream_schedule_of_c3_gradient():
+    """plan_streams (print mode 12): the activation-gradient GEMMs d11 / d18
+    run on the auxiliary stream beside the weight-gradient GEMMs they do not
+    depend on (d13 / d20), with an event wait for their producers; the next
+    weight gradient waits for them; primal plans (a dependent chain) stay on
+    one stream."""
+    w = W.c3()
+    f = _plan_only(w.text, w.fn, w.grad, "bf16")
+    s = f.print(12)
+    lines = s.splitlines()
+    assert lines[0] == "streams: two"
+    aux = [l for l in lines if " aux " in l]
+    assert any("%d11" in l and "wait[" in l for l in aux), s
+    assert any("%d18" in l and "wait[" in l for l in aux), s
+    assert any("main" in l and "%d20" in l and "wait[" in l for l in lines), s
+    assert f.print(11).startswith("streams: one")

@@ -1399,3 +1399,45 @@ def test_reduce_max_ties_bit_exact():
     k = (a == a.max(axis=1, keepdims=True)).sum(axis=1)
     pow2 = (k & (k - 1)) == 0
     np.testing.assert_array_equal(res["grad"][0][pow2], ref[pow2])
+
+
+_STREAMS_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+outs = []
+for w in (W.c3(256, layers=[(512, 512, "relu"), (512, 512, "relu"), (512, 256, None)]),
+          W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)])):
+    r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16", which="grad")
+    outs += r["grad"]
+    r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16", which="grad")
+    outs += r["grad"]  # a second run on the same handle state
+np.savez({out!r}, *outs)
+"""
+
+
+def test_two_stream_schedule_bit_identical(tmp_path):
+    """The executor's two-stream schedule (independent dW / dX GEMMs of a
+    layer on the handle's auxiliary stream, cross-stream event waits, dynamic
+    tile scheduling of the GEMMs; opt-in DLVM_CONCURRENT=1) gives
+    bit-identical gradients to one stream with static tile order (the
+    default), incl. split-K dW GEMMs."""
+    import os
+    import subprocess
+    import sys
+    import paper_1711_03016_b200 as P
+    w = W.c3(256, layers=[(512, 512, "relu"), (512, 512, "relu"), (512, 256, None)])
+    sched = P.Function(w.text, w.fn, w.grad, dot_precision="bf16", flags=P.DLVM_PLAN_ONLY).print(12)
+    assert sched.startswith("streams: two") and " aux " in sched, sched
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for conc in ("1", "0"):
+        out = str(tmp_path / f"s{conc}.npz")
+        script = _STREAMS_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_CONCURRENT=conc),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        outs[conc] = np.load(out)
+    for k in outs["0"].files:
+        np.testing.assert_array_equal(outs["0"][k], outs["1"][k])
