@@ -1461,9 +1461,24 @@ struct Planner {
     g.bx = bx;
     g.by = 256 / bx;
     g.gx = (cols + bx - 1) / bx;
-    int64_t want_gy = std::max<int64_t>(1, (148 * 8) / g.gx);
+    // rows per thread cap: 64, or 128 for programs with column sums (fewer
+    // CTAs and partial rows; measured on c2, GB/s fwd / fwd+adj: cap 64
+    // 6150 / 5840, 128 6117 / 5962, 256 5963 / 5955, 32 6168 / 5629).
+    // DLVM_EW_RPT overrides.
+    bool colsum = false;
+    for (int q = 0; q < g.prog.n_reduces; ++q) colsum |= g.prog.reduce_kind[q] == RED_COL;
+    static const int rpt_env = [] {
+      const char* e = std::getenv("DLVM_EW_RPT");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int rpt_max = rpt_env > 0 ? rpt_env : (colsum ? 128 : 64);
+    static const int ctas_per_sm = [] {  // DLVM_EW_CPS: target CTAs per SM of the row grid
+      const char* e = std::getenv("DLVM_EW_CPS");
+      return e ? std::atoi(e) : 8;
+    }();
+    int64_t want_gy = std::max<int64_t>(1, (148 * (int64_t)ctas_per_sm) / g.gx);
     int64_t rpt = (R + (int64_t)g.by * want_gy - 1) / ((int64_t)g.by * want_gy);
-    g.rpt = (int)std::min<int64_t>(64, std::max<int64_t>(1, rpt));
+    g.rpt = (int)std::min<int64_t>(rpt_max, std::max<int64_t>(1, rpt));
     g.gy = (R + (int64_t)g.by * g.rpt - 1) / ((int64_t)g.by * g.rpt);
     if (g.gy > 65535) {  // tall, thin spaces: more rows per thread keep the grid's y extent legal
       g.rpt = (int)((R + (int64_t)g.by * 65535 - 1) / ((int64_t)g.by * 65535));
