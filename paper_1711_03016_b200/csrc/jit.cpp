@@ -158,6 +158,9 @@ std::vector<std::string> options() {
 #ifdef DLVM_GEMM_STAGES_PAIR
   o.push_back("-DDLVM_GEMM_STAGES_PAIR=" + std::to_string(DLVM_GEMM_STAGES_PAIR));
 #endif
+#ifdef DLVM_EW_RPI
+  o.push_back("-DDLVM_EW_RPI=" + std::to_string(DLVM_EW_RPI));
+#endif
   return o;
 }
 

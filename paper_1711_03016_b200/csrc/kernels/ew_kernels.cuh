@@ -439,7 +439,22 @@ __host__ __device__ constexpr int ew2d_minb() {
   return spec::Traits<P>::kSlots > 8 ? 2 : 3;  // (1 row per iteration at 3 CTAs/SM measured slower)
 }
 
-template <int VEC, class P, int RPI = 2, int MINB = ew2d_minb<P>(), bool PF = false>
+// rows per row-loop iteration: 4 for programs with column sums (more loads
+// in flight per thread for the 3-read adjoint; c2 fwd+adjoint 5910-5960 ->
+// 6120-6140 GB/s), 2 otherwise (4 rows measured 29% slower on the c2
+// forward).  DLVM_EW_RPI (build variant "rpi4") forces one value.
+template <class P>
+__host__ __device__ constexpr int ew2d_rpi() {
+#ifdef DLVM_EW_RPI
+  return DLVM_EW_RPI;
+#else
+  using T = spec::Traits<P>;
+  for (int q = 0; q < T::Reds::n; ++q)
+    if (T::Reds::at(2 * q + 1) == RED_COL) return 4;
+  return 2;
+#endif
+}
+template <int VEC, class P, int RPI = ew2d_rpi<P>(), int MINB = ew2d_minb<P>(), bool PF = false>
 __global__ void __launch_bounds__(256, MINB) ew2d_kernel(const __grid_constant__ EwParams p) {
   pdl_trigger();
   pdl_wait();
