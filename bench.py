@@ -286,19 +286,23 @@ OWN_KERNELS = ("gemm_tc_kernel", "gemm_simt_kernel", "ew_kernel", "ew2d_kernel",
                "finalize_kernel", "cast_bf16_kernel", "pack_bf16_kernel")
 
 
-def gemm_roofline(kb, pk, region_s):
+def gemm_roofline(kb, pk, region_s, clocks=None):
     """Tensor roofline of a step's GEMMs.  `achieved` is the DOMINANT kernel's
     algorithmic FLOP (2*M*N*K summed over K segments) / its mean CUPTI
-    duration.  Peak: the measured burst bf16 figure for timed regions under
-    2 s (they run at max clock), the sustained one for longer regions
-    (MEASURED_PEAKS.json; both fractions reported).  The GEMM class
-    (all tcgen05/SIMT dots) is reported from exclusive times."""
+    duration.  Peak: the measured burst bf16 figure when the timed region ran
+    at (near) the maximum SM clock and lasted under 2 s, else the sustained
+    one (MEASURED_PEAKS.json, measured power-capped; both fractions
+    reported).  The GEMM class (all tcgen05/SIMT dots) is reported from
+    exclusive times."""
     gemm = [r for r in kb if r["flops"] > 0]
     if not gemm:
         return None
     top = max(gemm, key=lambda r: r["ms"])
     burst, sus = pk["bf16_tflops"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    peak, kind = (burst, "burst") if region_s < 2.0 else (sus, "sustained")
+    at_max = True
+    if clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz"):
+        at_max = clocks["sm_mhz"] >= 0.9 * clocks["sm_max_mhz"]
+    peak, kind = (burst, "burst") if (region_s < 2.0 and at_max) else (sus, "sustained")
     ach = top["flops"] / (top["ms"] * 1e-3) / 1e12
     g_ms = sum(r["excl_ms"] for r in gemm)
     g_fl = sum(r["flops"] for r in gemm)
@@ -683,7 +687,7 @@ def main():
     # per-kernel breakdown: a separate short pass under CUPTI activity tracing
     # (the timed region above runs without any profiler)
     kb = kernel_breakdown(f, 1, eager_step, min(K, 5), dev)
-    roof = gemm_roofline(kb, pk, ms * K * 1e-3)
+    roof = gemm_roofline(kb, pk, ms * K * 1e-3, clocks)
     tr = ncu_traffic(w.name)
     if tr and roof:
         roof["traffic"] = tr["traffic_bytes"]
