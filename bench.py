@@ -634,7 +634,25 @@ def main():
     train_step = lambda inp: dps.step(inp, seed)
     step = lambda: train_step(dev_in)
     sgd_info = None
-    if args.workload == "c5":
+    if args.workload == "c5" and args.dp == "fused":
+        # training step with the fused reduction and the sharded update:
+        # owners update their fp32 masters and all-gather the operand copies
+        from paper_1711_03016_b200.dp import ShardedSGD
+        dps.gather = False
+        copies = [a.name.startswith("w") for a in w.args[1:-1]]
+        upd = ShardedSGD(dps, host[1:-1], copies, 1e-3, WL.sgd_ir)
+        for j in range(len(copies)):
+            dev_in[1 + j] = upd.operands[j]
+
+        def train_step(inp):
+            outs = dps.step(inp, seed)
+            upd.step()
+            return outs
+
+        step = lambda: train_step(dev_in)
+        sgd_info = {"launches": upd.sgd.num_launches(0) if upd.sgd else 0,
+                    "params": int(sum(np.prod(a.shape) for a in w.args[1:-1]))}
+    elif args.workload == "c5":
         # full training step (config 5): fwd + adjoint, gradient all-reduce, and
         # the SGD update W <- W - lr*G (an IR function through the same C ABI)
         # writing the fp32 master and the bf16 copy the next step's dots read
@@ -782,7 +800,9 @@ def main():
     if e2e:
         out["e2e"] = e2e
     if sgd_info:
-        out["config"]["step"] = "fwd+adjoint + gradient all-reduce + SGD update (lr 1e-3) of %d params" % sgd_info["params"]
+        out["config"]["step"] = ("fwd+adjoint + fused gradient reduction + sharded SGD update (lr 1e-3) + all-gather "
+                                 "of %d params" if args.dp == "fused" else
+                                 "fwd+adjoint + gradient all-reduce + SGD update (lr 1e-3) of %d params") % sgd_info["params"]
     if rank == 0 and world == 1:
         try:
             out["cpu_baseline"] = cpu_baseline_mlp(w, args.cpu_rows or (32 if w.cfg == 1 else 128))

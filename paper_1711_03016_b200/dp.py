@@ -251,3 +251,77 @@ class FusedReduceStep:
                             peer.copy_(self.views[g])
                 self._barrier()
         return self.views + self.kept
+
+
+class ShardedSGD:
+    """The update after a FusedReduceStep, sharded by gradient ownership
+    ("reduce-scatter + a 1/N-sharded SGD update +
+    all-gather of the bf16 weights").  The grad_run operands of every
+    parameter -- bf16 copies of dot operands, f32 otherwise -- live in
+    symmetric memory so owners can write every rank's copy.  The owner of a
+    parameter keeps its fp32 master (the other ranks keep none: 1/N of the
+    optimiser state per rank), updates it from the global gradient in its own
+    copy of the fused gradient buffer with the SGD IR function
+    (workloads-style `p - lr g`, one element-wise launch through the C ABI,
+    writing the master and the operand copy), then copies the operand into
+    every peer's copy (peer stores over NVLink: the all-gather); a barrier
+    closes the step.  At world size 1 this is the plain full update."""
+
+    def __init__(self, fused: "FusedReduceStep", host_params, is_dot_operand, lr: float, sgd_ir_fn):
+        import numpy as np
+        import torch
+        import torch.distributed._symmetric_memory as symm
+        from .dlvm import Function
+        self.fused, self.lr = fused, lr
+        dev = fused.device
+        shapes = fused.shapes
+        self.bf = [bool(b) for b in is_dot_operand]
+        # one symmetric buffer per operand dtype, parameters at 256-byte aligned offsets
+        self.handles, self.operands, self.offsets = {}, [None] * len(shapes), [0] * len(shapes)
+        for dt, want in ((torch.bfloat16, True), (torch.float32, False)):
+            idx = [i for i in range(len(shapes)) if self.bf[i] == want]
+            if not idx:
+                continue
+            offs, total = flat_layout([shapes[i] for i in idx], align=128)
+            buf = symm.empty(max(total, 1), dtype=dt, device=dev)
+            h = symm.rendezvous(buf, fused.group.group_name)
+            self.handles[want] = (buf, h)
+            for i, o in zip(idx, offs):
+                k = int(np.prod(shapes[i]))
+                self.offsets[i] = o
+                self.operands[i] = buf[o:o + k].view(shapes[i])
+        for i, x in enumerate(host_params):
+            self.operands[i].copy_(torch.from_numpy(np.ascontiguousarray(x)).to(dev).to(self.operands[i].dtype))
+        self.owned = [i for i in range(len(shapes)) if fused.owner[i] == fused.rank]
+        # fp32 masters of the owned parameters (f32 operands are their own masters)
+        self.masters = {}
+        for i in self.owned:
+            self.masters[i] = (torch.from_numpy(np.ascontiguousarray(host_params[i])).to(dev) if self.bf[i]
+                               else self.operands[i])
+        self.sgd = None
+        if self.owned:
+            text = sgd_ir_fn([shapes[i] for i in self.owned], lr, [self.bf[i] for i in self.owned])
+            self.sgd = Function(text, "sgd", None)
+            self.sgd_in, self.sgd_out = [], []
+            for i in self.owned:
+                self.sgd_in += [self.masters[i], fused.views[i]]
+                self.sgd_out.append(self.masters[i])
+                if self.bf[i]:
+                    self.sgd_out.append(self.operands[i])
+            self.ws = self.sgd._workspace(0, dev)
+
+    def step(self, stream=None):
+        import torch
+        f = self.fused
+        st = stream or torch.cuda.current_stream(f.device)
+        with torch.cuda.stream(st):
+            if self.sgd is not None:
+                self.sgd.run(self.sgd_in, outputs=self.sgd_out, workspace=self.ws, stream=st.cuda_stream)
+            if f.world > 1:
+                for i in self.owned:  # all-gather: the updated operand into every peer's copy
+                    buf, h = self.handles[self.bf[i]]
+                    for r in range(f.world):
+                        if r != f.rank:
+                            h.get_buffer(r, self.operands[i].shape, buf.dtype,
+                                         storage_offset=self.offsets[i]).copy_(self.operands[i])
+                f._barrier()

@@ -113,8 +113,24 @@ def _worker(rank, world, port, out):
     step = FusedReduceStep(f, 2 * len(w.layers), dev)
     outs = step.step(ins, seed)
     torch.cuda.synchronize(dev)
+    grads = [o.double().cpu().numpy() for o in outs[:-1]]
+    # sharded update + all-gather: every rank ends with the same operands
+    from paper_1711_03016_b200.dp import ShardedSGD
+    host = w.inputs(row_offset=rank * w.batch)
+    dot_op = [a.name.startswith("w") for a in w.args[1:-1]]
+    step2 = FusedReduceStep(f, 2 * len(w.layers), dev, gather=False)
+    upd = ShardedSGD(step2, host[1:-1], dot_op, 1e-3, W.sgd_ir)
+    step2.step([ins[0]] + upd.operands + [ins[-1]], seed)
+    upd.step()
+    torch.cuda.synchronize(dev)
+    ops = [o.float().cpu() for o in upd.operands]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, [o.numpy() for o in ops])
     if rank == 0:
-        out.put([o.double().cpu().numpy() for o in outs[:-1]])
+        for other in gathered[1:]:
+            for a, b in zip(gathered[0], other):
+                assert np.array_equal(a, b)
+        out.put(grads)
     dist.destroy_process_group()
 
 
@@ -139,3 +155,60 @@ def test_fused_reduce_two_ranks_equals_global_gradient():
                      dot_policy="bf16")
     for k, (g, r) in enumerate(zip(got, ref[:-1])):
         assert_normwise(g, r, what=f"fused dp grad out{k}")
+
+
+def test_sharded_sgd_training_world_size_one_equals_plain_step():
+    """Two training steps (fwd+adjoint, gradient reduction, SGD) of a small
+    tanh MLP: FusedReduceStep + ShardedSGD (owners update their fp32 masters
+    and broadcast the operand copies; at world size 1 rank 0 owns all) give
+    bit-identical weights, operand copies and losses to DataParallelStep + the
+    full SGD IR function."""
+    import torch
+    import torch.distributed as dist
+    import paper_1711_03016_b200 as P
+    from paper_1711_03016_b200.dp import DataParallelStep, FusedReduceStep, ShardedSGD
+    if not dist.is_initialized():
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(_free_port())
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    w = W._mlp_workload(5, "c5s", 256, [(512, 512, "tanh")] * 2, ("normal",), ("uniform", -0.5, 0.5),
+                        1.0 / 256, "bf16", 256)
+    dev = torch.device("cuda:0")
+    host = w.inputs()
+    n = 2 * len(w.layers)
+    dot_op = [a.name.startswith("w") for a in w.args[1:-1]]
+    f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
+    seed = torch.tensor(np.float32(w.seed()), device=dev)
+    x = torch.from_numpy(host[0]).to(dev).to(torch.bfloat16)
+    t = torch.from_numpy(host[-1]).to(dev)
+    # plain: all-reduce path (world 1) + the full SGD IR function
+    shapes = [a.shape for a in w.args[1:-1]]
+    sgd = P.Function(W.sgd_ir(shapes, 1e-3, dot_op), "sgd", None)
+    masters = [torch.from_numpy(hp).to(dev) for hp in host[1:-1]]
+    ops = [m.to(torch.bfloat16) if b else m for m, b in zip(masters, dot_op)]
+    dps = DataParallelStep(f, n, dev)
+    sgd_in, sgd_out = [], []
+    for j in range(n):
+        sgd_in += [masters[j], dps.grads.views[j]]
+        sgd_out.append(masters[j])
+        if dot_op[j]:
+            sgd_out.append(ops[j])
+    losses_a = []
+    for _ in range(2):
+        outs = dps.step([x] + ops + [t], seed)
+        losses_a.append(outs[-1].clone())
+        sgd.run(sgd_in, outputs=sgd_out)
+    # fused reduction + sharded update
+    fused = FusedReduceStep(f, n, dev, gather=False)
+    upd = ShardedSGD(fused, host[1:-1], dot_op, 1e-3, W.sgd_ir)
+    losses_b = []
+    for _ in range(2):
+        outs = fused.step([x] + upd.operands + [t], seed)
+        losses_b.append(outs[-1].clone())
+        upd.step()
+    torch.cuda.synchronize()
+    for a, b in zip(losses_a, losses_b):
+        assert torch.equal(a, b)
+    for j in range(n):
+        assert torch.equal(ops[j], upd.operands[j]), j
+        assert torch.equal(masters[j], upd.masters[j]), j
