@@ -254,7 +254,7 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog
   tp->sched = p.sched;
 #ifdef DLVM_GEMM_TRACE
   // launch k of the traced run writes slice k % slots of [slots][148][8]
-  tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * 8
+  tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * 16
                                : nullptr;
 #endif
   const int BN = p.bn;

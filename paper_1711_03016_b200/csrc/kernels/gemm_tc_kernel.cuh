@@ -95,7 +95,7 @@ struct TcParams {
   do {                                                                              \
     unsigned long long t_;                                                          \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
-    if ((P_).trace) (P_).trace[(size_t)blockIdx.x * 8 + (slot)] = t_;               \
+    if ((P_).trace) (P_).trace[(size_t)blockIdx.x * 16 + (slot)] = t_;               \
   } while (0)
 #define DLVM_SECT(var)                                                  \
   do {                                                                  \
@@ -722,6 +722,14 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
 
 constexpr int kEpiReds = 2;  // reductions per GEMM epilogue (smem budget); more -> not fused
 
+template <bool B>
+struct bool_c {
+  static constexpr bool value = B;
+};
+template <class T, bool S>
+__host__ __device__ constexpr int epi_num_stores() {
+  if constexpr (S) return T::Stores::n; else return 0;
+}
 template <class T, bool S>
 __host__ __device__ constexpr int epi_num_reds() {
   if constexpr (S) return T::Reds::n; else return kEpiReds;
@@ -1117,8 +1125,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     const uint32_t in_base = base + (uint32_t)xt.epi_off;
     const uint32_t st_base = in_base + (uint32_t)(xt.n_in_bufs * xt.in_buf_bytes) +
                              (uint32_t)(ew * xt.st_slot_bytes);  // this warp's staging region
+    // per-slot descriptors of the TMA epilogue, read from the parameter
+    // space once: input kind / storage type / buffer offset / box width
+    // (log2 of its columns), store type and staging offset
+    constexpr int NIK = SPEC && T::kIn > 0 ? T::kIn : 1;
+    constexpr int NSK = epi_num_stores<T, SPEC>() > 0 ? epi_num_stores<T, SPEC>() : 1;
+    int in_kind[NIK], in_off[NIK], in_lgc[NIK];
+    uint8_t in_st[NIK], out_st[NSK];
+    uint32_t out_off[NSK];
+    if constexpr (TMA_EPI) {
+#pragma unroll
+      for (int s2 = 0; s2 < NIK; ++s2) {
+        in_kind[s2] = s2 > 0 && staged_in ? xt.in_kind[s2] : 0;
+        in_off[s2] = xt.in_off[s2];
+        in_st[s2] = E.in[s2].st;
+        in_lgc[s2] = in_st[s2] == (uint8_t)SType::U8 ? 7 : in_st[s2] == (uint8_t)SType::BF16 ? 6 : 5;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < NSK; ++s2) {
+        out_st[s2] = E.out[s2].st;
+        out_off[s2] = st_base + (uint32_t)xt.st_off[s2];
+      }
+    }
 #ifdef DLVM_GEMM_TRACE
-    long long sect[6] = {0, 0, 0, 0, 0, 0}, sect_t0 = clock64();
+    long long sect[7] = {0, 0, 0, 0, 0, 0, 0}, sect_t0 = clock64();
 #endif
     for (int it = 0;; ++it) {
       const int t = warp_tile(it);
@@ -1181,7 +1211,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       constexpr int GCH = 64 / CW;                 // chunks per 64-column group
       constexpr int NIT = BN / CW / 2;             // chunks per warp per tile
       auto chunk_of = [&](int i) { return (h + 2 * (i / GCH)) * GCH + i % GCH; };
-      auto staged = [&](int s2) { return staged_in && xt.in_kind[s2] != 0; };
+      auto staged = [&](int s2) {
+        if constexpr (TMA_EPI) return in_kind[s2] != 0; else return false;
+      };
       // fast TMA tile: every input is staged or constant along the row
       // (column vector / scalar: loaded once per tile) -- no per-chunk
       // global loads, prefetch registers or bounds checks
@@ -1203,13 +1235,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             if (seg_vector(E.in[s2]) && !staged(s2))
               epi_row_fetch<CW>(E.in[s2], m, (int64_t)tn * BN + chunk_of(0) * CW, pf[s2 - 1]);
       }
+      // the chunk loop, compiled twice: the fast TMA tile (FAST) and the
+      // general one, so the hot loop of a fast tile is a compact body
+      // (instruction-cache footprint) without the direct-path variants
+      auto chunk_loop = [&](auto fast_c) {
+      constexpr bool FAST = decltype(fast_c)::value;
       for (int it = 0; it < NIT; ++it) {
         const int ch = chunk_of(it);
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         const int ncol = tile_full ? CW : (int)min((int64_t)CW, max((int64_t)0, g.N - n0));  // valid columns
         const bool full = mval && ncol == CW && row_vec;
         RawSeg<CW> cur[NPF];
-        if constexpr (SPEC) if (!fast) {
+        if constexpr (SPEC && !FAST) {
 #pragma unroll
           for (int s2 = 0; s2 < NPF; ++s2) cur[s2] = pf[s2];
           const int nx = it + 1 < NIT ? chunk_of(it + 1) : 0;
@@ -1232,19 +1269,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #pragma unroll
           for (int s2 = 1; s2 < T::kIn; ++s2) {
             if constexpr (TMA_EPI) {
-              if (fast && !staged(s2)) {
+              if (FAST && !staged(s2)) {
 #pragma unroll
                 for (int j = 0; j < CW; ++j) v[s2][j] = rowc[s2];
                 continue;
               }
               if (staged(s2)) {
-                if (xt.in_kind[s2] == 1) {  // [M, N]: row 32q+lane, columns ch*16.. of the tile
-                  const int ic = xt.in_cols[s2], col = ch * CW;
-                  const int es = 128 / ic;
-                  box_read16(in_buf + xt.in_off[s2] + (col / ic) * (BM * 128), 32 * q + lane, ((col % ic) * es) >> 4,
-                             E.in[s2].st, reinterpret_cast<float*>(v[s2]));
+                if (in_kind[s2] == 1) {  // [M, N]: row 32q+lane, columns ch*16.. of the tile
+                  const int col = ch * CW, lg = in_lgc[s2];  // boxes of 2^lg columns (128-byte rows)
+                  box_read16(in_buf + in_off[s2] + (col >> lg) * (BM * 128), 32 * q + lane,
+                             ((col & ((1 << lg) - 1)) << (7 - lg)) >> 4, in_st[s2], reinterpret_cast<float*>(v[s2]));
                 } else {  // [1, N] row vector: the chunk's 16 values, same for every lane
-                  const uint32_t a0 = in_buf + xt.in_off[s2] + ch * 64;
+                  const uint32_t a0 = in_buf + in_off[s2] + ch * 64;
 #pragma unroll
                   for (int c = 0; c < 4; ++c) {
                     const uint4 x = lds128(a0 + 16 * c);
@@ -1255,28 +1291,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                 continue;
               }
             }
-            if (full && seg_vector(E.in[s2]))
-              epi_row_decode<CW>(E.in[s2], cur[s2 - 1], v[s2]);
-            else
-              epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+            if constexpr (!FAST) {
+              if (full && seg_vector(E.in[s2]))
+                epi_row_decode<CW>(E.in[s2], cur[s2 - 1], v[s2]);
+              else
+                epi_row_load<CW>(E.in[s2], m, n0, mval ? ncol : 0, full, v[s2]);
+            }
           }
           DLVM_SECT(sect[2]);  // inputs
           T::template exec<CW>(v);
           DLVM_SECT(sect[3]);  // program
-          if (tma_on) {
+          if (FAST || tma_on) {
             if constexpr (TMA_EPI) {
               // stage this chunk into the warp's 32 x 64 group boxes; the
               // group's first chunk waits until the TMA has read the
               // previous group, its last one hands the boxes to TMA
               const int gi = it % GCH;
               if (gi == 0) {
+                DLVM_SECT(sect[4]);
                 if (lane == 0) bulk_wait_read<0>();
                 __syncwarp();
+                DLVM_SECT(sect[6]);  // waiting for the staging to be read
               }
 #pragma unroll
               for (int s2 = 0; s2 < T::Stores::n; ++s2)
-                grp_write16(st_base + xt.st_off[s2], lane, gi, (s2 == 0 ? out0 : E.out[s2]).st,
-                            reinterpret_cast<const float*>(v[T::Stores::at(s2)]), T::is01(T::Stores::at(s2)));
+                grp_write16(out_off[s2], lane, gi, out_st[s2], reinterpret_cast<const float*>(v[T::Stores::at(s2)]),
+                            T::is01(T::Stores::at(s2)));
               if (gi == GCH - 1) {
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -1285,8 +1325,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                   const int32_t c0 = (int32_t)((int64_t)tn * BN + (ch - gi) * CW);  // the group's first column
 #pragma unroll
                   for (int s2 = 0; s2 < T::Stores::n; ++s2) {
-                    const uint32_t b = st_base + xt.st_off[s2];
-                    const bool f32 = (s2 == 0 ? out0 : E.out[s2]).st == (uint8_t)SType::F32;
+                    const uint32_t b = out_off[s2];
+                    const bool f32 = out_st[s2] == (uint8_t)SType::F32;
                     if (s2 == 0 && xt.split3d) {
                       tma_store_3d(&P.tma_st[0], b, c0, r0, split);
                       tma_store_3d(&P.tma_st[0], b + 4096, c0 + 32, r0, split);
@@ -1299,7 +1339,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                 }
               }
             }
-          } else {
+          } else if constexpr (!FAST) {
 #pragma unroll
             for (int s2 = 0; s2 < T::Stores::n; ++s2)
               epi_row_store<CW>(s2 == 0 ? out0 : E.out[s2], m, n0, mval ? ncol : 0, full, v[T::Stores::at(s2)]);
@@ -1337,6 +1377,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         }
         DLVM_SECT(sect[5]);  // reductions
       }
+      };
+      if (fast) chunk_loop(bool_c<true>{}); else chunk_loop(bool_c<false>{});
       // this warp is done with the tile's staged inputs
       if (staged_in) {
         __syncwarp();
@@ -1395,13 +1437,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     if (tma_on && lane == 0) bulk_wait_all();  // this warp's TMA stores are complete
     if (ew == 0 && lane == 0) DLVM_GT(P, 6);
 #ifdef DLVM_GEMM_TRACE
-    // epilogue section cycles of warp 4 (DLVM_EPI_DBG & 8): slots 0..4 =
-    // reductions, TMEM loads, inputs, program, stores
+    // epilogue section cycles of warp 4 (DLVM_EPI_DBG & 8): slots 8..14 =
+    // loop overhead, TMEM loads, inputs, program, stores, reductions, staging waits
     if ((xt.dbg & 8) && ew == 0 && lane == 0 && P.trace) {
       long long c_ = clock64();
       (void)c_;
-      P.trace[(size_t)blockIdx.x * 8 + 0] = (unsigned long long)sect[5];
-      for (int k = 1; k < 5; ++k) P.trace[(size_t)blockIdx.x * 8 + k] = (unsigned long long)sect[k];
+      for (int k = 0; k < 7; ++k) P.trace[(size_t)blockIdx.x * 16 + 8 + k] = (unsigned long long)sect[k];
     }
 #endif
   }

@@ -42,7 +42,7 @@ def main():
     G = len(gemms)
     L = P.dlvm.lib()
     L.dlvm_debug_gemm_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    buf = torch.zeros(G * 148 * 8, dtype=torch.int64, device=dev)
+    buf = torch.zeros(G * 148 * 16, dtype=torch.int64, device=dev)
     for _ in range(5):
         f.grad_run(ins, seed=seed, outputs=outs, workspace=ws)
     torch.cuda.synchronize()
@@ -52,7 +52,7 @@ def main():
         f.grad_run(ins, seed=seed, outputs=outs, workspace=ws)
         torch.cuda.synchronize()
         L.dlvm_debug_gemm_trace(None, 1)
-    t = buf.cpu().numpy().reshape(G, 148, 8).astype(np.float64)
+    t = buf.cpu().numpy().reshape(G, 148, 16).astype(np.float64)
     t0 = t[t > 0].min()
     prev_exit = None
     print(f"{'gemm':60s} " + " ".join(f"{n:>8s}" for n in NAMES) + f" {'last_exit':>9s} {'gap':>6s}")
