@@ -1441,3 +1441,46 @@ def test_two_stream_schedule_bit_identical(tmp_path):
         outs[conc] = np.load(out)
     for k in outs["0"].files:
         np.testing.assert_array_equal(outs["0"][k], outs["1"][k])
+
+
+_TMA_EPI_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+outs = []
+cases = [
+    (W.c3(200, layers=[(136, 264, "relu"), (264, 72, None)]), "bf16"),      # ragged M and N, mask input
+    (W.c3(384, layers=[(256, 1000, "relu"), (1000, 100, None)]), "bf16"),   # N = 1000 (bias N % 4 == 0), 128-wide tiles
+    (W._mlp_workload(5, "c5t", 320, [(256, 260, "tanh"), (260, 260, "tanh")], ("normal",), ("uniform", -0.5, 0.5),
+                     1.0 / 320, "bf16", 320), "bf16"),                        # f32 saved-activation input, N % 4 == 0
+    (W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)]), "bf16"),    # split-K dW (3-D partial stores)
+    (W.ce_mlp(256, layers=[(256, 256, "relu"), (256, 100, None)]), "bf16"),  # softmax-CE loss epilogue
+]
+for w, prec in cases:
+    r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision=prec)
+    outs += r["primal"] + r["grad"]
+np.savez({out!r}, *outs)
+"""
+
+
+def test_tma_epilogue_bit_identical_to_direct_stores(tmp_path):
+    """The TMA epilogue (staged stores and inputs, 64-column warp groups,
+    fast-tile loop) computes the same values in the same summation orders as
+    the direct row-per-lane epilogue (DLVM_GEMM_TMA_EPI=0): bit-identical
+    losses and gradients over ragged tiles, mask / saved-activation / bias
+    inputs, split-K partial stores and the softmax-CE loss."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for on in ("1", "0"):
+        out = str(tmp_path / f"e{on}.npz")
+        script = _TMA_EPI_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_GEMM_TMA_EPI=on),
+                           capture_output=True, text=True, timeout=900)
+        assert p.returncode == 0, p.stderr[-3000:]
+        outs[on] = np.load(out)
+    for k in outs["0"].files:
+        np.testing.assert_array_equal(outs["0"][k], outs["1"][k], err_msg=k)
