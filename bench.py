@@ -266,6 +266,13 @@ def kernel_breakdown(f, which, step, K, dev):
     return out
 
 
+def launched(kb):
+    """Kernels a step really launches: the plan's launches minus the optional
+    ones CUPTI saw skipped (a bf16 cast of bf16 input, a K-split sum step the
+    GEMM made redundant by adding into an f32 home)."""
+    return sum(1 for r in kb if r.get("kernel") != "(not launched)")
+
+
 def kernel_kind(desc):
     """Kernel-name fragments a plan launch with this description runs as."""
     if desc.startswith("gemm tcgen05"):
@@ -444,7 +451,7 @@ def bench_grad_leg(w, small, dev, K, W_, bf16_args, cpu_rows):
     out = {"workload": w.name, "value": round(w.global_batch / (ms * 1e-3), 1), "unit": "samples/s",
            "ms_per_step": round(ms, 4), "step_tflops": round(flops / (ms * 1e-3) / 1e12, 1),
            "step_frac_of_burst": round(flops / (ms * 1e-3) / 1e12 / pk["bf16_tflops"], 4),
-           "launches": f.num_launches(1), "roofline": gemm_roofline(kb, pk, ms * K * 1e-3)}
+           "launches": launched(kb), "roofline": gemm_roofline(kb, pk, ms * K * 1e-3)}
     detail = [dict(r, desc=r["desc"][:110]) for r in kb]
     try:
         cores = oracle_threads()
@@ -712,7 +719,7 @@ def main():
         roof["traffic_kernel"] = tr["kernel"]
         roof["traffic_source"] = tr["source"]
     step_flops = sum(r["flops"] for r in kb)
-    launches = (f.num_launches(1) + (sgd_info["launches"] if sgd_info else 0)) * K
+    launches = (launched(kb) + (sgd_info["launches"] if sgd_info else 0)) * K
     detail = {"n_gpus": world, "workload": w.name,
               "kernels": [{"desc": r["desc"][:120], "kernel": r.get("kernel"), "ms": round(r["ms"], 4),
                            "excl_ms": round(r["excl_ms"], 4), "flops": r["flops"], "bytes": r["bytes"],

@@ -446,6 +446,11 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
     if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   }
   bool aux_used = false;
+  static const bool split_red_env = [] {
+    const char* e = std::getenv("DLVM_GEMM_SPLITRED");
+    return !(e && e[0] == '0');
+  }();
+  int red_skip = -1;
   for (size_t si = 0; si < P.steps.size(); ++si) {
     const Step& st = P.steps[si];
     void* const jf = si < jit.size() ? jit[si] : nullptr;
@@ -457,8 +462,17 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         if ((e = cudaStreamWaitEvent(stream, fn->events[w], 0)) != cudaSuccess)
           return fail(DLVM_ERR_CUDA, std::string("cudaStreamWaitEvent: ") + cudaGetErrorString(e));
     }
-    if (st.kind == Step::EW && st.ew.finalize && st.ew.direct_buf >= 0 && b.st[st.ew.direct_buf] == (uint8_t)SType::F32)
-      continue;  // the producer wrote the single partial into the f32 home
+    // steps with nothing to do in this binding: a finalize whose producer
+    // wrote the single partial into the f32 home, and the sum of K-split
+    // partials that the GEMM added into the f32 home itself (split_red)
+    if ((st.kind == Step::EW && st.ew.finalize && st.ew.direct_buf >= 0 && b.st[st.ew.direct_buf] == (uint8_t)SType::F32) ||
+        (int)si == red_skip) {
+      if (st.counted_launch() && (e = mark(li++)) != cudaSuccess)  // an empty interval keeps the events aligned
+        return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+      if (conc && fn->step_signals[which][si] && (e = cudaEventRecord(fn->events[si], stream)) != cudaSuccess)
+        return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
+      continue;
+    }
     if (st.counted_launch() && (e = mark(li++)) != cudaSuccess)
       return fail(DLVM_ERR_CUDA, std::string("cudaEventRecord: ") + cudaGetErrorString(e));
     // one NVTX range per launch group, named by the plan step
@@ -525,6 +539,19 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
         gp.pf_row_bytes[gp.n_pf] = r.s[0] * es;
         gp.pf_esize[gp.n_pf] = es;
         ++gp.n_pf;
+      }
+      // K split in two with a store-only sum step after it, whose home is
+      // bound as f32: zero the home and let both splits add into it
+      if (g.split_red_ok && split_red_env && g.tensor_core && aligned && gp.bf16 && si + 1 < P.steps.size() &&
+          P.steps[si + 1].kind == Step::EW && b.st[P.steps[si + 1].ew.stores[0].buf] == (uint8_t)SType::F32) {
+        EwParams np;
+        to_dev(P.steps[si + 1].ew, b, &np);
+        gp.epi.out[0] = np.out[0];
+        gp.epi.vec = epi_vec(gp.epi);
+        gp.split_red = 1;
+        e = cudaMemset2DAsync(np.out[0].ptr, (size_t)np.out[0].s[0] * 4, 0, (size_t)g.N * 4, (size_t)g.M, stream);
+        if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaMemset2DAsync: ") + cudaGetErrorString(e));
+        red_skip = (int)si + 1;
       }
       if (g.tensor_core && aligned && gp.bf16) {
         GemmLaunchFn sf = fn->specialize ? find_gemm_spec(g.epi.sig.c_str(), g.bn) : nullptr;

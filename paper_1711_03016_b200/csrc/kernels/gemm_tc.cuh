@@ -164,7 +164,7 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
     const EwDevOut& r = E.out[o];
     const int es = es_of(r.st);
     if (r.s[1] != 1 || r.st == (uint8_t)SType::F32_ADD) return;  // accumulated outputs: direct red path
-    const bool split = o == 0 && p.ksplit > 1;
+    const bool split = o == 0 && p.ksplit > 1 && !p.split_red;
     if (!encode_epi(&tp->tma_st[o], r.ptr, r.st, p.N, p.M, r.s[0] * es, es == 4 ? 32 : 64, 32,
                     split ? p.ksplit : 0, split ? p.split_bytes : 0))
       return;
@@ -172,7 +172,8 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
     et.st_off[o] = off;
     off += es == 4 ? 8192 : es == 2 ? 4096 : 2048;
   }
-  et.split3d = p.ksplit > 1;
+  et.split3d = p.ksplit > 1 && !p.split_red;
+  et.red0 = p.split_red && p.ksplit > 1;
   et.st_slot_bytes = round_up(off, 1024);
   // staged inputs: [M, N] rows (kind 1: boxes of 128 rows x 128 bytes) and
   // [1, N] f32 row vectors (kind 2)
@@ -311,6 +312,11 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog
     }
   }
   setup_tma_epilogue(p, tp, ctas, spec_prog);
+  if (p.split_red && p.ksplit > 1) {
+    if (p.epi.prog.n_stores != 1 || p.epi.out[0].st != (uint8_t)SType::F32) return false;
+    tp->g.split_bytes = 0;  // every split addresses the one output
+    if (!tp->et.on) tp->g.epi.out[0].st = (uint8_t)SType::F32_ADD;  // direct stores: red.global.add
+  }
   return true;
 }
 

@@ -66,6 +66,7 @@ struct EpiTma {
   int32_t st_off[kMaxStores];   // byte offset of store o in a warp's staging region
   int32_t st_slot_bytes;        // one warp's staging region (one 32 x 64 group of every store)
   int32_t split3d;              // store 0 is the split-K partial: 3-D map {N, M, S}
+  int32_t red0;                 // store 0 adds into its (zeroed) home: TMA reduce-add, no partials
   int32_t epi_off;              // byte offset of the staging region from the aligned base
   int32_t dbg;                  // DLVM_EPI_DBG & 8 (trace builds): per-section cycles of epilogue warp 4
 };
@@ -200,6 +201,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
                "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+// smem -> global element-wise f32 add (performed at L2; the K-split work
+// items of a tile add their accumulators into one zeroed output)
+__device__ __forceinline__ void tma_red_add_2d(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -1330,6 +1339,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
                     if (s2 == 0 && xt.split3d) {
                       tma_store_3d(&P.tma_st[0], b, c0, r0, split);
                       tma_store_3d(&P.tma_st[0], b + 4096, c0 + 32, r0, split);
+                    } else if (s2 == 0 && xt.red0) {
+                      tma_red_add_2d(&P.tma_st[0], b, c0, r0);
+                      tma_red_add_2d(&P.tma_st[0], b + 4096, c0 + 32, r0);
                     } else {
                       tma_store_2d(&P.tma_st[s2], b, c0, r0);
                       if (f32) tma_store_2d(&P.tma_st[s2], b + 4096, c0 + 32, r0);

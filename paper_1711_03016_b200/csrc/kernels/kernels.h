@@ -73,6 +73,10 @@ struct GemmParams {
   // output at + split * split_bytes (a following EW step sums the splits)
   int32_t ksplit;
   int64_t split_bytes;
+  // split_red: instead, every work item adds its accumulator into out[0] (f32,
+  // zeroed by the caller; program: store of the accumulator only), by TMA
+  // reduce-add, else by red.global.add (SType::F32_ADD); split_bytes unused
+  int32_t split_red;
   int* sched;                // tcgen05: zeroed work counter (dynamic tile scheduling) or nullptr
   int32_t n_pf;
   const void* pf_ptr[4];

@@ -1833,6 +1833,11 @@ struct Planner {
       gm.epi = st;
       gm.ksplit = S;
       gm.split_bytes = gm.M * gm.N * 4;
+      const EwProgram& sp = split_ew.prog;
+      gm.split_red_ok = S == 2 && sp.n_ins == 0 && sp.n_lits == 0 && sp.n_in == 1 && sp.n_stores == 1 &&
+                        sp.n_reduces == 0 && sp.store_slot[0] == 0 && split_ew.stores.size() == 1 &&
+                        split_ew.stores[0].buf >= 0 && split_ew.stores[0].strides[1] == 1 &&
+                        split_ew.stores[0].strides[0] == gm.N;
     }
     std::ostringstream d;
     d << (gm.tensor_core ? "gemm tcgen05 bf16" : (bf ? "gemm simt bf16" : "gemm simt f32")) << " %"
@@ -1866,6 +1871,7 @@ struct Planner {
       de << "ew [" << gm.M << "," << gm.N << "] vec" << split_ew.vec << " sum of " << S << " K-split partials of %"
          << f.names[dv] << " + epilogue ops=" << (int)split_ew.prog.n_ins << " stores=" << (int)split_ew.prog.n_stores
          << " reductions=" << (int)split_ew.prog.n_reduces;
+      if (gm.split_red_ok) de << " (skipped when the home is bound as f32: the GEMM adds the splits into it)";
       e.desc = de.str();
       e.ew.desc = e.desc;
       plan.steps.push_back(e);

@@ -103,6 +103,13 @@ struct GemmStep {
   bool tensor_core = false;      // tcgen05 (bf16) vs SIMT (f32/bf16 operands)
   int ksplit = 1;                // > 1: K split into raw partial tiles, summed by the next EW step
   int64_t split_bytes = 0;       // byte stride between the partial tiles
+  // ksplit == 2 and the next EW step only stores the sum of the partials
+  // into a home with unit column stride: when that home is bound as f32 at
+  // run time, the executor zeroes it and the GEMM adds both splits into it
+  // (GemmParams::split_red), skipping the partials and the EW step.
+  // 0 + a + b rounds once per add in either order: fl(a + b), bit-identical
+  // to the EW step's partial0 + partial1 (DLVM_GEMM_SPLITRED=0 disables)
+  bool split_red_ok = false;
   int bm = 128, bn = 128;        // tile shape (partials layout of epilogue reductions)
   EwGroup epi;                   // iteration space [M, N]; input slot 0 = accumulator
   int sched_index = -1;          // tcgen05: this GEMM's work counter in Plan::sched_buf (dynamic scheduling)

@@ -514,6 +514,10 @@ def test_planner_layout_heuristics():
     assert "pack %" not in c3.print(3)                                         # batch 1024: no padded weight copy
     c4 = _plan_only(W.c4().text, W.c4().fn, W.c4().grad, "bf16")
     assert "pack %w3 to bf16 rows of 1024" in c4.print(3)                      # batch 65536: padded copy
+    # dW GEMMs with K = 65536 split in two: the sum steps are optional (the
+    # GEMM adds both splits into an f32-bound home)
+    sums = [l for l in c4.print(3).splitlines() if "sum of 2 K-split partials" in l]
+    assert len(sums) == 2 and all("skipped when the home is bound as f32" in l for l in sums), sums
     # a [2, 96] reduction result (rank 2, last dim 96 -> would pad to 128): unpadded, 768 bytes
     t = ('module "m"\nstage raw\nfunc @f: (<2 x 50 x 96 x f32>) -> <2 x 96 x f32> {\n'
          "'entry(%x: <2 x 50 x 96 x f32>):\n    %t = tanh %x: <2 x 50 x 96 x f32>\n"

@@ -1484,3 +1484,52 @@ def test_tma_epilogue_bit_identical_to_direct_stores(tmp_path):
         outs[on] = np.load(out)
     for k in outs["0"].files:
         np.testing.assert_array_equal(outs["0"][k], outs["1"][k], err_msg=k)
+
+
+_SPLIT_RED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+from torch.profiler import ProfilerActivity, profile
+outs, n_ew = [], 0
+cases = [
+    W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)]),    # dW GEMMs with K = 8192 split in two
+    W.c3(8192, layers=[(264, 520, "relu"), (520, 136, None)]),    # ragged tiles
+]
+for w in cases:
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16", which="grad")
+        torch.cuda.synchronize()
+    n_ew += sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "ew" in e.name and "gemm" not in e.name)
+    outs += r["grad"]
+np.savez({out!r}, *outs, n_ew=np.int64(n_ew))
+"""
+
+
+def test_split_k_reduce_add_bit_identical_to_partials(tmp_path):
+    """A GEMM whose K is split in two and whose output is bound as f32 adds
+    both splits into the zeroed output (TMA reduce-add; red.global.add with
+    the direct epilogue) instead of storing partials for a sum step: 0 + a + b
+    rounds to fl(a + b) in either order, so the gradients are bit-identical
+    to the partials + sum-step path (DLVM_GEMM_SPLITRED=0), and the sum
+    steps' EW launches are gone."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for red, tma in (("0", "1"), ("1", "1"), ("1", "0")):
+        out = str(tmp_path / f"r{red}{tma}.npz")
+        script = _SPLIT_RED_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script],
+                           env=dict(os.environ, DLVM_GEMM_SPLITRED=red, DLVM_GEMM_TMA_EPI=tma),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        outs[red + tma] = np.load(out)
+    ref = outs["01"]
+    for key in ("11", "10"):
+        for k in ref.files:
+            if k != "n_ew":
+                np.testing.assert_array_equal(outs[key][k], ref[k], err_msg=f"{key} {k}")
+        assert int(outs[key]["n_ew"]) < int(ref["n_ew"]), (key, int(outs[key]["n_ew"]), int(ref["n_ew"]))
