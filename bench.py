@@ -178,6 +178,41 @@ def time_steps(step, K, dev, world, group=None):
     return ms
 
 
+class _Rec:
+    """One kernel activity record (name, start ns, duration ns, stream)."""
+
+    def __init__(self, name, start, dur, stream):
+        self.name, self.start, self.dur, self.stream = name, start, dur, stream
+        self.parts = 1  # kernels folded into this record (a hybrid GEMM: 2)
+
+
+def _merge_hybrid(ks):
+    """A hybrid GEMM launch is two kernels: multicast clusters on the
+    caller's stream and CTA pairs on an auxiliary stream (gemm_tc.cuh
+    launch_hybrid).  Each GEMM kernel off the main stream (the stream most
+    kernels ran on) is folded into the main-stream GEMM kernel it overlaps,
+    which then spans both; the result is sorted by start time."""
+    if not ks:
+        return ks
+    streams = [k.stream for k in ks]
+    main = max(set(streams), key=streams.count)
+    mains = sorted([k for k in ks if k.stream == main], key=lambda k: k.start)
+    for c in (k for k in ks if k.stream != main):
+        best, ov = None, 0
+        for m in mains:
+            o = min(m.start + m.dur, c.start + c.dur) - max(m.start, c.start)
+            if "gemm_tc" in m.name and o > ov:
+                best, ov = m, o
+        if best is None:
+            mains.append(c)  # not a companion: keep it as a launch of its own
+            continue
+        end = max(best.start + best.dur, c.start + c.dur)
+        best.start = min(best.start, c.start)
+        best.dur = end - best.start
+        best.parts += c.parts
+    return sorted(mains, key=lambda k: k.start)
+
+
 def kernel_breakdown(f, which, step, K, dev):
     """Per-launch device times of K steps from CUPTI kernel activity records
     (torch.profiler / kineto), which -- unlike CUDA events recorded between
@@ -199,9 +234,10 @@ def kernel_breakdown(f, which, step, K, dev):
             for _ in range(K + 1):  # the first step primes the tracer (its first kernel can be missed)
                 step()
             torch.cuda.synchronize(dev)
-        ks = [e for e in prof.profiler.kineto_results.events()
+        ks = [_Rec(e.name(), e.start_ns(), e.duration_ns(), e.device_resource_id())
+              for e in prof.profiler.kineto_results.events()
               if e.device_type() == DeviceType.CUDA and any(k in e.name() for k in OWN_KERNELS)]
-        ks.sort(key=lambda e: e.start_ns())
+        ks = _merge_hybrid(ks)
         # match the plan's launches to the recorded kernels by kind, walking
         # back from the last step (a kernel the plan does not count -- e.g.
         # a conditional finalize -- is skipped instead of shifting the rest)
@@ -211,10 +247,10 @@ def kernel_breakdown(f, which, step, K, dev):
         for _ in range(K):
             step_k = []
             for i in reversed(range(n)):
-                if optional[i] and (j < 0 or not any(frag in ks[j].name() for frag in want[i])):
+                if optional[i] and (j < 0 or not any(frag in ks[j].name for frag in want[i])):
                     step_k.append(None)  # e.g. a cast skipped because the input came as bf16
                     continue
-                while j >= 0 and not any(frag in ks[j].name() for frag in want[i]):
+                while j >= 0 and not any(frag in ks[j].name for frag in want[i]):
                     j -= 1
                 if j < 0:
                     raise RuntimeError(f"CUPTI kernels do not match the plan (launch {i}: {want[i]})")
@@ -225,6 +261,7 @@ def kernel_breakdown(f, which, step, K, dev):
         if len(ks) == K * n:
             dur = [[0.0] * K for _ in range(n)]
             exc = [[0.0] * K for _ in range(n)]
+            parts = [0] * n
             names = [""] * n
             last_end = None
             for j, e in enumerate(ks):
@@ -232,16 +269,18 @@ def kernel_breakdown(f, which, step, K, dev):
                 if e is None:
                     names[i] = "(not launched)"
                     continue
-                s0, e0 = e.start_ns(), e.start_ns() + e.duration_ns()
-                dur[i][k] = e.duration_ns() * 1e-6
+                s0, e0 = e.start, e.start + e.dur
+                dur[i][k] = e.dur * 1e-6
+                parts[i] = max(parts[i], e.parts)
                 exc[i][k] = max(0, e0 - (s0 if last_end is None else max(s0, last_end))) * 1e-6
                 last_end = e0 if last_end is None else max(last_end, e0)
-                names[i] = e.name()
+                names[i] = e.name
             out = []
             for i in range(n):
                 desc, flops, nbytes = f.launch_info(which, i)
                 out.append({"desc": desc, "kernel": names[i][:60], "ms": statistics.mean(dur[i]),
-                            "excl_ms": statistics.mean(exc[i]), "flops": flops, "bytes": nbytes, "timing": "cupti"})
+                            "excl_ms": statistics.mean(exc[i]), "flops": flops, "bytes": nbytes, "timing": "cupti",
+                            "kernels": parts[i]})
     except Exception as ex:  # noqa: BLE001
         out = None
         why = repr(ex)[:200]
@@ -269,8 +308,9 @@ def kernel_breakdown(f, which, step, K, dev):
 def launched(kb):
     """Kernels a step really launches: the plan's launches minus the optional
     ones CUPTI saw skipped (a bf16 cast of bf16 input, a K-split sum step the
-    GEMM made redundant by adding into an f32 home)."""
-    return sum(1 for r in kb if r.get("kernel") != "(not launched)")
+    GEMM made redundant by adding into an f32 home), counting both kernels of
+    a hybrid GEMM launch."""
+    return sum(r.get("kernels", 1) for r in kb if r.get("kernel") != "(not launched)")
 
 
 def kernel_kind(desc):
@@ -723,7 +763,7 @@ def main():
     detail = {"n_gpus": world, "workload": w.name,
               "kernels": [{"desc": r["desc"][:120], "kernel": r.get("kernel"), "ms": round(r["ms"], 4),
                            "excl_ms": round(r["excl_ms"], 4), "flops": r["flops"], "bytes": r["bytes"],
-                           "timing": r["timing"]} for r in kb]}
+                           "timing": r["timing"], "kernels": r.get("kernels", 1)} for r in kb]}
 
     def e2e_leg(f32_inputs: bool):
         """End to end through the public API: every step copies its own batch

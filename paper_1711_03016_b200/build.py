@@ -20,7 +20,8 @@ VARIANT = os.environ.get("DLVM_BUILD_VARIANT", "")
 OUT = os.path.join(PKG, "libdlvm.so" if not VARIANT else f"libdlvm_{VARIANT}.so")
 OBJ = os.path.join(PKG, "build" if not VARIANT else f"build_{VARIANT}")
 VARIANT_FLAGS = {"": [], "trace": ["-DDLVM_GEMM_TRACE"], "s4": ["-DDLVM_GEMM_STAGES_PAIR=4"],
-                 "s5": ["-DDLVM_GEMM_STAGES_PAIR=5"], "rpi4": ["-DDLVM_EW_RPI=4"]}[VARIANT]
+                 "s5": ["-DDLVM_GEMM_STAGES_PAIR=5"], "rpi4": ["-DDLVM_EW_RPI=4"],
+                 "probe": ["-DDLVM_PROBE_SKIP_B"]}[VARIANT]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

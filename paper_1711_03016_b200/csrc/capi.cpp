@@ -441,8 +441,9 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
   // dynamic tile scheduling (DLVM_GEMM_DYN=1, or every GEMM of a two-stream
   // run): the work counters live in the workspace and start at zero
   const bool dyn = (dyn_env || conc) && P.sched_buf >= 0;
-  if (dyn) {
-    cudaError_t e = cudaMemsetAsync(b.ptr[P.sched_buf], 0, (size_t)P.n_sched * 4, stream_main);
+  const bool hyb = !dyn && P.hybrid_counters && P.sched_buf >= 0 && gemm_hybrid_enabled();  // multicast + pair
+  if (dyn || hyb) {
+    cudaError_t e = cudaMemsetAsync(b.ptr[P.sched_buf], 0, (size_t)P.n_sched * 8, stream_main);
     if (e != cudaSuccess) return fail(DLVM_ERR_CUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   }
   bool aux_used = false;
@@ -518,7 +519,8 @@ dlvm_status execute(dlvm_fn fn, int which, const dlvm_tensor* in, int n_in, cons
       gp.bm = g.bm;
       gp.bn = g.bn;
       gp.ksplit = g.ksplit;
-      gp.sched = dyn && g.sched_index >= 0 ? static_cast<int*>(b.ptr[P.sched_buf]) + g.sched_index : nullptr;
+      gp.sched = dyn && g.sched_index >= 0 ? static_cast<int*>(b.ptr[P.sched_buf]) + 2 * g.sched_index : nullptr;
+      gp.hyb = hyb && g.sched_index >= 0 ? static_cast<int*>(b.ptr[P.sched_buf]) + 2 * g.sched_index : nullptr;
       gp.split_bytes = g.split_bytes;
       to_dev(g.epi, b, &gp.epi);
       gp.epi.vec = epi_vec(gp.epi);

@@ -27,6 +27,8 @@ cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream) {
   return launch_prog<128, VmEpi<4>>(p, stream);
 }
 
+bool gemm_hybrid_enabled() { return mc_mode() == 1; }
+
 int gemm_tc_ctas(int64_t M, int bn) {
   GemmParams p;
   std::memset(&p, 0, sizeof(p));
@@ -39,9 +41,9 @@ cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStrea
   TcParams tp;
   if (!make_params(p, &tp, ctas, true)) return cudaErrorInvalidValue;  // NVRTC kernels run compile-time programs
   const int smem = launch_smem(tp, p.bn, ctas);
-  const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);  // work items (tile x K split)
-  const int grid = ctas * std::min(items, num_sms() / ctas);
-  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), smem, stream, (unsigned)ctas, 1);
+  int cluster = 1, grid = 1;
+  grid_of(tp, ctas, &cluster, &grid);
+  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), smem, stream, (unsigned)cluster, 1);
   void* args[] = {&tp};
   return launch_jit(fn, L, args);
 }
@@ -69,7 +71,7 @@ int num_gemm_specs() {
 #ifdef DLVM_GEMM_TRACE
 // Trace builds only (not part of dlvm.h): tcgen05 GEMM launches k = 0, 1, ...
 // after this call write their phase stamps to slice k % slots of `dev`
-// ([slots][148][8] u64, caller-owned device memory); NULL stops tracing.
+// ([slots][148][32] u64, caller-owned device memory); NULL stops tracing.
 // Used by tools/gemm_trace.py.
 namespace dlvm {
 namespace kern {

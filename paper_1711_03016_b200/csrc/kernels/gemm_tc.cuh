@@ -124,6 +124,48 @@ bool encode_epi(CUtensorMap* map, const void* ptr, uint8_t st, int64_t cols, int
   return r == CUDA_SUCCESS;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// 4-CTA clusters that can be resident at once with one CTA per SM (GPCs
+// whose SM count is not a multiple of 4 leave SMs over); 0 if unknown
+__global__ void mc_probe_kernel() {}
+int max_clusters4() {
+  static const int n = [] {
+    if (cudaFuncSetAttribute(mc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * 64, 1, 1);
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = kMaxDynSmem;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 4;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, (const void*)mc_probe_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    return c;
+  }();
+  return n;
+}
+
 // TMA epilogue set-up (see EpiTma): stores, staged inputs, stage count.
 // `spec_prog`: the kernel runs a compile-time program (ahead-of-time or
 // NVRTC), whose chunk width follows from its slot count.
@@ -137,10 +179,11 @@ void setup_tma_epilogue(const GemmParams& p, TcParams* tp, int ctas, bool spec_p
   }();
   if (verbose) {
     const EpiTma& et = tp->et;
-    fprintf(stderr, "dlvm gemm M=%lld N=%lld bn=%d ctas=%d spec=%d slots=%d stores=%d: tma_epi=%d nst=%d in_bufs=%d "
-            "in_buf=%d st_region=%d\n", (long long)p.M, (long long)p.N, p.bn, ctas, (int)spec_prog,
+    fprintf(stderr, "dlvm gemm M=%lld N=%lld bn=%d ctas=%d mc=%d sup=%d spec=%d slots=%d stores=%d: tma_epi=%d "
+            "nst=%d in_bufs=%d in_buf=%d st_region=%d clusters4=%d\n", (long long)p.M, (long long)p.N, p.bn, ctas,
+            tp->mc, tp->super_items, (int)spec_prog,
             p.epi.prog.n_in + p.epi.prog.n_lits + p.epi.prog.n_ins, p.epi.prog.n_stores, et.on, et.nst,
-            et.n_in_bufs, et.in_buf_bytes, et.st_slot_bytes);
+            et.n_in_bufs, et.in_buf_bytes, et.st_slot_bytes, max_clusters4());
   }
 }
 
@@ -238,24 +281,57 @@ void setup_tma_epilogue_impl(const GemmParams& p, TcParams* tp, int ctas, bool s
   }
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+// Multicast clusters (DLVM_GEMM_MC: 0 off (default), 1 hybrid, 2 alone):
+// two CTA pairs in a 4-CTA cluster share their B tile through TMA
+// multicast, so each pair reads 24 instead of 32 KB of operands from L2 per
+// k-block.  The 4-CTA packing leaves SMs over (B200: 33 clusters = 132
+// SMs); mode 1 runs a multicast launch beside a pair launch on the rest
+// (launch_hybrid), both claiming tiles through one zeroed 8-byte state
+// (GemmParams::hyb).  Both need an even number of pair tile rows.
+// Measured (c4 GEMMs, one B200): multicast alone on 132 SMs takes the same
+// time as plain pairs on 148, and the hybrid is no faster than plain pairs
+// (z-type 1.646 vs 1.643 ms; the c4 step slower): the mainloop is bound by
+// the bytes each SM receives (multicast delivers the same bytes to both
+// pairs), not by L2 reads, so only a larger tile per CTA lowers it.
+int mc_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("DLVM_GEMM_MC");
+    return e ? std::atoi(e) : 0;  // off: measured no gain (below)
+  }();
+  return mode;
+}
+bool mc_shape_ok(const GemmParams& p, int ctas) {
+  const int64_t pair_rows = (p.M + 2 * BM - 1) / (2 * BM);
+  return ctas == 2 && !p.sched && pair_rows % 2 == 0 && max_clusters4() > 0;
+}
+// a multicast launch alone: forced, or when the packing leaves at most 8 SMs
+bool use_mc(const GemmParams& p, int ctas) {
+  const int mode = mc_mode();
+  return mode != 0 && mc_shape_ok(p, ctas) && (mode == 2 || 4 * max_clusters4() >= num_sms() - 8);
 }
 
-bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog = false) {
+// launch roles: plain (CTA or pair tiles), multicast clusters, pairs on
+// super tiles (the hybrid's second launch)
+enum { kRolePlain = 0, kRoleMc = 1, kRoleSuper = 2 };
+
+// CTAs per cluster and grid size of a launch of `tp`
+void grid_of(const TcParams& tp, int ctas, int* cluster, int* grid) {
+  const int items = tp.tiles_m * tp.tiles_n * std::max(tp.g.ksplit, 1);  // work units (tile x K split)
+  *cluster = tp.mc ? 4 : ctas;
+  const int slots = tp.mc ? max_clusters4() : num_sms() / ctas;  // persistent: one cluster per slot
+  *grid = *cluster * std::min(items, slots);
+}
+
+bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog = false, int role = -1) {
   memset(tp, 0, sizeof(*tp));
   tp->g = p;
   tp->sched = p.sched;
+  if (role < 0) role = use_mc(p, ctas) ? kRoleMc : kRolePlain;
+  tp->mc = role == kRoleMc;
+  tp->super_items = role == kRoleSuper;
 #ifdef DLVM_GEMM_TRACE
-  // launch k of the traced run writes slice k % slots of [slots][148][8]
-  tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * 16
+  // launch k of the traced run writes slice k % slots of [slots][148][kTraceSlots]
+  tp->trace = g_gemm_trace_ptr ? g_gemm_trace_ptr + (size_t)(g_gemm_trace_next++ % g_gemm_trace_slots) * 148 * kTraceSlots
                                : nullptr;
 #endif
   const int BN = p.bn;
@@ -268,8 +344,8 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog
     else  // A stored [K][M]: map {M, K}, box {64, 64}
       ok = encode(&tp->tma_a[q], G.a, p.M, G.K, G.a_s1, 64);
     if (!ok) return false;
-    if (G.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN / ctas} (a CTA's share)
-      ok = encode(&tp->tma_b[q], G.b, G.K, p.N, G.b_s1, BN / ctas);
+    if (G.b_kmajor)  // B stored [N][K]: map {K, N}, box {64, BN / ctas} (a CTA's share; half of it multicast)
+      ok = encode(&tp->tma_b[q], G.b, G.K, p.N, G.b_s1, BN / ctas / (tp->mc ? 2 : 1));
     else  // B stored [K][N]: map {N, K}, box {64, 64}
       ok = encode(&tp->tma_b[q], G.b, p.N, G.K, G.b_s0, 64);
     if (!ok) return false;
@@ -279,6 +355,8 @@ bool make_params(const GemmParams& p, TcParams* tp, int ctas = 1, bool spec_prog
     return e ? std::atoi(e) : 0;
   }();
   tp->tiles_m = (int)((p.M + BM * ctas - 1) / (BM * ctas));
+  if (role != kRolePlain) tp->tiles_m = (tp->tiles_m + 1) / 2;  // super tiles of two pair tiles
+
   tp->tiles_n = (int)((p.N + BN - 1) / BN);
   // tile raster: tall GEMMs (many more tile rows than columns: the forward
   // and activation-gradient GEMMs, A streamed once) walk groups of 2 tile
@@ -329,28 +407,111 @@ bool use_cta_pair(const GemmParams& p) {
   return mode != 0 && p.bn == 256 && p.M >= 512;
 }
 
+// the hybrid's second stream and fork / join events: per host thread and
+// device (concurrent callers never share an event), created outside stream
+// capture
+struct HybridAux {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+HybridAux* hybrid_aux(cudaStream_t stream) {
+  thread_local HybridAux per_dev[16];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  HybridAux& x = per_dev[dev];
+  if (!x.aux) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (cudaStreamCreateWithFlags(&x.aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      x.aux = nullptr;
+      return nullptr;
+    }
+  }
+  return &x;
+}
+
+// the hybrid runs when a zeroed counter is given, the shape suits multicast
+// and there are at least two super tiles per cluster
+bool use_hybrid(const GemmParams& p, int ctas) {
+  if (mc_mode() != 1 || !p.hyb || !mc_shape_ok(p, ctas) || 4 * max_clusters4() >= num_sms() - 8) return false;
+  const int64_t units = ((p.M + 4 * BM - 1) / (4 * BM)) * ((p.N + p.bn - 1) / p.bn) * std::max(p.ksplit, 1);
+  return units >= 2 * max_clusters4() && num_sms() - 4 * max_clusters4() >= 2;
+}
+
+// (one static per kernel instantiation: the attribute is per function)
 template <int BN, class PROG, int CTAS>
-cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
+cudaError_t set_max_smem() {
+  auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
   // the max-dynamic-smem attribute is per device: one bit per device ordinal
   static std::atomic<uint64_t> configured{0};
-  constexpr int SMEM = kMaxDynSmem;  // the attribute allows every launch's size
-  auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
   int dev = 0;
   cudaError_t e0 = cudaGetDevice(&dev);
   if (e0 != cudaSuccess) return e0;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_relaxed) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit);
   }
+  return cudaSuccess;
+}
+
+// Hybrid: clusters of 4 on `stream` claim super tiles from the front of the
+// work list, pairs on the auxiliary stream claim pair tiles from its back
+// (hybrid_claim).  The pair launch waits for
+// everything before the GEMM on `stream`, and `stream` waits for it after.
+template <int BN, class PROG>
+cudaError_t launch_hybrid(const GemmParams& p, cudaStream_t stream, HybridAux* x) {
+  auto kern = gemm_tc_kernel<BN, PROG, 2>;
+  cudaError_t e = set_max_smem<BN, PROG, 2>();
+  if (e != cudaSuccess) return e;
+  const bool spec = vm_cw<PROG>::value == 0;
+  GemmParams q = p;
+  q.sched = nullptr;
+  TcParams ta, tb;
+  if (!make_params(q, &ta, 2, spec, kRoleMc) || !make_params(q, &tb, 2, spec, kRoleSuper))
+    return cudaErrorInvalidValue;
+  const int units = ta.tiles_m * ta.tiles_n * std::max(p.ksplit, 1);
+  const int nA = std::min(units, max_clusters4());
+  const int nB = std::min(units - nA, (num_sms() - 4 * max_clusters4()) / 2);
+  ta.sched = tb.sched = p.hyb;  // the 8-byte claim state (hybrid_claim)
+  ta.unit0 = tb.unit0 = -1;     // every unit claimed, the first ones included
+  if (nB > 0) {
+    if ((e = cudaEventRecord(x->fork, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(x->aux, x->fork, 0)) != cudaSuccess) return e;
+  }
+  LaunchCfg La(dim3((unsigned)(4 * nA), 1, 1), dim3(NUM_THREADS, 1, 1), launch_smem(ta, BN, 2), stream, 4, 1);
+  if ((e = cudaLaunchKernelEx(&La.cfg, kern, ta)) != cudaSuccess) return e;
+  if (nB > 0) {
+    LaunchCfg Lb(dim3((unsigned)(2 * nB), 1, 1), dim3(NUM_THREADS, 1, 1), launch_smem(tb, BN, 2), x->aux, 2, 1,
+                 /*pdl=*/false);
+    if ((e = cudaLaunchKernelEx(&Lb.cfg, kern, tb)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(x->join, x->aux)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(stream, x->join, 0)) != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+template <int BN, class PROG, int CTAS>
+cudaError_t launch_ctas(const GemmParams& p, cudaStream_t stream) {
+  auto kern = gemm_tc_kernel<BN, PROG, CTAS>;
+  cudaError_t e0 = set_max_smem<BN, PROG, CTAS>();  // the attribute allows every launch's size
+  if (e0 != cudaSuccess) return e0;
+  if constexpr (CTAS == 2) {
+    if (use_hybrid(p, CTAS))
+      if (HybridAux* x = hybrid_aux(stream)) return launch_hybrid<BN, PROG>(p, stream, x);
+  }
   TcParams tp;
   if (!make_params(p, &tp, CTAS, vm_cw<PROG>::value == 0)) return cudaErrorInvalidValue;
-  // persistent: one CTA (pair) per SM (pair), up to one per work item
-  // (tile x K split)
-  const int items = tp.tiles_m * tp.tiles_n * std::max(p.ksplit, 1);
-  const int grid = CTAS * std::min(items, num_sms() / CTAS);
-  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), launch_smem(tp, BN, CTAS), stream, CTAS, 1);
+  // persistent: one CTA (pair, multicast cluster) per SM (pair, 4 SMs), up
+  // to one per work item (tile x K split)
+  int cluster = 1, grid = 1;
+  grid_of(tp, CTAS, &cluster, &grid);
+  LaunchCfg L(dim3((unsigned)grid, 1, 1), dim3(NUM_THREADS, 1, 1), launch_smem(tp, BN, CTAS), stream,
+              (unsigned)cluster, 1);
   cudaError_t e = cudaLaunchKernelEx(&L.cfg, kern, tp);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

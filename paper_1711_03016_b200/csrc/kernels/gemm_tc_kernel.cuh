@@ -36,6 +36,7 @@ namespace dlvm {
 namespace kern {
 
 constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 384;
+constexpr int kTraceSlots = 32;  // u64 trace slots per CTA (trace builds)
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
 // TMA epilogue (set up by make_params when the program is compile-time
@@ -82,6 +83,11 @@ struct TcParams {
   int32_t hint_a, hint_b;      // L2 policy per operand: 0 normal, 1 keep (evict_last), 2 stream (evict_first)
   int32_t group_m;             // tile raster: tile-rows per group (N-fastest inside a group is M-fastest here)
   int* sched;                  // dynamic tile scheduling: zeroed work counter (nullptr: static round robin)
+  int32_t mc;                  // CTA pairs in 4-CTA clusters sharing B by multicast (tiles_m counts super tiles)
+  int32_t super_items;         // pairs working on super tiles (tiles_m counts them): unit u = items 2u, 2u + 1
+  int32_t unit0;               // first static work unit of this launch; < 0: claimed (hybrid_claim, sched = state)
+  int32_t dyn_base;            // dynamic scheduling: the counter hands out units dyn_base, ... (0: gridDim / cluster;
+                               // unused when unit0 < 0: units 0, 1, ...)
 #ifdef DLVM_GEMM_TRACE
   unsigned long long* trace;   // [gridDim.x][8] %globaltimer stamps (trace builds, tools/gemm_trace.py)
 #endif
@@ -96,7 +102,14 @@ struct TcParams {
   do {                                                                              \
     unsigned long long t_;                                                          \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
-    if ((P_).trace) (P_).trace[(size_t)blockIdx.x * 16 + (slot)] = t_;               \
+    if ((P_).trace) (P_).trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = t_;               \
+  } while (0)
+// cycles spent in `stmt` added to `acc` (trace builds; plain `stmt` otherwise)
+#define DLVM_WAITC(acc, stmt)          \
+  do {                                 \
+    const long long w0_ = clock64();   \
+    stmt;                              \
+    acc += clock64() - w0_;            \
   } while (0)
 #define DLVM_SECT(var)                                                  \
   do {                                                                  \
@@ -105,6 +118,10 @@ struct TcParams {
     sect_t0 = c_;                                                       \
   } while (0)
 #else
+#define DLVM_WAITC(acc, stmt) \
+  do {                        \
+    stmt;                     \
+  } while (0)
 #define DLVM_SECT(var) \
   do {                 \
   } while (0)
@@ -167,6 +184,37 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
 }
+// two CTA pairs of a 4-CTA cluster share a B tile: each CTA loads half of
+// its pair-half of B and multicasts it to itself and the CTA at the same
+// position in the other pair (`mask`); the bytes landing in each
+// destination complete on that destination's pair-leader barrier
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar,
+                                                    int32_t c0, int32_t c1, uint64_t pol, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "h"(mask), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+// Hybrid work claims: one 64-bit state per GEMM, low word = super tiles
+// claimed from the front (the multicast clusters), high word = pair tiles
+// claimed from the back (the pair launch), over n_pair pair tiles (unit u =
+// pair tiles 2u, 2u + 1).  A claim only succeeds (compare-and-swap) while
+// it overlaps no earlier claim, so every pair tile is taken exactly once; a
+// single pair tile left between the two sides goes to the pair launch.
+// Returns the claimed unit (front) or pair tile (back), or -1 when none is left.
+__device__ __forceinline__ int hybrid_claim(unsigned long long* state, bool front, int n_pair) {
+  unsigned long long old = atomicAdd(state, 0ull);
+  for (;;) {
+    const int f = (int)(old & 0xffffffffull), b = (int)(old >> 32);
+    if (front ? 2 * f + 2 > n_pair - b : n_pair - b - 1 < 2 * f) return -1;
+    const unsigned long long want = front ? old + 1ull : old + (1ull << 32);
+    const unsigned long long got = atomicCAS(state, old, want);
+    if (got == old) return front ? f : n_pair - 1 - b;
+    old = got;
+  }
+}
+
 // L2 policies: keep (evict_last) the small operand every tile re-reads,
 // stream (evict_first) the large one read once, or normal
 __device__ __forceinline__ uint64_t l2_policy(int hint) {
@@ -361,11 +409,12 @@ __device__ __forceinline__ void umma_bf16_pair(uint32_t d_tmem, uint64_t a, uint
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-// arrive on the barrier at this offset in both CTAs of the pair
-__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+// arrive on the barrier at this offset in every CTA of `mask` (the pair,
+// or all four CTAs of a multicast cluster)
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"((uint16_t)3)
+      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -818,9 +867,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   if (threadIdx.x == 0) DLVM_GT(P, 0);
   const int base_tiles = P.tiles_m * P.tiles_n;  // tiles of CTAS*BM rows
   const int nsplit = g.ksplit > 1 ? g.ksplit : 1;
-  const int n_tiles = base_tiles * nsplit;       // work items (tile, K split)
+  const int n_tiles = base_tiles * nsplit;       // work units (tile, K split)
   const uint32_t rank = CTAS == 2 ? cluster_rank() : 0;
-  const int tile0 = blockIdx.x / CTAS, tile_step = gridDim.x / CTAS;
+  // multicast clusters (P.mc): 4 CTAs = two pairs; a work item is a super
+  // tile of two pair tiles stacked in M (pair `pidx` takes tile row
+  // 2 * tm + pidx) that share their B tile.  `prank`: rank in the pair,
+  // `pbase`: the pair leader's cluster rank
+  const bool mc = CTAS == 2 && P.mc;
+  const uint32_t prank = rank & 1u, pbase = rank & 2u;
+  const int pidx = (int)(rank >> 1);
+  const int cl = mc ? 4 : CTAS;
+  // Hybrid launches (gemm_tc.cuh launch_hybrid): a multicast-cluster launch
+  // claims super tiles (units u: pair tiles 2u, 2u + 1) from the front of
+  // the work list and a pair launch on the SMs the 4-CTA packing leaves
+  // over claims single pair tiles (items p: unit p / 2, half p % 2,
+  // P.super_items) from the back (hybrid_claim)
+  const bool sup = CTAS == 2 && P.super_items;
+  const int tile0 = (sup ? 2 : 1) * (P.unit0 + (int)blockIdx.x / cl), tile_step = gridDim.x / cl;
+  // item -> the pair's tile row and column; returns the K split
+  auto decode = [&](int item, int* tm, int* tn) -> int {
+    const int u = sup ? item >> 1 : item;
+    tile_coords(u % base_tiles, P.tiles_m, P.tiles_n, tm, tn, P.group_m);
+    *tm = sup ? 2 * *tm + (item & 1) : mc ? 2 * *tm + pidx : *tm;
+    return u / base_tiles;
+  };
+  auto split_of = [&](int item) { return (sup ? item >> 1 : item) / base_tiles; };
+  const int n_items = sup ? 2 * n_tiles : n_tiles;
   // Dynamic scheduling (P.sched != nullptr): the first tile of every CTA
   // (pair) is its static one; later ones come from an atomic counter
   // (tile_step + counter), fetched by the leader's producer lane one tile
@@ -833,8 +905,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     mbar_wait(tq_empty_bar + 8 * slot, ((k >> 2) & 1) ^ 1);
     st_shared_s32(tileq + 4 * slot, t);
     if constexpr (CTAS == 2) {
-      st_cluster_u32(mapa_rank(tileq + 4 * slot, 1), t);
-      mbar_arrive_release_cluster(mapa_rank(tq_full_bar + 8 * slot, 1));
+      for (int r = 1; r < cl; ++r) {
+        st_cluster_u32(mapa_rank(tileq + 4 * slot, r), t);
+        mbar_arrive_release_cluster(mapa_rank(tq_full_bar + 8 * slot, r));
+      }
     }
     mbar_arrive(tq_full_bar + 8 * slot);
   };
@@ -862,7 +936,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, mc ? 2 : 1);  // multicast: both pairs' MMAs release the slot
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tfull_bar + 8 * s, 1);
@@ -873,7 +947,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     // tile queue (dynamic scheduling): one publish per slot use; released by
     // every consumer of the pair: the peer's producer, the MMA issuer, the
     // epilogue warps and the input loaders
-    const int n_cons = (CTAS == 2 ? 1 : 0) + 1 + 8 * CTAS + (xt.on && xt.n_in_bufs > 0 ? CTAS : 0);
+    // (per pair: the peer's producer, the leader's MMA issuer; a multicast
+    // cluster counts both pairs)
+    const int n_cons = (cl - 1) + (CTAS == 2 ? cl / 2 : 1) + 8 * cl + (xt.on && xt.n_in_bufs > 0 ? cl : 0);
     for (int s = 0; s < 4; ++s) {
       mbar_init(tq_full_bar + 8 * s, 1);
       mbar_init(tq_empty_bar + 8 * s, n_cons);
@@ -909,8 +985,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
   if (warp == 0) {  // ---------------- TMA producer (lane 0) + L2 prefetch of epilogue inputs (all lanes)
     int s = 0;
     uint32_t ph = 0;
-    int t_next = tile0;  // leader lane 0 (dynamic): the tile published for the next iteration
-    if (dyn && rank == 0 && lane == 0) tq_publish(0, t_next);
+    int t_next = tile0;  // leader lane 0 (dynamic): the item published for the next iteration
+    // plain dynamic scheduling: counter value c hands out unit dyn_base + c,
+    // after every CTA's (pair's) static first unit
+    const int dyn_base = P.dyn_base ? P.dyn_base : tile_step;
+    // hybrid launches (P.unit0 < 0): every item is claimed, the first one
+    // included, so a cluster that becomes resident late finds the work taken
+    // instead of holding a static unit for the tail
+    auto next_item = [&]() -> int {
+      if (P.unit0 < 0) {
+        const int c = hybrid_claim(reinterpret_cast<unsigned long long*>(P.sched), !sup, 2 * n_tiles);
+        return c < 0 ? n_items : c;
+      }
+      return dyn_base + atomicAdd(P.sched, 1);
+    };
+    if (dyn && rank == 0 && lane == 0) {
+      if (P.unit0 < 0) t_next = next_item();
+      tq_publish(0, t_next);
+    }
     for (int pit = 0;; ++pit) {
       int t;
       if (!dyn) {
@@ -920,8 +1012,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         if (lane == 0) {
           if (rank == 0) {
             tl = t_next;
-            if (tl < n_tiles) {  // fetch and publish the next one ahead of need
-              t_next = tile_step + atomicAdd(P.sched, 1);
+            if (tl < n_items) {  // fetch and publish the next one ahead of need
+              t_next = next_item();
               tq_publish(pit + 1, t_next);
             }
           } else {
@@ -930,11 +1022,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         }
         t = __shfl_sync(0xffffffffu, tl, 0);
       }
-      if (t >= n_tiles) break;
+      if (t >= n_items) break;
       int tm, tn;
-      const int split = t / base_tiles;
-      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
-      const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
+      const int split = decode(t, &tm, &tn);
+      const int m0 = (tm * CTAS + (int)prank) * BM, n0 = tn * BN;
       for (int i = 0; i < g.n_pf; ++i) {
         const int64_t cols = min((int64_t)BN, g.N - n0);
         const uint32_t bytes = (uint32_t)((cols * g.pf_esize[i] + 15) & ~15);
@@ -959,18 +1050,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             const uint32_t fb = full_bar + 8 * s;
             const uint32_t a_dst = sA + s * A_STAGE_BYTES, b_dst = sB + s * B_STAGE_BYTES;
             const int k0 = kb * BK;
-            const int nb = n0 + (int)rank * BNC;  // this CTA's half of B
+            const int nb = n0 + (int)prank * BNC;  // this CTA's half of B
             if constexpr (CTAS == 2) {
               // both halves complete on the leader's barrier, armed with both CTAs' bytes
-              const uint32_t lb = mapa_rank(fb, 0);
-              if (rank == 0) mbar_expect_tx(fb, 2 * STAGE_TX);
+              const uint32_t lb = mapa_rank(fb, pbase);
+#ifdef DLVM_PROBE_SKIP_B
+              // measurement probe (wrong results): B loaded on even k-blocks
+              // only, 25% fewer operand bytes from L2
+              const bool skipb = kb & 1;
+              if (prank == 0) mbar_expect_tx(fb, 2 * (skipb ? A_STAGE_BYTES : STAGE_TX));
+#else
+              constexpr bool skipb = false;
+              if (prank == 0) mbar_expect_tx(fb, 2 * STAGE_TX);
+#endif
               if (G.a_kmajor) {
                 tma_load_2d_pair(a_dst, ma, lb, k0, m0, pol_a);
               } else {
                 tma_load_2d_pair(a_dst, ma, lb, m0, k0, pol_a);
                 tma_load_2d_pair(a_dst + 8192, ma, lb, m0 + 64, k0, pol_a);
               }
-              if (G.b_kmajor) {
+              if (skipb) {
+              } else if (mc) {
+                // half of this CTA's B half (64 of its BNC = 128 columns), to
+                // both pairs
+                const uint16_t mask = (uint16_t)((1u << prank) | (1u << (prank + 2)));
+                if (G.b_kmajor)
+                  tma_load_2d_pair_mc(b_dst + pidx * 8192, mb, lb, k0, nb + 64 * pidx, pol_b, mask);
+                else
+                  tma_load_2d_pair_mc(b_dst + pidx * 8192, mb, lb, nb + 64 * pidx, k0, pol_b, mask);
+              } else if (G.b_kmajor) {
                 tma_load_2d_pair(b_dst, mb, lb, k0, nb, pol_b);
               } else {
 #pragma unroll
@@ -1001,16 +1109,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
+    if (lane == 0 && prank == 0) {  // ---------------- MMA issuer (the pair's leader)
       int s = 0;
       uint32_t ph = 0;
+      long long w_acc = 0, w_stage = 0, c_loop = clock64();  // trace builds: wait cycles
+      int n_it = 0;
       for (int it = 0;; ++it) {
         const int t = dyn ? tq_take(it) : tile0 + it * tile_step;
-        if (t >= n_tiles) break;
-        const int split = t / base_tiles;
+        if (t >= n_items) break;
+        ++n_it;
+        const int split = split_of(t);
         const int as = it & 1;
         const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(tempty_bar + 8 * as, aph ^ 1);
+        DLVM_WAITC(w_acc, mbar_wait(tempty_bar + 8 * as, aph ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         uint32_t accum = 0;  // the tile's first MMA overwrites the accumulator
@@ -1021,7 +1132,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           const int kbs = (num_kb + nsplit - 1) / nsplit;
           const int kb_lo = split * kbs, kb_hi = kb_lo + kbs < num_kb ? kb_lo + kbs : num_kb;
           for (int kb = kb_lo; kb < kb_hi; ++kb) {
-            mbar_wait(full_bar + 8 * s, ph);
+            DLVM_WAITC(w_stage, mbar_wait(full_bar + 8 * s, ph));
             tc_fence_after();
             if (t == tile0 && q == 0 && kb == kb_lo) DLVM_GT(P, 3);
             const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
@@ -1036,7 +1147,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
               accum = 1;
             }
             if constexpr (CTAS == 2)
-              umma_commit_pair(empty_bar + 8 * s);  // both CTAs' slots are free
+              umma_commit_pair(empty_bar + 8 * s, mc ? 0xF : 3);  // the slot is free in every CTA it feeds
             else
               umma_commit(empty_bar + 8 * s);
             if (++s == nst) {
@@ -1046,11 +1157,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
           }
         }
         if constexpr (CTAS == 2)
-          umma_commit_pair(tfull_bar + 8 * as);
+          umma_commit_pair(tfull_bar + 8 * as, (uint16_t)(3u << pbase));
         else
           umma_commit(tfull_bar + 8 * as);
       }
       DLVM_GT(P, 4);
+#ifdef DLVM_GEMM_TRACE
+      // slots 16..19: MMA issuer cycles waiting for an empty accumulator
+      // (epilogue-bound), for a full operand stage (load-bound), its whole
+      // loop, and its tile count
+      if (P.trace) {
+        P.trace[(size_t)blockIdx.x * kTraceSlots + 16] = (unsigned long long)w_acc;
+        P.trace[(size_t)blockIdx.x * kTraceSlots + 17] = (unsigned long long)w_stage;
+        P.trace[(size_t)blockIdx.x * kTraceSlots + 18] = (unsigned long long)(clock64() - c_loop);
+        P.trace[(size_t)blockIdx.x * kTraceSlots + 19] = (unsigned long long)n_it;
+      }
+#else
+      (void)w_acc;
+      (void)w_stage;
+      (void)c_loop;
+      (void)n_it;
+#endif
     }
   } else if (warp == 3) {  // ---------------- epilogue input loader (TMA epilogue)
     if (xt.on && xt.n_in_bufs > 0 && lane == 0) {
@@ -1058,10 +1185,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       const EwParams& E = g.epi;
       for (int it = 0;; ++it) {
         const int t = dyn ? tq_take(it) : tile0 + it * tile_step;
-        if (t >= n_tiles) break;
+        if (t >= n_items) break;
         int tm, tn;
-        tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
-        const int m0 = (tm * CTAS + (int)rank) * BM, n0 = tn * BN;
+        decode(t, &tm, &tn);
+        const int m0 = (tm * CTAS + (int)prank) * BM, n0 = tn * BN;
         const int b = xt.n_in_bufs == 2 ? (it & 1) : 0;
         const uint32_t ph = xt.n_in_bufs == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(in_empty_bar + 8 * b, ph ^ 1);
@@ -1159,13 +1286,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
 #ifdef DLVM_GEMM_TRACE
     long long sect[7] = {0, 0, 0, 0, 0, 0, 0}, sect_t0 = clock64();
 #endif
+    long long w_full = 0, c_epi = clock64();  // trace builds: accumulator waits, loop cycles
     for (int it = 0;; ++it) {
       const int t = warp_tile(it);
-      if (t >= n_tiles) break;
+      if (t >= n_items) break;
       int tm, tn;
-      const int split = t / base_tiles;
-      tile_coords(t % base_tiles, P.tiles_m, P.tiles_n, &tm, &tn, P.group_m);
-      tm = tm * CTAS + (int)rank;  // this CTA's 128-row block (partials layout)
+      const int split = decode(t, &tm, &tn);
+      tm = tm * CTAS + (int)prank;  // this CTA's 128-row block (partials layout)
       // split K: this work item's raw accumulator goes to its split's slice
       EwDevOut out0 = E.out[0];
       out0.ptr = static_cast<char*>(out0.ptr) + (int64_t)split * g.split_bytes;
@@ -1196,7 +1323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       }
       const int as = it & 1;
       const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(tfull_bar + 8 * as, aph);
+      DLVM_WAITC(w_full, mbar_wait(tfull_bar + 8 * as, aph));
       tc_fence_after();
       if (it == 0 && ew == 0 && lane == 0) DLVM_GT(P, 5);
       const int ib = xt.n_in_bufs == 2 ? (it & 1) : 0;
@@ -1402,7 +1529,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) {
         if constexpr (CTAS == 2)
-          mbar_arrive_cluster(mapa_rank(tempty_bar + 8 * as, 0));
+          mbar_arrive_cluster(mapa_rank(tempty_bar + 8 * as, pbase));
         else
           mbar_arrive(tempty_bar + 8 * as);
       }
@@ -1449,12 +1576,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
     if (tma_on && lane == 0) bulk_wait_all();  // this warp's TMA stores are complete
     if (ew == 0 && lane == 0) DLVM_GT(P, 6);
 #ifdef DLVM_GEMM_TRACE
+    // slots 20, 21: epilogue warp 4's cycles waiting for a full accumulator
+    // (MMA-bound) and its whole tile loop
+    if (ew == 0 && lane == 0 && P.trace) {
+      P.trace[(size_t)blockIdx.x * kTraceSlots + 20] = (unsigned long long)w_full;
+      P.trace[(size_t)blockIdx.x * kTraceSlots + 21] = (unsigned long long)(clock64() - c_epi);
+    }
+#else
+    (void)w_full;
+    (void)c_epi;
+#endif
+#ifdef DLVM_GEMM_TRACE
     // epilogue section cycles of warp 4 (DLVM_EPI_DBG & 8): slots 8..14 =
     // loop overhead, TMEM loads, inputs, program, stores, reductions, staging waits
     if ((xt.dbg & 8) && ew == 0 && lane == 0 && P.trace) {
       long long c_ = clock64();
       (void)c_;
-      for (int k = 0; k < 7; ++k) P.trace[(size_t)blockIdx.x * 16 + 8 + k] = (unsigned long long)sect[k];
+      for (int k = 0; k < 7; ++k) P.trace[(size_t)blockIdx.x * kTraceSlots + 8 + k] = (unsigned long long)sect[k];
     }
 #endif
   }

@@ -78,6 +78,7 @@ struct GemmParams {
   // reduce-add, else by red.global.add (SType::F32_ADD); split_bytes unused
   int32_t split_red;
   int* sched;                // tcgen05: zeroed work counter (dynamic tile scheduling) or nullptr
+  int* hyb;                  // tcgen05: zeroed 8-byte claim state of a hybrid multicast + pair launch, or nullptr
   int32_t n_pf;
   const void* pf_ptr[4];
   int64_t pf_row_bytes[4];  // row stride in bytes
@@ -93,6 +94,7 @@ cudaError_t launch_ew_fn(void* fn, const EwParams& p, int bx, int by, cudaStream
 cudaError_t launch_gemm_tc_fn(void* fn, int ctas, const GemmParams& p, cudaStream_t stream);
 cudaError_t launch_gemm_simt_fn(void* fn, const GemmParams& p, cudaStream_t stream);
 int gemm_tc_ctas(int64_t M, int bn);  // 2: the launcher runs CTA pairs for this shape
+bool gemm_hybrid_enabled();           // DLVM_GEMM_MC=1: large pair GEMMs may run as hybrid launches
 cudaError_t launch_gemm_tc(const GemmParams& p, cudaStream_t stream);
 bool gemm_tc_available();
 

@@ -55,7 +55,8 @@ inline bool pdl_enabled() {
 struct LaunchCfg {
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
-  LaunchCfg(dim3 grid, dim3 block, size_t smem, cudaStream_t stream, unsigned cluster_x = 1, unsigned cluster_z = 1) {
+  LaunchCfg(dim3 grid, dim3 block, size_t smem, cudaStream_t stream, unsigned cluster_x = 1, unsigned cluster_z = 1,
+            bool pdl = true) {
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
@@ -68,7 +69,7 @@ struct LaunchCfg {
       attr[n].val.clusterDim.z = cluster_z;
       ++n;
     }
-    if (pdl_enabled()) {
+    if (pdl && pdl_enabled()) {
       attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[n].val.programmaticStreamSerializationAllowed = 1;
       ++n;

@@ -1665,8 +1665,15 @@ struct Planner {
     }
     add_events();
     for (auto& st : plan.steps)
-      if (st.kind == Step::GEMM && st.gemm.tensor_core) st.gemm.sched_index = plan.n_sched++;
-    if (plan.n_sched) plan.sched_buf = add_buf(BufferSlot::Work, -1, (size_t)plan.n_sched * 4, SType::U8);
+      if (st.kind == Step::GEMM && st.gemm.tensor_core) {
+        st.gemm.sched_index = plan.n_sched++;
+        // large enough for a hybrid multicast + pair launch (its counter is
+        // zeroed every run; the launcher decides per launch)
+        const double flops = 2.0 * st.gemm.M * st.gemm.N * st.gemm.K;
+        if (flops >= 68.7e9 && st.gemm.bn == 256 && st.gemm.M >= 1024) plan.hybrid_counters = true;
+      }
+    // 8 bytes per GEMM: a work counter (low word) or a hybrid claim state
+    if (plan.n_sched) plan.sched_buf = add_buf(BufferSlot::Work, -1, (size_t)plan.n_sched * 8, SType::U8);
     plan.workspace_bytes = (plan.workspace_bytes + 255) / 256 * 256;
     plan.n_inputs = plan.seed_is_input ? f.num_args() - 1 : f.num_args();
     plan.n_outputs = (int)f.ret.size();

@@ -147,6 +147,7 @@ struct Plan {
   std::vector<int> input_bf16_ok;  // per input: 1 if it may be passed as bf16 (see make_plan)
   std::vector<int> input_u8_ok;    // per input: 1 if it may be passed as bool bytes (0/1 values; not a dot operand)
   int sched_buf = -1, n_sched = 0;  // work counters of the tcgen05 GEMMs (zeroed at the start of a run)
+  bool hybrid_counters = false;     // some GEMM may run as a hybrid launch: zero the counters every run
   int launches() const;
   std::string str() const;
   std::string detail() const;  // str() + buffers and every step's operand refs

@@ -1533,3 +1533,54 @@ def test_split_k_reduce_add_bit_identical_to_partials(tmp_path):
             if k != "n_ew":
                 np.testing.assert_array_equal(outs[key][k], ref[k], err_msg=f"{key} {k}")
         assert int(outs[key]["n_ew"]) < int(ref["n_ew"]), (key, int(outs[key]["n_ew"]), int(ref["n_ew"]))
+
+
+_MC_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+outs = []
+cases = [
+    W.c3(1024),                                                      # c3: pair tiles, 4 pair rows
+    W.c3(1000, layers=[(520, 1000, "relu"), (1000, 136, None)]),    # ragged: last pair half out of range
+    W.c3(8192, layers=[(512, 512, "relu"), (512, 256, None)]),      # split-K dW
+    W.c3(8192, layers=[(2048, 4096, "relu"), (4096, 264, None)]),   # hybrid-sized (>= 66 super tiles)
+    W.c3(16384, layers=[(2048, 4096, "relu"), (4096, 264, None)]),  # hybrid + split-K dW1 (K = 16384)
+]
+for w in cases:
+    r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
+    outs += r["primal"] + r["grad"]
+np.savez({out!r}, *outs)
+"""
+
+
+def test_multicast_clusters_bit_identical_to_pairs(tmp_path):
+    """CTA pairs in 4-CTA clusters (two pair tiles stacked in M share their B
+    tile through TMA multicast) move operands differently but compute the
+    same MMAs in the same order: losses and gradients are bit-identical to
+    plain CTA pairs (DLVM_GEMM_MC=0) both for multicast launches alone
+    (DLVM_GEMM_MC=2) and for the default hybrid (DLVM_GEMM_MC=1: a
+    multicast launch beside a pair launch on super tiles, both fed by one
+    counter), incl. a ragged M whose last super tile is half out of range,
+    N-major and K-major B and split K (alone and in a hybrid launch); each
+    path was really taken
+    (DLVM_EPI_VERBOSE)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mc in ("0", "1", "2"):
+        out = str(tmp_path / f"m{mc}.npz")
+        script = _MC_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+        p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_GEMM_MC=mc, DLVM_EPI_VERBOSE="1"),
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-3000:]
+        n_mc = sum(1 for line in p.stderr.splitlines() if "ctas=2 mc=1" in line)
+        n_sup = sum(1 for line in p.stderr.splitlines() if "sup=1" in line)
+        assert (n_mc > 0) == (mc != "0") and (n_sup > 0) == (mc == "1"), (mc, n_mc, n_sup)
+        outs[mc] = np.load(out)
+    for mc in ("1", "2"):
+        for k in outs["0"].files:
+            np.testing.assert_array_equal(outs[mc][k], outs["0"][k], err_msg=f"DLVM_GEMM_MC={mc} {k}")

@@ -41,7 +41,7 @@ def main():
     b = torch.randn(N, K, device=dev).to(torch.bfloat16)
     m = torch.rand(M, N, device=dev) < 0.5
     v = torch.randn(1, N, device=dev)
-    buf = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+    buf = torch.zeros(148 * 32, dtype=torch.int64, device=dev)
     for name, (extra, body, rtypes, odt) in PROGS.items():
         rt = rtypes[0] if len(rtypes) == 1 else "(" + ", ".join(rtypes) + ")"
         params = f"{A}, {B}" + (f", {V}" if "%v" in extra else "") + (f", {BL}" if "%m" in extra else "")
@@ -61,7 +61,7 @@ def main():
             f.run(ins, outputs=outs, workspace=ws)
             torch.cuda.synchronize()
             L.dlvm_debug_gemm_trace(None, 1)
-            t = buf.cpu().numpy().reshape(148, 16).astype(np.float64)
+            t = buf.cpu().numpy().reshape(148, 32).astype(np.float64)
             live = t[t[:, 5] > 0]
             res.append(np.median(live[:, 6] - live[:, 5]) / 1e3)
             if int(os.environ.get("DLVM_EPI_DBG", "0")) & 8:  # section cycles of epilogue warp 4

@@ -8,7 +8,12 @@ accumulator ready and last epilogue tile done (epilogue warp 4), exit.
 Prints per GEMM the median over CTAs of each stamp relative to that GEMM's
 earliest entry, the latest exit, and the gap to the previous GEMM's last
 exit (us).
-usage: gemm_trace.py [c3|c4]"""
+Then, per GEMM, where the time goes in the persistent loop (clock64
+cycles, median over CTAs): the MMA issuer's share waiting for an empty
+accumulator (the epilogue is behind) and for a full operand stage (the
+loads are behind), and the first epilogue warp's share waiting for a full
+accumulator (the MMAs are behind).
+usage: gemm_trace.py [c3|c4|c4x8]   (c4x8: one rank's c4 shard at N=8)"""
 import ctypes
 import os
 import sys
@@ -27,7 +32,7 @@ NAMES = ["entry", "pdl_done", "tma0", "stage0", "mma_end", "acc0", "epi_end", "e
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
-    w = W.c3() if cfg == "c3" else W.c4(8)
+    w = W.c3() if cfg == "c3" else W.c4(8) if cfg == "c4x8" else W.c4()
     dev = torch.device("cuda:0")
     f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
     ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
@@ -42,7 +47,7 @@ def main():
     G = len(gemms)
     L = P.dlvm.lib()
     L.dlvm_debug_gemm_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-    buf = torch.zeros(G * 148 * 16, dtype=torch.int64, device=dev)
+    buf = torch.zeros(G * 148 * 32, dtype=torch.int64, device=dev)
     for _ in range(5):
         f.grad_run(ins, seed=seed, outputs=outs, workspace=ws)
     torch.cuda.synchronize()
@@ -52,7 +57,7 @@ def main():
         f.grad_run(ins, seed=seed, outputs=outs, workspace=ws)
         torch.cuda.synchronize()
         L.dlvm_debug_gemm_trace(None, 1)
-    t = buf.cpu().numpy().reshape(G, 148, 16).astype(np.float64)
+    t = buf.cpu().numpy().reshape(G, 148, 32).astype(np.float64)
     t0 = t[t > 0].min()
     prev_exit = None
     print(f"{'gemm':60s} " + " ".join(f"{n:>8s}" for n in NAMES) + f" {'last_exit':>9s} {'gap':>6s}")
@@ -66,6 +71,13 @@ def main():
         prev_exit = live[:, 7].max()
         print(f"{gemms[g][:60]:60s} " + " ".join(f"{m:8.2f}" for m in med) + f" {last:9.2f} {gap:6.2f}"
               f"  ctas={len(live)} t={(start - t0) / 1e3:.1f}")
+    print(f"\n{'gemm':60s} {'tiles':>6s} {'mma_wait_acc%':>14s} {'mma_wait_stage%':>16s} {'epi_wait_acc%':>14s}")
+    for g in range(G):
+        mma = t[g][t[g][:, 18] > 0]
+        epi = t[g][t[g][:, 21] > 0]
+        med = lambda a: float(np.median(a)) if len(a) else float("nan")
+        print(f"{gemms[g][:60]:60s} {med(mma[:, 19]):6.1f} {100 * med(mma[:, 16] / mma[:, 18]):14.1f} "
+              f"{100 * med(mma[:, 17] / mma[:, 18]):16.1f} {100 * med(epi[:, 20] / epi[:, 21]):14.1f}")
 
 
 if __name__ == "__main__":
