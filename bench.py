@@ -375,6 +375,20 @@ def oracle_threads():
     return n
 
 
+def blas_info():
+    """numpy version and the BLAS library / threads the oracle's dots ran on."""
+    import numpy as np
+    info = {"numpy": np.__version__}
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [p for p in threadpool_info() if p.get("user_api") == "blas"]
+        if blas:
+            info["blas"] = f"{blas[0].get('internal_api')} {blas[0].get('version')} ({blas[0].get('num_threads')} threads)"
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
 def cpu_baseline_mlp(w, rows: int):
     """The oracle (plain float64 numpy interpreter + reverse sweep) timed on
     `rows` rows of the same workload with full-size weights."""
@@ -386,15 +400,15 @@ def cpu_baseline_mlp(w, rows: int):
     m = oracle.parse(ws.text)
     ins = [x.astype(np.float64) for x in ws.inputs()] + [np.float64(w.seed())]
     reps, t0 = 0, time.perf_counter()
-    while True:  # at least one pass, and >= 2 s of work for tiny configs
+    while True:  # passes over the same rows until >= 10 s of CPU work (bounded sample, ④)
         oracle.run(m, ws.grad, ins)
         reps += 1
         dt = time.perf_counter() - t0
-        if dt >= 2.0 or w.cfg != 1:
+        if dt >= 10.0:
             break
     return {"value": rows * reps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
             "sample": f"{rows} rows of {w.name} (full {len(w.layers)}-layer weights), {reps} fwd+adjoint pass(es), "
-                      f"float64 numpy ({dt:.2f} s)"}
+                      f"float64 numpy ({dt:.2f} s)", **blas_info()}
 
 
 def cpu_baseline_chain(rows: int, C: int = 16384):
