@@ -219,6 +219,14 @@ def test_c5_small_tanh_bf16():
     _check_c3(w)
 
 
+def test_c5_full_width_reduced_batch():
+    """c5 with its full weights (8 tanh layers of 8192 x 8192, SURVEY 8(d):
+    "full weights, batch reduced to 256 rows") against the float64 oracle:
+    every gradient (A18' vs the bf16-policy oracle, A18 vs the unrounded
+    one: a kink-free network) and the loss."""
+    _check_c3(W.c5(256, 256))
+
+
 def test_c3_bf16_inputs_passed_as_bf16():
     """Inputs that feed only dots may be passed as bf16 (dlvm.h): identical
     results to passing f32 (the library's own RNE cast)."""
