@@ -1511,7 +1511,20 @@ for w in cases:
         torch.cuda.synchronize()
     n_ew += sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "ew" in e.name and "gemm" not in e.name)
     outs += r["grad"]
-np.savez({out!r}, *outs, n_ew=np.int64(n_ew))
+# gradients bound as bf16: the sum step runs (the GEMM cannot add into a
+# bf16 home) and stores the bf16 rounding of the same f32 sums
+import paper_1711_03016_b200 as P
+w = cases[0]
+f = P.Function(w.text, w.fn, w.grad, dot_precision="bf16")
+dev = torch.device("cuda:0")
+ins = [torch.from_numpy(x).to(dev) for x in w.inputs()]
+seed = torch.tensor(np.float32(w.seed()), device=dev)
+o32 = f.grad_run(ins, seed=seed)
+o16 = [torch.empty(o.shape, dtype=torch.bfloat16, device=dev) for o in o32]
+f.grad_run(ins, seed=seed, outputs=o16)
+torch.cuda.synchronize()
+bf16_same = all(torch.equal(a.to(torch.bfloat16), b) for a, b in zip(o32, o16))
+np.savez({out!r}, *outs, n_ew=np.int64(n_ew), bf16_same=np.int64(bf16_same))
 """
 
 
@@ -1521,7 +1534,8 @@ def test_split_k_reduce_add_bit_identical_to_partials(tmp_path):
     the direct epilogue) instead of storing partials for a sum step: 0 + a + b
     rounds to fl(a + b) in either order, so the gradients are bit-identical
     to the partials + sum-step path (DLVM_GEMM_SPLITRED=0), and the sum
-    steps' EW launches are gone."""
+    steps' EW launches are gone.  With the gradients bound as bf16 the sum
+    step runs and stores exactly the bf16 rounding of the f32 results."""
     import os
     import subprocess
     import sys
@@ -1538,9 +1552,10 @@ def test_split_k_reduce_add_bit_identical_to_partials(tmp_path):
     ref = outs["01"]
     for key in ("11", "10"):
         for k in ref.files:
-            if k != "n_ew":
+            if k not in ("n_ew", "bf16_same"):
                 np.testing.assert_array_equal(outs[key][k], ref[k], err_msg=f"{key} {k}")
         assert int(outs[key]["n_ew"]) < int(ref["n_ew"]), (key, int(outs[key]["n_ew"]), int(ref["n_ew"]))
+        assert int(outs[key]["bf16_same"]) == 1, key
 
 
 _MC_SCRIPT = r"""
