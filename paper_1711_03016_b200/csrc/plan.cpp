@@ -1802,8 +1802,22 @@ struct Planner {
     // the GEMM stores S raw partial tiles and the epilogue program moves to
     // an EW step that sums them in split order (deterministic)
     const int S = split_k(gm);
+    // An epilogue reading three or more f32 [M, N] operands (mlp_hvp's
+    // second-order term %d9: four) cannot stage them through shared memory
+    // (128 KB per operand per 256-wide tile) and loads them row per lane at
+    // a fraction of HBM bandwidth: the GEMM stores its raw accumulator and
+    // the epilogue program runs as the next EW step instead (same program on
+    // the same f32 values: bit-identical; DLVM_EPI_DEFER=0 keeps it fused).
+    // Measured (mlp_hvp, one B200): %d9 286 -> 66 + 187 us; with two such
+    // operands (%o) deferring lost (95 -> 58 + 48 us), hence the threshold
+    const int heavy = f32_row_inputs(gm.epi);
+    static const bool defer_on = [] {
+      const char* e = std::getenv("DLVM_EPI_DEFER");
+      return !(e && e[0] == '0');
+    }();
+    const bool defer = S == 1 && defer_on && gm.tensor_core && heavy >= 3;
     EwGroup split_ew;
-    if (S > 1) {
+    if (S > 1 || defer) {
       split_ew = gm.epi;
       const int pbuf = add_buf(BufferSlot::Work, -1, (size_t)S * gm.M * gm.N * 4, SType::F32);
       IterRef part;
@@ -1867,16 +1881,21 @@ struct Planner {
       }
     }
     if (S > 1) d << " (K split " << S << ", raw partials; epilogue in the next step)";
+    if (defer) d << " (raw accumulator; epilogue with " << heavy << " f32 [M,N] operands in the next step)";
     s.desc = d.str();
     gm.epi.desc = s.desc;
     plan.steps.push_back(s);
-    if (S > 1) {
+    if (S > 1 || defer) {
       Step e;
       e.kind = Step::EW;
       e.ew = split_ew;
       std::ostringstream de;
-      de << "ew [" << gm.M << "," << gm.N << "] vec" << split_ew.vec << " sum of " << S << " K-split partials of %"
-         << f.names[dv] << " + epilogue ops=" << (int)split_ew.prog.n_ins << " stores=" << (int)split_ew.prog.n_stores
+      de << "ew [" << gm.M << "," << gm.N << "] vec" << split_ew.vec;
+      if (S > 1)
+        de << " sum of " << S << " K-split partials of %" << f.names[dv];
+      else
+        de << " deferred epilogue of %" << f.names[dv];
+      de << " + epilogue ops=" << (int)split_ew.prog.n_ins << " stores=" << (int)split_ew.prog.n_stores
          << " reductions=" << (int)split_ew.prog.n_reduces;
       if (gm.split_red_ok) de << " (skipped when the home is bound as f32: the GEMM adds the splits into it)";
       e.desc = de.str();
@@ -1893,6 +1912,18 @@ struct Planner {
   // launcher chooses) leaves the last wave partly idle; splitting K into S
   // work items per tile is worth it when it raises the busy fraction by > 5
   // points and every split keeps K/S >= 4096 (DLVM_GEMM_SPLITK=0 disables)
+  // [M, N] row-contiguous f32 operands of a GEMM epilogue (slot 0, the
+  // accumulator, excluded); caller inputs count as f32 (their usual binding)
+  int f32_row_inputs(const EwGroup& g) const {
+    int n = 0;
+    for (size_t q = 1; q < g.inputs.size(); ++q) {
+      const IterRef& r = g.inputs[q];
+      if (r.buf < 0 || r.nchunks != 1 || r.strides[1] != 1 || r.strides[0] == 0) continue;
+      if (plan.bufs[r.buf].st == SType::F32) ++n;
+    }
+    return n;
+  }
+
   static int split_k(const GemmStep& gm) {
     static const bool on = [] {
       const char* e = std::getenv("DLVM_GEMM_SPLITK");

@@ -1607,3 +1607,42 @@ def test_multicast_clusters_bit_identical_to_pairs(tmp_path):
     for mc in ("1", "2"):
         for k in outs["0"].files:
             np.testing.assert_array_equal(outs[mc][k], outs["0"][k], err_msg=f"DLVM_GEMM_MC={mc} {k}")
+
+
+_DEFER_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import workloads as W
+from helpers import gpu_run
+outs, plans = [], []
+for w in (W.mlp_hvp(256, 128, 192, 64), W.mlp_hvp(1000, 512, 520, 136)):   # the second ragged
+    r = gpu_run(w.text, w.fn, w.grad, w.inputs(), seed=w.seed(), dot_precision="bf16")
+    outs += r["primal"] + r["grad"]
+    plans.append(r["fn"].print(3))
+np.savez({out!r}, *outs, deferred=np.int64(sum(p.count("deferred epilogue") for p in plans)))
+"""
+
+
+def test_deferred_epilogue_bit_identical_to_fused():
+    """A GEMM epilogue with three or more f32 [M, N] operands (mlp_hvp) runs as
+    an EW step after the GEMM stores its raw accumulator: the same program on
+    the same f32 values, so losses and Hessian-vector products are
+    bit-identical to the fused epilogue (DLVM_EPI_DEFER=0), incl. ragged tiles."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for d in ("0", "1"):
+            out = os.path.join(tmp, f"d{d}.npz")
+            script = _DEFER_SCRIPT.format(root=root, tests=os.path.dirname(os.path.abspath(__file__)), out=out)
+            p = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, DLVM_EPI_DEFER=d),
+                               capture_output=True, text=True, timeout=600)
+            assert p.returncode == 0, p.stderr[-3000:]
+            outs[d] = dict(np.load(out))
+    assert outs["0"]["deferred"] == 0 and outs["1"]["deferred"] >= 2, (outs["0"]["deferred"], outs["1"]["deferred"])
+    for k in outs["0"]:
+        if k != "deferred":
+            np.testing.assert_array_equal(outs["1"][k], outs["0"][k], err_msg=k)
