@@ -357,11 +357,14 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
 // per-thread column pointers advanced by one row stride per step, operands
 // that do not depend on the row (bias / scale vectors, scalars) loaded once,
 // RPI rows loaded before they are computed.  Same arithmetic as ew_kernel.
-// ew2d_kernel's row loop when every row-varying input and every store is
-// f32 with unit column stride (the common case: the planner stores f32 and
-// element-wise inputs are f32): float4 loads and stores through pointers that
-// advance by the row step -- no per-load storage-type dispatch or 64-bit
-// index products.  Same arithmetic as the general loop.
+// ew2d_kernel's row loop when every row-varying input is f32 and every store
+// f32 or bf16, all with unit column stride (the common case: the planner
+// stores f32 or bf16 and element-wise inputs are f32): float4 loads and
+// 16- / 8-byte stores through pointers that advance by the row step -- no
+// per-load storage-type dispatch or 64-bit index products.  Same arithmetic
+// and the same bf16 rounding (f2bf) as the general loop.  (bf16 stores
+// through the general loop ran at 3.2-4.4 TB/s against 5.8-6.7 for f32:
+// tools/ew_inputs_probe.py.)
 template <class P, int RPI, int NI, int NR>
 __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int64_t r0, int by, const bool* rinv,
                                               const float (*inv)[4], float (*acc)[4]) {
@@ -376,12 +379,15 @@ __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int6
     ip[i] = reinterpret_cast<const float*>(p.in[i].ptr) + (rinv[i] ? 0 : r0 * p.in[i].s[0] + c);
     is[i] = rinv[i] ? 0 : (int64_t)by * p.in[i].s[0];
   }
-  float* op[NO];
-  int64_t os[NO];
+  char* op[NO];     // byte pointers: f32 or bf16 rows
+  int64_t os[NO];   // row step in bytes
+  bool ob[NO];      // store s2 is bf16
 #pragma unroll
   for (int s2 = 0; s2 < T::Stores::n; ++s2) {
-    op[s2] = reinterpret_cast<float*>(p.out[s2].ptr) + r0 * p.out[s2].s[0] + c;
-    os[s2] = (int64_t)by * p.out[s2].s[0];
+    ob[s2] = p.out[s2].st == (uint8_t)SType::BF16;
+    const int64_t es = ob[s2] ? 2 : 4;
+    op[s2] = reinterpret_cast<char*>(p.out[s2].ptr) + (r0 * p.out[s2].s[0] + c) * es;
+    os[s2] = (int64_t)by * p.out[s2].s[0] * es;
   }
   for (int k = 0; k < p.rpt; k += RPI) {
     bool ok[RPI];
@@ -415,8 +421,15 @@ __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int6
       for (int u = 0; u < RPI; ++u)
         if (ok[u]) {
           const int sl = T::Stores::at(s2);
-          *reinterpret_cast<float4*>(op[s2] + u * os[s2]) =
-              make_float4(w[sl][u * 4], w[sl][u * 4 + 1], w[sl][u * 4 + 2], w[sl][u * 4 + 3]);
+          if (ob[s2]) {
+            uint2 x;
+            x.x = (unsigned)f2bf(w[sl][u * 4]) | ((unsigned)f2bf(w[sl][u * 4 + 1]) << 16);
+            x.y = (unsigned)f2bf(w[sl][u * 4 + 2]) | ((unsigned)f2bf(w[sl][u * 4 + 3]) << 16);
+            *reinterpret_cast<uint2*>(op[s2] + u * os[s2]) = x;
+          } else {
+            *reinterpret_cast<float4*>(op[s2] + u * os[s2]) =
+                make_float4(w[sl][u * 4], w[sl][u * 4 + 1], w[sl][u * 4 + 2], w[sl][u * 4 + 3]);
+          }
         }
 #pragma unroll
     for (int q = 0; q < T::Reds::n; ++q)
@@ -503,7 +516,8 @@ __global__ void __launch_bounds__(256, MINB) ew2d_kernel(const __grid_constant__
   for (int i = 0; i < T::kIn; ++i)
     f32rows &= rinv[i] || (p.in[i].st == (uint8_t)SType::F32 && p.in[i].s[1] == 1 && p.in[i].nchunks == 1);
 #pragma unroll
-  for (int s2 = 0; s2 < T::Stores::n; ++s2) f32rows &= p.out[s2].st == (uint8_t)SType::F32 && p.out[s2].s[1] == 1;
+  for (int s2 = 0; s2 < T::Stores::n; ++s2)
+    f32rows &= (p.out[s2].st == (uint8_t)SType::F32 || p.out[s2].st == (uint8_t)SType::BF16) && p.out[s2].s[1] == 1;
   if constexpr (VEC == 4) {
     if (cval && f32rows) {
       ew2d_rows_f32<P, RPI, NI, NR>(p, c, r0, by, rinv, inv, acc);

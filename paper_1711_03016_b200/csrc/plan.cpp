@@ -1802,20 +1802,20 @@ struct Planner {
     // the GEMM stores S raw partial tiles and the epilogue program moves to
     // an EW step that sums them in split order (deterministic)
     const int S = split_k(gm);
-    // An epilogue reading three or more f32 [M, N] operands (mlp_hvp's
-    // second-order term %d9: four) cannot stage them through shared memory
-    // (128 KB per operand per 256-wide tile) and loads them row per lane at
-    // a fraction of HBM bandwidth: the GEMM stores its raw accumulator and
-    // the epilogue program runs as the next EW step instead (same program on
-    // the same f32 values: bit-identical; DLVM_EPI_DEFER=0 keeps it fused).
-    // Measured (mlp_hvp, one B200): %d9 286 -> 66 + 187 us; with two such
-    // operands (%o) deferring lost (95 -> 58 + 48 us), hence the threshold
+    // An epilogue reading two or more f32 [M, N] operands (mlp_hvp's
+    // second-order terms %o: two, %d9: four) cannot stage them through
+    // shared memory (128 KB per operand per 256-wide tile) and loads them row
+    // per lane at a fraction of HBM bandwidth: the GEMM stores its raw
+    // accumulator and the epilogue program runs as the next EW step instead
+    // (same program on the same f32 values: bit-identical).  DLVM_EPI_DEFER=n
+    // sets the operand count (0: never).  Measured (mlp_hvp step, one B200):
+    // 1.414 ms fused, 1.326 deferring at 3 operands, 1.318 at 2
     const int heavy = f32_row_inputs(gm.epi);
-    static const bool defer_on = [] {
+    static const int defer_min = [] {  // DLVM_EPI_DEFER=n: the operand count that defers (0: never)
       const char* e = std::getenv("DLVM_EPI_DEFER");
-      return !(e && e[0] == '0');
+      return e ? std::atoi(e) : 2;
     }();
-    const bool defer = S == 1 && defer_on && gm.tensor_core && heavy >= 3;
+    const bool defer = S == 1 && defer_min > 0 && gm.tensor_core && heavy >= defer_min;
     EwGroup split_ew;
     if (S > 1 || defer) {
       split_ew = gm.epi;
