@@ -1815,7 +1815,13 @@ struct Planner {
       const char* e = std::getenv("DLVM_EPI_DEFER");
       return e ? std::atoi(e) : 2;
     }();
-    const bool defer = S == 1 && defer_min > 0 && gm.tensor_core && heavy >= defer_min;
+    // likewise stores whose TMA staging (one 32 x 64 group of each per
+    // epilogue warp: 8 KB f32, 4 KB bf16, 2 KB bytes) exceeds the 12 KB per
+    // warp the pipeline can give up: they would fall back to row-per-lane
+    // stores (mlp_hvp %z: two f32 + two bf16 stores, 24 KB; 367 us fused vs
+    // 200 us for the same GEMM storing only its accumulator)
+    const int stage_kb = store_stage_kb(gm.epi);
+    const bool defer = S == 1 && defer_min > 0 && gm.tensor_core && (heavy >= defer_min || stage_kb > 12);
     EwGroup split_ew;
     if (S > 1 || defer) {
       split_ew = gm.epi;
@@ -1881,7 +1887,9 @@ struct Planner {
       }
     }
     if (S > 1) d << " (K split " << S << ", raw partials; epilogue in the next step)";
-    if (defer) d << " (raw accumulator; epilogue with " << heavy << " f32 [M,N] operands in the next step)";
+    if (defer)
+      d << " (raw accumulator; epilogue with " << heavy << " f32 [M,N] operands, " << stage_kb
+        << " KB of store staging per warp, in the next step)";
     s.desc = d.str();
     gm.epi.desc = s.desc;
     plan.steps.push_back(s);
@@ -1922,6 +1930,17 @@ struct Planner {
       if (plan.bufs[r.buf].st == SType::F32) ++n;
     }
     return n;
+  }
+
+  // TMA store staging per epilogue warp in KB (setup_tma_epilogue): one
+  // 32 x 64 group of every store; caller outputs count as f32
+  int store_stage_kb(const EwGroup& g) const {
+    int kb = 0;
+    for (auto& r : g.stores) {
+      const SType st = r.buf >= 0 ? plan.bufs[r.buf].st : SType::F32;
+      kb += st == SType::F32 ? 8 : st == SType::BF16 ? 4 : 2;
+    }
+    return kb;
   }
 
   static int split_k(const GemmStep& gm) {
