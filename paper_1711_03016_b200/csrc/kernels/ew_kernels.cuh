@@ -365,7 +365,9 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
 // and the same bf16 rounding (f2bf) as the general loop.  (bf16 stores
 // through the general loop ran at 3.2-4.4 TB/s against 5.8-6.7 for f32:
 // tools/ew_inputs_probe.py.)
-template <class P, int RPI, int NI, int NR>
+// BF16: some stores are bf16 (a separate instantiation: the per-store type
+// test costs the all-f32 loop ~17% on c2 fwd+adjoint)
+template <class P, int RPI, int NI, int NR, bool BF16>
 __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int64_t r0, int by, const bool* rinv,
                                               const float (*inv)[4], float (*acc)[4]) {
   using T = spec::Traits<P>;
@@ -384,7 +386,7 @@ __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int6
   bool ob[NO];      // store s2 is bf16
 #pragma unroll
   for (int s2 = 0; s2 < T::Stores::n; ++s2) {
-    ob[s2] = p.out[s2].st == (uint8_t)SType::BF16;
+    ob[s2] = BF16 && p.out[s2].st == (uint8_t)SType::BF16;
     const int64_t es = ob[s2] ? 2 : 4;
     op[s2] = reinterpret_cast<char*>(p.out[s2].ptr) + (r0 * p.out[s2].s[0] + c) * es;
     os[s2] = (int64_t)by * p.out[s2].s[0] * es;
@@ -421,7 +423,7 @@ __device__ __forceinline__ void ew2d_rows_f32(const EwParams& p, int64_t c, int6
       for (int u = 0; u < RPI; ++u)
         if (ok[u]) {
           const int sl = T::Stores::at(s2);
-          if (ob[s2]) {
+          if (BF16 && ob[s2]) {
             uint2 x;
             x.x = (unsigned)f2bf(w[sl][u * 4]) | ((unsigned)f2bf(w[sl][u * 4 + 1]) << 16);
             x.y = (unsigned)f2bf(w[sl][u * 4 + 2]) | ((unsigned)f2bf(w[sl][u * 4 + 3]) << 16);
@@ -511,16 +513,21 @@ __global__ void __launch_bounds__(256, MINB) ew2d_kernel(const __grid_constant__
       }
     }
   };
-  bool f32rows = VEC == 4;
+  bool f32rows = VEC == 4, anybf = false;
 #pragma unroll
   for (int i = 0; i < T::kIn; ++i)
     f32rows &= rinv[i] || (p.in[i].st == (uint8_t)SType::F32 && p.in[i].s[1] == 1 && p.in[i].nchunks == 1);
 #pragma unroll
-  for (int s2 = 0; s2 < T::Stores::n; ++s2)
+  for (int s2 = 0; s2 < T::Stores::n; ++s2) {
     f32rows &= (p.out[s2].st == (uint8_t)SType::F32 || p.out[s2].st == (uint8_t)SType::BF16) && p.out[s2].s[1] == 1;
+    anybf |= p.out[s2].st == (uint8_t)SType::BF16;
+  }
   if constexpr (VEC == 4) {
     if (cval && f32rows) {
-      ew2d_rows_f32<P, RPI, NI, NR>(p, c, r0, by, rinv, inv, acc);
+      if (anybf)
+        ew2d_rows_f32<P, RPI, NI, NR, true>(p, c, r0, by, rinv, inv, acc);
+      else
+        ew2d_rows_f32<P, RPI, NI, NR, false>(p, c, r0, by, rinv, inv, acc);
     }
   }
   if (cval && !f32rows) {
