@@ -154,22 +154,29 @@ def mlp_setup(w, dev, rank):
     return f, dev_in, seed, host, 2 * len(w.layers)
 
 
-def time_steps(step, K, dev, world, group=None):
+def time_steps(step, K, dev, world, group=None, stats=None):
     """K steps bracketed by barrier + synchronize; device time by CUDA events
-    on the current stream; max over ranks.  Returns ms per step."""
+    on the current stream; max over ranks.  Returns ms per step.  An event
+    after every step (a marker: it does not synchronise) gives this rank's
+    per-step times; with `stats` (a dict) their p10 / median / p90 go there
+    (SURVEY 8(d) protocol)."""
     import torch
     import torch.distributed as dist
     st = torch.cuda.current_stream(dev)
     if world > 1:
         dist.barrier(group=group)
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(K):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    ev[0].record(st)
+    for k in range(K):
         step()
-    e1.record(st)
+        ev[k + 1].record(st)
     torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / K
+    ms = ev[0].elapsed_time(ev[K]) / K
+    if stats is not None and K > 0:
+        per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(K))
+        q = lambda f: per[min(K - 1, int(round(f * (K - 1))))]
+        stats.update({"p10": round(q(0.1), 4), "median": round(q(0.5), 4), "p90": round(q(0.9), 4)})
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
@@ -546,7 +553,8 @@ def compact_line(out):
     """The one JSON line: every contract key, and of each sub-measurement
     only its headline numbers (the full records go to the detail file), so
     the line stays short enough for the driver's stdout tail."""
-    line = _pick(out, ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+    line = _pick(out, ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "step_ms",
+                       "higher_is_better",
                        "scaling", "vs_baseline", "dtype", "data", "config", "step_tflops", "gpu_launches", "clocks"])
     line["config"] = _pick(out["config"], ["workload", "global_batch", "per_rank_batch", "parallelism", "l2",
                                            "cuda_graph", "step", "gradient_reduction"])
@@ -759,7 +767,8 @@ def main():
         use_graph = False
     with ClockSampler(local) as clk:
         t0 = time.time()
-        ms = time_steps(step, K, dev, world)
+        step_stats = {}
+        ms = time_steps(step, K, dev, world, stats=step_stats)
         clk.window = (t0, time.time())
     clocks = clk.summary()
     value = w.global_batch / (ms * 1e-3)
@@ -844,7 +853,8 @@ def main():
         if not args.no_e2e_f32 and w.dot_precision == "bf16":
             e2e["f32_inputs"] = e2e_leg(True)
     out = {"metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": K,
-           "warmup": W_, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+           "warmup": W_, "ms_per_step": round(ms, 4), "step_ms": step_stats, "higher_is_better": True,
+           "scaling": "strong",
            "vs_baseline": None, "dtype": "bf16" if w.dot_precision == "bf16" else "f32",
            "data": "synthetic (seeded PCG64 per workloads.py; Glorot weights)",
            "config": {"workload": w.name, "global_batch": w.global_batch, "per_rank_batch": w.batch,
