@@ -777,9 +777,19 @@ def main():
     roof = gemm_roofline(kb, pk, ms * K * 1e-3, clocks)
     tr = ncu_traffic(w.name)
     if tr and roof:
-        roof["traffic"] = tr["traffic_bytes"]
-        roof["traffic_kernel"] = tr["kernel"]
-        roof["traffic_source"] = tr["source"]
+        # the capture of the kernel the roofline names (its %value in the
+        # plan description), else the workload's dominant-kernel capture
+        import re
+        m = re.search(r"(%\w+)", roof["kernel"])
+        per = tr.get("kernels", {}).get(m.group(1)) if m else None
+        if per:
+            roof["traffic"] = per["traffic_bytes"]
+            roof["traffic_kernel"] = m.group(1)
+            roof["traffic_source"] = tr["kernels_source"]
+        else:
+            roof["traffic"] = tr["traffic_bytes"]
+            roof["traffic_kernel"] = tr["kernel"]
+            roof["traffic_source"] = tr["source"]
     step_flops = sum(r["flops"] for r in kb)
     launches = (launched(kb) + (sgd_info["launches"] if sgd_info else 0)) * K
     detail = {"n_gpus": world, "workload": w.name,
