@@ -412,9 +412,18 @@ def cpu_baseline_mlp(w, rows: int):
         dt = time.perf_counter() - t0
         if dt >= 10.0:
             break
-    return {"value": rows * reps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
-            "sample": f"{rows} rows of {w.name} (full {len(w.layers)}-layer weights), {reps} fwd+adjoint pass(es), "
-                      f"float64 numpy ({dt:.2f} s)", **blas_info()}
+    out = {"value": rows * reps / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+           "sample": f"{rows} rows of {w.name} (full {len(w.layers)}-layer weights), {reps} fwd+adjoint pass(es), "
+                     f"float64 numpy ({dt:.2f} s)", **blas_info()}
+    try:  # one pass on one BLAS thread (the 1-thread time beside the all-core one)
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            oracle.run(m, ws.grad, ins)
+            out["one_thread"] = round(rows / (time.perf_counter() - t0), 2)
+    except Exception:  # noqa: BLE001
+        pass
+    return out
 
 
 def cpu_baseline_chain(rows: int, C: int = 16384):
