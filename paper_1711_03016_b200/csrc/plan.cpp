@@ -1821,7 +1821,11 @@ struct Planner {
     // stores (mlp_hvp %z: two f32 + two bf16 stores, 24 KB; 367 us fused vs
     // 200 us for the same GEMM storing only its accumulator)
     const int stage_kb = store_stage_kb(gm.epi);
-    const bool defer = S == 1 && defer_min > 0 && gm.tensor_core && (heavy >= defer_min || stage_kb > 12);
+    // (not epilogues with reductions: the EW kernel sums in another order
+    // than the epilogue's butterflies, so the result would be equal only to
+    // rounding, A17, where the fused and deferred forms are now bit-identical)
+    const bool defer = S == 1 && defer_min > 0 && gm.tensor_core && gm.epi.prog.n_reduces == 0 &&
+                       (heavy >= defer_min || stage_kb > 12);
     EwGroup split_ew;
     if (S > 1 || defer) {
       split_ew = gm.epi;

@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Stress sweep of planner paths on random wide N-d programs (tests/nd_programs.py,
+bf16 policy): for seeds [a, b) runs every program's primal + gradient under
+two settings of an environment switch (default DLVM_EPI_DEFER=0 vs 2) in
+separate processes and checks the outputs bit for bit; prints how many plans
+took the path (the count of `marker` in the printed plans).
+usage: defer_sweep.py a b [VAR v0 v1 marker]"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
+import nd_programs as ND
+from helpers import gpu_run
+outs, n = [], 0
+for seed in range({a}, {b}):
+    kw = dict(wide=True, allow_select=False)
+    text, args = ND.nd_program(np.random.default_rng(9000 + seed), **kw)
+    ins = ND.nd_inputs(np.random.default_rng(99 + seed), args)
+    try:
+        r = gpu_run(text, "f", "g", ins, dot_precision="bf16")
+    except Exception as ex:
+        outs.append(np.array([float(seed)])); print("seed", seed, "error", repr(ex)[:120]); continue
+    outs += r["primal"] + r["grad"]
+    n += r["fn"].print(2).count({marker!r}) + r["fn"].print(3).count({marker!r})
+np.savez({out!r}, *outs, n=np.int64(n))
+"""
+
+
+def main():
+    a, b = int(sys.argv[1]), int(sys.argv[2])
+    var, v0, v1, marker = (sys.argv[3:7] if len(sys.argv) > 6 else ("DLVM_EPI_DEFER", "0", "2", "deferred epilogue"))
+    import numpy as np
+    res = {}
+    for v in (v0, v1):
+        out = f"/tmp/sweep_{v}.npz"
+        p = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT, a=a, b=b, out=out, marker=marker)],
+                           env=dict(os.environ, **{var: v}), capture_output=True, text=True, timeout=3000)
+        if p.returncode:
+            print(p.stderr[-2000:])
+            sys.exit(1)
+        res[v] = dict(np.load(out))
+    bad = [k for k in res[v0] if k != "n" and not np.array_equal(res[v0][k], res[v1][k])]
+    print(f"seeds {a}..{b}: {len(res[v0]) - 1} outputs, {var}={v1} path taken {int(res[v1]['n'])} times "
+          f"({int(res[v0]['n'])} at {v0}); mismatches: {bad[:10]}")
+
+
+if __name__ == "__main__":
+    main()
