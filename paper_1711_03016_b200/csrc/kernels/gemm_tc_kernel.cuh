@@ -1136,8 +1136,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
             tc_fence_after();
             if (t == tile0 && q == 0 && kb == kb_lo) DLVM_GT(P, 3);
             const uint32_t a0 = sA + s * A_STAGE_BYTES, b0 = sB + s * B_STAGE_BYTES;
+            // a K tail (c4 d11: K = 1000 = 15 x 64 + 40): only the 16-wide
+            // steps that hold data; the rest of the zero-filled box would
+            // add exact zeros
+            const int nk16 = kb == num_kb - 1 ? (int)((G.K - (int64_t)kb * BK + 15) / 16) : BK / 16;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
+              if (k >= nk16) break;
               const uint64_t ad = G.a_kmajor ? umma_desc(a0 + 32 * k, 16, 1024) : umma_desc(a0 + 2048 * k, 8192, 1024);
               const uint64_t bd = G.b_kmajor ? umma_desc(b0 + 32 * k, 16, 1024) : umma_desc(b0 + 2048 * k, 8192, 1024);
               if constexpr (CTAS == 2)
