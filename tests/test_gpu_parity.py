@@ -219,6 +219,17 @@ def test_c5_small_tanh_bf16():
     _check_c3(w)
 
 
+@pytest.mark.parametrize("n_ranks", [8, 4])
+def test_c4_per_rank_shard_plans(n_ranks):
+    """The per-rank program c4 runs at N = 4 and 8 GPUs (global batch 65536
+    split in 16384 / 8192 rows, seed 1/65536): other split-K decisions and
+    tile counts than N = 1.  One rank's shard gradients against the float64
+    oracle on the same rows (A18' vs the bf16-policy oracle; the last layer's
+    dW, db and the loss also A18 vs the unrounded one); summing the shards
+    over ranks is the linearity F15 pinned on CPU."""
+    _check_c3(W.c4(n_ranks))
+
+
 def test_c5_full_width_reduced_batch():
     """c5 with its full weights (8 tanh layers of 8192 x 8192, SURVEY 8(d):
     "full weights, batch reduced to 256 rows") against the float64 oracle:
