@@ -1343,8 +1343,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) gemm_tc_kernel(const __grid_co
         const int64_t n0 = (int64_t)tn * BN + ch * CW;
         return mval && row_vec && n0 + CW <= g.N;
       };
-      // warp h takes every other 16-column block (chunks of CW < 16 walk a
-      // block in order), so which warp sums which columns -- and with
+      // warp h takes every other 64-column block (its GCH chunks of CW
+      // columns in order), so which warp sums which columns -- and with
       // element-by-element row/full sums the whole summation order -- does
       // not depend on the chunk width: a kept loss computed by the gradient's
       // epilogue equals the primal's bit for bit (reading A20) even when the
