@@ -4,7 +4,7 @@ bf16 policy): for seeds [a, b) runs every program's primal + gradient under
 two settings of an environment switch (default DLVM_EPI_DEFER=0 vs 2) in
 separate processes and checks the outputs bit for bit; prints how many plans
 took the path (the count of `marker` in the printed plans).
-usage: defer_sweep.py a b [VAR v0 v1 marker]"""
+usage: [SWEEP_PREC=f32] defer_sweep.py a b [VAR v0 v1 marker]"""
 import os
 import subprocess
 import sys
@@ -18,11 +18,11 @@ import nd_programs as ND
 from helpers import gpu_run
 outs, n, owner = [], 0, []
 for seed in range({a}, {b}):
-    kw = dict(wide=True, allow_select=False)
+    kw = dict(wide=True, allow_select={prec!r} == "f32")
     text, args = ND.nd_program(np.random.default_rng(9000 + seed), **kw)
     ins = ND.nd_inputs(np.random.default_rng(99 + seed), args)
     try:
-        r = gpu_run(text, "f", "g", ins, dot_precision="bf16")
+        r = gpu_run(text, "f", "g", ins, dot_precision={prec!r})
     except Exception as ex:
         outs.append(np.array([float(seed)])); owner.append(seed); print("seed", seed, "error", repr(ex)[:120]); continue
     outs += r["primal"] + r["grad"]
@@ -39,7 +39,8 @@ def main():
     res = {}
     for v in (v0, v1):
         out = f"/tmp/sweep_{v}.npz"
-        p = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT, a=a, b=b, out=out, marker=marker)],
+        prec = os.environ.get("SWEEP_PREC", "bf16")  # f32: the SIMT dot path (and selects in the programs)
+        p = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT, a=a, b=b, out=out, marker=marker, prec=prec)],
                            env=dict(os.environ, **{var: v}), capture_output=True, text=True, timeout=3000)
         if p.returncode:
             print(p.stderr[-2000:])
