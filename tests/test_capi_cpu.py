@@ -635,3 +635,24 @@ def test_two_stream_schedule_of_c3_gradient():
     assert any("%d18" in l and "wait[" in l for l in aux), s
     assert any("main" in l and "%d20" in l and "wait[" in l for l in lines), s
     assert f.print(11).startswith("streams: one")
+
+
+def test_deferred_epilogues_and_split_reduce_add_plans():
+    """Plan-time choices of round 2, pinned per benchmarked config: only
+    mlp_hvp defers GEMM epilogues (%z: 24 KB of store staging per warp; %o,
+    %d9: two and four f32 [M,N] operands; none has reductions), and only the
+    K-split-in-two dW GEMMs with store-only epilogues (c4's %d20 / %d25,
+    mlp_hvp's %d45) may add into an f32 home instead of running their sum
+    step."""
+    import re
+    expect = {"mlp_hvp": (["%z", "%o", "%d9"], 1), "c4_mlp": ([], 2), "c3_mlp": ([], 0), "c5_mlp": ([], 0),
+              "rnn": ([], 0)}
+    for w in (W.mlp_hvp(), W.c4(), W.c3(), W.c5(), W.rnn()):
+        t = _plan_only(w.text, w.fn, w.grad, "bf16").print(3)
+        deferred = [re.search(r"%\w+", l).group(0) for l in t.splitlines() if "raw accumulator" in l]
+        assert (deferred, t.count("skipped when the home is bound as f32")) == expect[w.name], (w.name, deferred)
+        # every deferred GEMM is followed by its epilogue step, and that step has no reductions
+        lines = t.splitlines()
+        for i, l in enumerate(lines):
+            if "raw accumulator" in l:
+                assert "deferred epilogue" in lines[i + 1] and "reductions=0" in lines[i + 1], lines[i + 1]
